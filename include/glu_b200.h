@@ -1,0 +1,181 @@
+/*
+ * glu_b200.h -- C ABI of the B200-native GLU3.0 numeric-factorization path.
+ *
+ * Drop-in boundary for the reference package `levlu` 0.1.0.  Every entry
+ * point names the reference interface it replaces (file:line relative to
+ * /root/reference/pkg/src/levlu).  Plain pointers and sizes only: indices
+ * are int64 (as the reference stores them, sparse.py:61-62), values fp64.
+ * The caller owns every host buffer; device buffers are owned by the
+ * handle, except the `*_device` calls, which operate on caller-owned device
+ * memory (e.g. torch tensors) on the caller's stream.
+ *
+ * Status codes follow the reference kernels' return convention
+ * (_kernels.py:30-34, :114, :147 and numeric.py:110-126):
+ *     GLU_OK (-1)         success
+ *     >= 0                failing pivot column  -> PivotError(column)
+ *     GLU_MISMATCH (-2)   structurally absent slot -> PatternMismatchError
+ *     GLU_ECUDA (-3)      CUDA runtime error (message: glu_last_error)
+ *     GLU_EINVAL (-4)     invalid argument      (message: glu_last_error)
+ *     GLU_ESTRUCT (-5)    structural error      -> SymbolicError
+ * Threading: one handle per host thread / stream; distinct handles are
+ * independent.  No C++ exception crosses this boundary.
+ */
+#ifndef GLU_B200_H
+#define GLU_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GLU_OK (-1)
+#define GLU_MISMATCH (-2)
+#define GLU_ECUDA (-3)
+#define GLU_EINVAL (-4)
+#define GLU_ESTRUCT (-5)
+
+#define GLU_CONTRACT_A 0 /* ascending-source MAC order: factor_left_looking,
+                            factor_right_looking_seq, factor_parallel(deterministic=True) */
+#define GLU_CONTRACT_B 1 /* level-major MAC order: factor_parallel(deterministic=False) */
+
+typedef struct glu_pattern glu_pattern; /* filled pattern (host) */
+typedef struct glu_plan glu_plan;       /* per-level update plan (host) */
+typedef struct glu_handle glu_handle;   /* device-resident pattern + plan */
+
+/* Last error message of the calling thread. Returns its length. */
+int64_t glu_last_error(char *buf, int64_t len);
+/* Library version / build string (sm_100a). */
+const char *glu_version(void);
+
+/* ---- host analysis (computed once per pattern) ------------------------ */
+
+/* symbolic.py:92-145 symbolic_fillin + sparse.py:267-278 make_csr_view.
+   Returns GLU_OK, or GLU_ESTRUCT with *bad_col set and *bad_kind = 1 (empty
+   column, symbolic.py:122) or 2 (missing diagonal, symbolic.py:124-125). */
+int64_t glu_symbolic_fillin(int64_t n, const int64_t *a_col_ptr, const int64_t *a_row_idx,
+                            int32_t inject_diagonal, glu_pattern **out, int64_t *injected,
+                            int64_t *bad_col, int32_t *bad_kind);
+int64_t glu_pattern_nnz(const glu_pattern *p);
+/* Copies the pattern out: col_ptr[n+1], row_idx[nnz], diag_pos[n],
+   row_ptr[n+1], col_idx[nnz], csc_pos[nnz] (CsrView, sparse.py:121-138). */
+void glu_pattern_export(const glu_pattern *p, int64_t *col_ptr, int64_t *row_idx,
+                        int64_t *diag_pos, int64_t *row_ptr, int64_t *col_idx,
+                        int64_t *csc_pos);
+void glu_pattern_free(glu_pattern *p);
+
+/* sparse.py:267-278 make_csr_view (stable: ascending columns per row). */
+int64_t glu_csr_view(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                     int64_t *row_ptr, int64_t *col_idx, int64_t *csc_pos);
+
+/* depgraph.py:96-126 detect_relaxed.  dep_idx must hold nnz entries (an
+   upper bound).  Returns the edge count; deps of column k are
+   dep_idx[dep_ptr[k]:dep_ptr[k+1]], sorted ascending, unique. */
+int64_t glu_detect_relaxed(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                           const int64_t *diag_pos, const int64_t *row_ptr,
+                           const int64_t *col_idx, int64_t *dep_ptr, int64_t *dep_idx);
+/* depgraph.py:96-110 detect_upward (same output convention). */
+int64_t glu_detect_upward(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                          const int64_t *diag_pos, int64_t *dep_ptr, int64_t *dep_idx);
+
+/* depgraph.py:159-170 levelize.  Returns the level count; level_cols lists
+   the columns level by level, ascending within each level. */
+int64_t glu_levelize(int64_t n, const int64_t *dep_ptr, const int64_t *dep_idx,
+                     int64_t *level_of, int64_t *level_ptr, int64_t *level_cols);
+
+/* _kernels.py:15-34 scatter_values on the host (reference semantics):
+   returns GLU_OK or the first column of A with entries outside the
+   filled pattern. */
+int64_t glu_scatter_values(int64_t n, const int64_t *a_col_ptr, const int64_t *a_row_idx,
+                           const double *a_vals, const int64_t *f_col_ptr,
+                           const int64_t *f_row_idx, double *out);
+
+/* depgraph.py:173-205 simulate_hazards, evaluated in O(MACs): same-level
+   write/read conflicts of the right-looking updates under level_of.
+   Writes up to max_out rows {level, writer, reader, i, k} sorted by
+   (level, writer, reader, element); returns the total found. */
+int64_t glu_find_hazards(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                         const int64_t *diag_pos, const int64_t *row_ptr, const int64_t *col_idx,
+                         const int64_t *level_of, int64_t max_out, int64_t *out);
+
+/* ---- update plan: the precomputed scatter schedule -------------------- */
+
+/* Builds the destination-owned update plan for the given level schedule.
+   contract: GLU_CONTRACT_A or GLU_CONTRACT_B.  max_item_macs bounds the
+   MACs one warp task carries (0 = default).  Returns GLU_OK or
+   GLU_MISMATCH when an update targets a slot absent from the pattern
+   (the condition _kernels.py:113-114 reports at run time). */
+int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                       const int64_t *diag_pos, const int64_t *level_of, int32_t contract,
+                       int64_t max_item_macs, int32_t n_threads, glu_plan **out);
+/* info[0..7] = n_levels, n_items, n_chunks, n_map (= MACs), max_item_macs,
+   max_chunks_per_item, deferred_macs (contract A), plan bytes */
+void glu_plan_info(const glu_plan *p, int64_t *info);
+/* level_item_ptr[n_levels+1]; items[n_items*6] = {map_off, base, span, c0, c1, macs};
+   chunks[n_chunks*4] = {m, d, p0, cnt}  (all slots absolute). */
+void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
+                     int64_t *chunks);
+void glu_plan_free(glu_plan *p);
+
+/* ---- device handle ---------------------------------------------------- */
+
+/* Uploads pattern, level schedule and plan to the current CUDA device and
+   builds the uint16 scatter map on the device.  Replaces the per-call
+   setup of numeric.py:241-317 (caps, workspaces, crew). */
+int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                   const int64_t *diag_pos, const int64_t *row_ptr, const int64_t *col_idx,
+                   const int64_t *csc_pos, const int64_t *level_of, const glu_plan *plan,
+                   glu_handle **out);
+void glu_destroy(glu_handle *h);
+/* Options: key 1 = record per-level GPU timestamps (value 0/1; read with
+   glu_level_times, FactorStats.level_times, numeric.py:321-327); key 2 =
+   failing-pivot order: 0 = earliest level then min column (factor_parallel,
+   numeric.py:279-285), 1 = min column (sequential paths, numeric.py:129-159). */
+int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value);
+/* Per-level milliseconds of the last timed factorization; returns count. */
+int64_t glu_level_times(const glu_handle *h, double *ms, int64_t len);
+/* info[0..11]: n, nnz, n_levels, n_items, n_chunks, macs, device bytes,
+   grid CTAs, threads/CTA, lsolve levels, usolve levels, sm count */
+void glu_handle_info(const glu_handle *h, int64_t *info);
+
+/* A -> A_s slot map for device-side scatter (_kernels.py:15-34). Returns
+   GLU_OK or the first column of A with entries outside the pattern. */
+int64_t glu_set_input_pattern(glu_handle *h, int64_t nz, const int64_t *a_col_ptr,
+                              const int64_t *a_row_idx);
+
+/* Device-side scatter: v[nnz] = 0; v[slot(e)] = a_vals[e].  Device ptrs. */
+int64_t glu_scatter_device(glu_handle *h, const double *a_vals, double *v, void *stream);
+
+/* Numeric factorization in place over device A_s-slot values (numeric.py:
+   241-351 level loop + _kernels.py:119-173).  Returns GLU_OK, the failing
+   pivot column (min column of the earliest failing level), or an error.
+   Per-level GPU times are recorded when
+   enabled with glu_set_option(h, 1, 1). */
+int64_t glu_factor_device(glu_handle *h, double *v, double thresh, void *stream);
+
+/* Asynchronous launch (no host synchronization, for timing loops) and the
+   status read that completes it. */
+int64_t glu_factor_device_async(glu_handle *h, double *v, double thresh, void *stream);
+int64_t glu_factor_status(glu_handle *h, void *stream);
+
+/* Batch refactorization: `batch` value sets stored batch-minor
+   (v[slot*batch + b]) on the device; fail_cols (host, batch) receives
+   GLU_OK or the failing column per matrix. */
+int64_t glu_factor_batch_device(glu_handle *h, int64_t batch, double *v, double thresh,
+                                int64_t *fail_cols, void *stream);
+
+/* numeric.py:354-378 solve: x (device, n) holds b on entry, x on exit.
+   lu (device) are factor values. Returns GLU_OK or the column of a zero
+   U diagonal (_kernels.py:190-191). */
+int64_t glu_solve_device(glu_handle *h, const double *lu, double *x, void *stream);
+int64_t glu_lower_solve_device(glu_handle *h, const double *lu, double *x, void *stream);
+int64_t glu_upper_solve_device(glu_handle *h, const double *lu, double *x, void *stream);
+
+/* End-to-end host-buffer calls (the reference-facing plugin boundary):
+   H2D of A values, device scatter, factor, D2H of LU. */
+int64_t glu_factor_host(glu_handle *h, const double *a_vals, double *lu_out, double thresh);
+int64_t glu_solve_host(glu_handle *h, const double *lu, const double *b, double *x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,662 @@
+// glu_host.cpp -- host side of the B200 GLU3.0 path: symbolic fill-in,
+// relaxed dependency detection, levelization, and the precomputed
+// destination-owned update plan that the persistent sm_100a kernel walks.
+//
+// Everything here runs once per sparsity pattern.  The pattern, the
+// dependency lists and the levels are uniquely determined by the input
+// pattern, so any correct algorithm reproduces the reference's arrays
+// bit for bit; parity is checked against the reference's own outputs in
+// tests/test_analysis.py.
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "glu_b200.h"
+#include "glu_internal.h"
+
+namespace glu {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string &s) { g_last_error = s; }
+
+}  // namespace glu
+
+using glu::set_error;
+using i64 = int64_t;
+using i32 = int32_t;
+
+extern "C" int64_t glu_last_error(char *buf, int64_t len) {
+    const std::string &e = glu::g_last_error;
+    if (buf && len > 0) {
+        size_t m = std::min<size_t>((size_t)len - 1, e.size());
+        std::memcpy(buf, e.data(), m);
+        buf[m] = 0;
+    }
+    return (int64_t)e.size();
+}
+
+// ---------------------------------------------------------------------------
+// Symbolic fill-in (symbolic.py:92-145).  Column j's filled pattern is the
+// set of rows reachable from A(:,j) through the L columns left of j.  We use
+// the Gilbert-Peierls DFS of symbolic.py:66-89 plus Eisenstat-Liu symmetric
+// pruning: once column s is known, any column k < s with both L(s,k) and
+// U(k,s) nonzero only needs its L rows <= s for later reachability (rows
+// below s of L(:,k) are contained in L(:,s)).  Pruning changes the
+// traversal cost only, never the reach set.
+// ---------------------------------------------------------------------------
+struct glu_pattern {
+    i64 n = 0;
+    std::vector<i64> col_ptr, row_idx, diag_pos, row_ptr, col_idx, csc_pos;
+};
+
+static void build_csr(i64 n, const i64 *col_ptr, const i64 *row_idx, i64 *row_ptr, i64 *col_idx,
+                      i64 *csc_pos) {
+    i64 nnz = col_ptr[n];
+    std::fill(row_ptr, row_ptr + n + 1, 0);
+    for (i64 p = 0; p < nnz; p++) row_ptr[row_idx[p] + 1]++;
+    for (i64 i = 0; i < n; i++) row_ptr[i + 1] += row_ptr[i];
+    std::vector<i64> fill(row_ptr, row_ptr + n);
+    // columns visited in ascending order => ascending columns within each row
+    // (the stable argsort of sparse.py:275-277)
+    for (i64 j = 0; j < n; j++) {
+        for (i64 p = col_ptr[j]; p < col_ptr[j + 1]; p++) {
+            i64 t = fill[row_idx[p]]++;
+            col_idx[t] = j;
+            csc_pos[t] = p;
+        }
+    }
+}
+
+extern "C" int64_t glu_csr_view(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                int64_t *row_ptr, int64_t *col_idx, int64_t *csc_pos) {
+    if (n < 0) { set_error("n < 0"); return GLU_EINVAL; }
+    build_csr(n, col_ptr, row_idx, row_ptr, col_idx, csc_pos);
+    return GLU_OK;
+}
+
+extern "C" int64_t glu_symbolic_fillin(int64_t n, const int64_t *a_col_ptr,
+                                       const int64_t *a_row_idx, int32_t inject_diagonal,
+                                       glu_pattern **out, int64_t *injected, int64_t *bad_col,
+                                       int32_t *bad_kind) {
+    *out = nullptr;
+    *injected = 0;
+    *bad_col = -1;
+    *bad_kind = 0;
+    if (n < 0) { set_error("n < 0"); return GLU_EINVAL; }
+    auto *pat = new glu_pattern();
+    pat->n = n;
+    pat->col_ptr.assign(n + 1, 0);
+    pat->diag_pos.assign(n, 0);
+    std::vector<i64> &rows = pat->row_idx;
+    rows.reserve((size_t)std::max<i64>(2 * a_col_ptr[n], 16));
+    std::vector<i64> visited(n, -1), stack, scratch, arow;
+    std::vector<i64> l_lo(n, 0), l_hi(n, 0);  // traversal range of L(:,k) (pruned)
+    std::vector<char> pruned(n, 0);
+    stack.reserve(n);
+    scratch.reserve(n);
+    for (i64 j = 0; j < n; j++) {
+        i64 alo = a_col_ptr[j], ahi = a_col_ptr[j + 1];
+        if (ahi == alo) {
+            *bad_col = j; *bad_kind = 1;
+            set_error("column " + std::to_string(j) + " is structurally empty (singular)");
+            delete pat;
+            return GLU_ESTRUCT;
+        }
+        arow.assign(a_row_idx + alo, a_row_idx + ahi);
+        if (std::find(arow.begin(), arow.end(), j) == arow.end()) {
+            if (!inject_diagonal) {
+                *bad_col = j; *bad_kind = 2;
+                set_error("structural diagonal missing in column " + std::to_string(j));
+                delete pat;
+                return GLU_ESTRUCT;
+            }
+            (*injected)++;
+            arow.push_back(j);
+        }
+        scratch.clear();
+        for (i64 r : arow) {
+            if (visited[r] == j) continue;
+            visited[r] = j;
+            stack.clear();
+            stack.push_back(r);
+            while (!stack.empty()) {
+                i64 k = stack.back();
+                stack.pop_back();
+                scratch.push_back(k);
+                if (k < j) {
+                    for (i64 q = l_lo[k]; q < l_hi[k]; q++) {
+                        i64 i = rows[q];
+                        if (visited[i] != j) {
+                            visited[i] = j;
+                            stack.push_back(i);
+                        }
+                    }
+                }
+            }
+        }
+        std::sort(scratch.begin(), scratch.end());
+        i64 start = (i64)rows.size();
+        rows.insert(rows.end(), scratch.begin(), scratch.end());
+        i64 end = (i64)rows.size();
+        pat->col_ptr[j + 1] = end;
+        i64 d = start + (i64)(std::lower_bound(scratch.begin(), scratch.end(), j) - scratch.begin());
+        pat->diag_pos[j] = d;
+        l_lo[j] = d + 1;
+        l_hi[j] = end;
+        // symmetric pruning with s = j: for every U(k,j) != 0 (k < j) whose
+        // L(:,k) contains row j, keep only L(:,k) rows <= j for traversal.
+        for (i64 p = start; p < d; p++) {
+            i64 k = rows[p];
+            if (pruned[k]) continue;
+            const i64 *b = rows.data() + l_lo[k], *e = rows.data() + l_hi[k];
+            const i64 *it = std::lower_bound(b, e, j);
+            if (it != e && *it == j) {
+                l_hi[k] = (i64)(it - rows.data()) + 1;
+                pruned[k] = 1;
+            }
+        }
+    }
+    rows.shrink_to_fit();
+    i64 nnz = (i64)rows.size();
+    pat->row_ptr.resize(n + 1);
+    pat->col_idx.resize(nnz);
+    pat->csc_pos.resize(nnz);
+    build_csr(n, pat->col_ptr.data(), rows.data(), pat->row_ptr.data(), pat->col_idx.data(),
+              pat->csc_pos.data());
+    *out = pat;
+    return GLU_OK;
+}
+
+extern "C" int64_t glu_pattern_nnz(const glu_pattern *p) { return p ? (int64_t)p->row_idx.size() : 0; }
+
+extern "C" void glu_pattern_export(const glu_pattern *p, int64_t *col_ptr, int64_t *row_idx,
+                                   int64_t *diag_pos, int64_t *row_ptr, int64_t *col_idx,
+                                   int64_t *csc_pos) {
+    auto cp = [](const std::vector<i64> &v, int64_t *dst) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(i64));
+    };
+    cp(p->col_ptr, col_ptr);
+    cp(p->row_idx, row_idx);
+    cp(p->diag_pos, diag_pos);
+    cp(p->row_ptr, row_ptr);
+    cp(p->col_idx, col_idx);
+    cp(p->csc_pos, csc_pos);
+}
+
+extern "C" void glu_pattern_free(glu_pattern *p) { delete p; }
+
+// ---------------------------------------------------------------------------
+// Dependency detection (depgraph.py:96-126) and levelization
+// (depgraph.py:159-170).  Column k depends on
+//   upward:  every i < k with U(i,k) != 0 and a non-empty L(:,i)
+//   relaxed: upward  U  every i < k with L(k,i) != 0 (row k left of diag)
+// Both sources are ascending lists, so a merge yields the sorted unique
+// list that np.unique produces in the reference.
+// ---------------------------------------------------------------------------
+extern "C" int64_t glu_detect_relaxed(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                      const int64_t *diag_pos, const int64_t *row_ptr,
+                                      const int64_t *col_idx, int64_t *dep_ptr,
+                                      int64_t *dep_idx) {
+    i64 e = 0;
+    dep_ptr[0] = 0;
+    for (i64 k = 0; k < n; k++) {
+        i64 a = col_ptr[k], ae = diag_pos[k];        // U rows of column k (ascending)
+        i64 b = row_ptr[k], be = row_ptr[k + 1];      // row k columns (ascending)
+        while (true) {
+            // skip U rows whose L column is empty
+            while (a < ae && !(col_ptr[row_idx[a] + 1] - diag_pos[row_idx[a]] > 1)) a++;
+            bool ha = a < ae;
+            bool hb = b < be && col_idx[b] < k;
+            if (!ha && !hb) break;
+            i64 x;
+            if (ha && (!hb || row_idx[a] <= col_idx[b])) {
+                x = row_idx[a];
+                if (hb && col_idx[b] == x) b++;
+                a++;
+            } else {
+                x = col_idx[b];
+                b++;
+            }
+            dep_idx[e++] = x;
+        }
+        dep_ptr[k + 1] = e;
+    }
+    return e;
+}
+
+extern "C" int64_t glu_detect_upward(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                     const int64_t *diag_pos, int64_t *dep_ptr, int64_t *dep_idx) {
+    i64 e = 0;
+    dep_ptr[0] = 0;
+    for (i64 k = 0; k < n; k++) {
+        for (i64 p = col_ptr[k]; p < diag_pos[k]; p++) {
+            i64 i = row_idx[p];
+            if (col_ptr[i + 1] - diag_pos[i] > 1) dep_idx[e++] = i;
+        }
+        dep_ptr[k + 1] = e;
+    }
+    return e;
+}
+
+extern "C" int64_t glu_levelize(int64_t n, const int64_t *dep_ptr, const int64_t *dep_idx,
+                                int64_t *level_of, int64_t *level_ptr, int64_t *level_cols) {
+    i64 nl = 0;
+    for (i64 j = 0; j < n; j++) {
+        i64 lv = 0;
+        for (i64 t = dep_ptr[j]; t < dep_ptr[j + 1]; t++) lv = std::max(lv, level_of[dep_idx[t]] + 1);
+        level_of[j] = lv;
+        nl = std::max(nl, lv + 1);
+    }
+    if (n == 0) nl = 0;
+    std::fill(level_ptr, level_ptr + nl + 1, 0);
+    for (i64 j = 0; j < n; j++) level_ptr[level_of[j] + 1]++;
+    for (i64 l = 0; l < nl; l++) level_ptr[l + 1] += level_ptr[l];
+    std::vector<i64> fill(level_ptr, level_ptr + std::max<i64>(nl, 1));
+    for (i64 j = 0; j < n; j++) level_cols[fill[level_of[j]]++] = j;  // ascending within level
+    return nl;
+}
+
+extern "C" int64_t glu_scatter_values(int64_t n, const int64_t *a_col_ptr,
+                                      const int64_t *a_row_idx, const double *a_vals,
+                                      const int64_t *f_col_ptr, const int64_t *f_row_idx,
+                                      double *out) {
+    std::fill(out, out + f_col_ptr[n], 0.0);
+    for (i64 j = 0; j < n; j++) {
+        i64 q = f_col_ptr[j], hi = f_col_ptr[j + 1];
+        for (i64 p = a_col_ptr[j]; p < a_col_ptr[j + 1]; p++) {
+            i64 r = a_row_idx[p];
+            while (q < hi && f_row_idx[q] < r) q++;
+            if (q >= hi || f_row_idx[q] != r) return j;
+            out[q] = a_vals[p];
+            q++;
+        }
+    }
+    return GLU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Schedule hazards (the condition depgraph.py:173-205 simulates): in one
+// level, writer w updates (i,k) for i in L(:,w), k in subcolumns(w); a
+// same-level column r reads (r,k') for k' > r and (i',r) for i' > r.  So
+// (i,k) is a hazard against reader i when level(i) == level(w) and k > i,
+// and against reader k when level(k) == level(w) and i > k.  Output rows
+// {level, writer, reader, i, k}, sorted like the reference's report.
+// ---------------------------------------------------------------------------
+extern "C" int64_t glu_find_hazards(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                    const int64_t *diag_pos, const int64_t *row_ptr,
+                                    const int64_t *col_idx, const int64_t *level_of,
+                                    int64_t max_out, int64_t *out) {
+    struct H { i64 l, w, r, i, k; };
+    std::vector<H> hz;
+    for (i64 w = 0; w < n; w++) {
+        const i64 lw = level_of[w];
+        for (i64 t = row_ptr[w]; t < row_ptr[w + 1]; t++) {
+            const i64 k = col_idx[t];
+            if (k <= w) continue;
+            for (i64 p = diag_pos[w] + 1; p < col_ptr[w + 1]; p++) {
+                const i64 i = row_idx[p];
+                if (level_of[i] == lw && k > i) hz.push_back({lw, w, i, i, k});
+                if (level_of[k] == lw && i > k) hz.push_back({lw, w, k, i, k});
+                if ((i64)hz.size() > 4 * std::max<i64>(max_out, 1) + 1000000) goto sort;
+            }
+        }
+    }
+sort:
+    std::sort(hz.begin(), hz.end(), [](const H &a, const H &b) {
+        if (a.l != b.l) return a.l < b.l;
+        if (a.w != b.w) return a.w < b.w;
+        if (a.r != b.r) return a.r < b.r;
+        if (a.i != b.i) return a.i < b.i;
+        return a.k < b.k;
+    });
+    const i64 m = std::min<i64>(max_out, (i64)hz.size());
+    for (i64 x = 0; x < m; x++) {
+        out[5 * x + 0] = hz[x].l; out[5 * x + 1] = hz[x].w; out[5 * x + 2] = hz[x].r;
+        out[5 * x + 3] = hz[x].i; out[5 * x + 4] = hz[x].k;
+    }
+    return (i64)hz.size();
+}
+
+// ---------------------------------------------------------------------------
+// Update plan.
+//
+// Right-looking GLU3.0 (paper Alg. 2, _kernels.py:119-149) applies, for
+// every source column j and every subcolumn k (U(j,k) != 0, k > j), the
+// MACs  A_s(i,k) -= (A_s(i,j) / A_s(j,j)) * A_s(j,k)  for i in L(:,j).
+// The plan fixes, for every target slot, the order of its MACs:
+//
+//   contract B  every MAC of source j runs in the phase of level(j); inside
+//               a phase a target receives its MACs in ascending j.  This is
+//               factor_parallel(deterministic=False) bit for bit.
+//   contract A  a MAC (j -> (i,k)) runs in phase max{level(j') : j' <= j a
+//               source of (i,k)}, so each target receives its MACs in
+//               ascending j overall: left-looking order, i.e.
+//               factor_left_looking / factor_right_looking_seq /
+//               factor_parallel(deterministic=True) bit for bit.  Deferring
+//               a MAC past level(j) is safe: every consumer of (i,k) sits in
+//               a level above all of its sources (relaxed dependencies).
+//
+// Values are never divided in place during the phases (the division runs on
+// the fly inside each MAC, exactly as push_updates_owned does), so deferred
+// MACs read the same undivided L values; one final pass pivot-checks and
+// divides every column.
+//
+// Work unit ("item"): one destination column segment in one phase, with its
+// ordered list of "chunks" (contiguous runs of one source's L entries).  One
+// warp owns an item, so ordering needs no atomics.  Segments bound the MACs
+// per item (hub columns split over many warps) and keep the target offsets
+// of an item within uint16 range of its base slot.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct RawChunk {
+    i32 lvl;
+    i32 m, d, p0, cnt;
+};
+
+struct LocalItem {
+    i32 lvl;
+    i32 k;
+    i64 base;    // absolute slot of the segment start
+    i32 span;    // positions covered
+    i64 macs;
+    i64 c0, c1;  // chunk range in the thread-local chunk vector
+};
+
+struct ThreadOut {
+    std::vector<LocalItem> items;
+    std::vector<RawChunk> chunks;
+    i64 deferred = 0;
+    bool mismatch = false;
+    i64 mismatch_col = -1;
+};
+
+}  // namespace
+
+struct glu_plan {
+    i64 n_levels = 0;
+    std::vector<i64> level_item_ptr;
+    std::vector<glu::Item> items;
+    std::vector<glu::Chunk> chunks;
+    i64 n_map = 0;
+    i64 max_item_macs = 0;
+    i64 max_chunks = 0;
+    i64 deferred = 0;
+};
+
+static constexpr i64 kMaxSpan = 65535;
+
+extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                  const int64_t *diag_pos, const int64_t *level_of,
+                                  int32_t contract, int64_t max_item_macs, int32_t n_threads,
+                                  glu_plan **out) {
+    *out = nullptr;
+    if (contract != GLU_CONTRACT_A && contract != GLU_CONTRACT_B) {
+        set_error("contract must be GLU_CONTRACT_A or GLU_CONTRACT_B");
+        return GLU_EINVAL;
+    }
+    if (col_ptr[n] >= (int64_t)INT32_MAX) {
+        set_error("pattern has >= 2^31 entries; slot indices are int32 on the device");
+        return GLU_EINVAL;
+    }
+    const i64 T = max_item_macs > 0 ? max_item_macs : 1024;
+    i64 n_levels = 0;
+    for (i64 j = 0; j < n; j++) n_levels = std::max(n_levels, level_of[j] + 1);
+    int nt = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    nt = (int)std::min<i64>(nt, std::max<i64>(1, n / 64));
+    std::vector<ThreadOut> outs(nt);
+    std::atomic<i64> next{0};
+    const i64 block = 256;
+
+    auto worker = [&](int tid) {
+        ThreadOut &o = outs[tid];
+        std::vector<i32> posmap(n, -1);
+        std::vector<i32> runmax;   // contract A: running max level per position
+        std::vector<i64> hist;     // MACs per position for segmentation
+        std::vector<RawChunk> raw;
+        std::vector<i32> lvl_of_entry;
+        std::vector<i64> order;
+        while (true) {
+            i64 k0 = next.fetch_add(block);
+            if (k0 >= n) break;
+            i64 k1 = std::min<i64>(n, k0 + block);
+            for (i64 k = k0; k < k1; k++) {
+                i64 cb = col_ptr[k], ce = col_ptr[k + 1], len = ce - cb;
+                raw.clear();
+                bool any = false;
+                for (i64 m = cb; m < diag_pos[k]; m++) {
+                    i64 j = row_idx[m];
+                    if (col_ptr[j + 1] - diag_pos[j] > 1) { any = true; break; }
+                }
+                if (!any) continue;
+                for (i64 t = 0; t < len; t++) posmap[row_idx[cb + t]] = (i32)t;
+                if (contract == GLU_CONTRACT_A) runmax.assign(len, -1);
+                bool bad = false;
+                for (i64 m = cb; m < diag_pos[k] && !bad; m++) {
+                    i64 j = row_idx[m];
+                    i64 lo = diag_pos[j] + 1, hi = col_ptr[j + 1];
+                    if (lo >= hi) continue;
+                    i32 lj = (i32)level_of[j];
+                    if (contract == GLU_CONTRACT_B) {
+                        for (i64 p = lo; p < hi; p++)
+                            if (posmap[row_idx[p]] < 0) { bad = true; break; }
+                        raw.push_back({lj, (i32)m, (i32)diag_pos[j], (i32)lo, (i32)(hi - lo)});
+                    } else {
+                        i64 run0 = lo;
+                        i32 run_l = -1;
+                        for (i64 p = lo; p < hi; p++) {
+                            i32 pos = posmap[row_idx[p]];
+                            if (pos < 0) { bad = true; break; }
+                            i32 l = std::max(runmax[pos], lj);
+                            runmax[pos] = l;
+                            if (l != lj) o.deferred++;
+                            if (p == lo) run_l = l;
+                            else if (l != run_l) {
+                                raw.push_back({run_l, (i32)m, (i32)diag_pos[j], (i32)run0, (i32)(p - run0)});
+                                run0 = p;
+                                run_l = l;
+                            }
+                        }
+                        if (!bad)
+                            raw.push_back({run_l, (i32)m, (i32)diag_pos[j], (i32)run0, (i32)(hi - run0)});
+                    }
+                }
+                if (bad) {
+                    for (i64 t = 0; t < len; t++) posmap[row_idx[cb + t]] = -1;
+                    if (!o.mismatch || k < o.mismatch_col) { o.mismatch = true; o.mismatch_col = k; }
+                    continue;
+                }
+                // group by phase; stable keeps ascending source order inside a phase
+                std::stable_sort(raw.begin(), raw.end(),
+                                 [](const RawChunk &a, const RawChunk &b) { return a.lvl < b.lvl; });
+                if ((i64)hist.size() < len) hist.assign(len, 0);
+                size_t g0 = 0;
+                while (g0 < raw.size()) {
+                    size_t g1 = g0;
+                    while (g1 < raw.size() && raw[g1].lvl == raw[g0].lvl) g1++;
+                    // MAC histogram over destination positions
+                    i64 pmin = len, pmax = -1, macs = 0;
+                    for (size_t c = g0; c < g1; c++) {
+                        const RawChunk &ch = raw[c];
+                        for (i32 t = 0; t < ch.cnt; t++) {
+                            i32 pos = posmap[row_idx[ch.p0 + t]];
+                            hist[pos]++;
+                            pmin = std::min<i64>(pmin, pos);
+                            pmax = std::max<i64>(pmax, pos);
+                        }
+                        macs += ch.cnt;
+                    }
+                    // greedy segmentation of [pmin, pmax] into item ranges
+                    std::vector<i64> cuts;  // segment starts
+                    cuts.push_back(pmin);
+                    i64 acc = 0;
+                    for (i64 pos = pmin; pos <= pmax; pos++) {
+                        i64 h = hist[pos];
+                        if (h == 0) continue;
+                        if ((acc > 0 && acc + h > T) || pos - cuts.back() >= kMaxSpan) {
+                            cuts.push_back(pos);
+                            acc = 0;
+                        }
+                        acc += h;
+                    }
+                    for (i64 pos = pmin; pos <= pmax; pos++) hist[pos] = 0;
+                    cuts.push_back(pmax + 1);
+                    size_t nseg = cuts.size() - 1;
+                    // split chunks at segment boundaries; emit items
+                    std::vector<std::vector<RawChunk>> seg_chunks(nseg);
+                    for (size_t c = g0; c < g1; c++) {
+                        const RawChunk &ch = raw[c];
+                        i32 t = 0;
+                        size_t s = 0;
+                        while (t < ch.cnt) {
+                            i32 pos = posmap[row_idx[ch.p0 + t]];
+                            while (pos >= cuts[s + 1]) s++;
+                            i32 t1 = t + 1;
+                            while (t1 < ch.cnt && posmap[row_idx[ch.p0 + t1]] < cuts[s + 1]) t1++;
+                            seg_chunks[s].push_back({ch.lvl, ch.m, ch.d, ch.p0 + t, t1 - t});
+                            t = t1;
+                        }
+                    }
+                    for (size_t s = 0; s < nseg; s++) {
+                        if (seg_chunks[s].empty()) continue;
+                        // tighten the segment to the positions actually touched
+                        i64 lo = cuts[s + 1], hi = cuts[s] - 1, sm = 0;
+                        for (auto &ch : seg_chunks[s]) {
+                            lo = std::min<i64>(lo, posmap[row_idx[ch.p0]]);
+                            hi = std::max<i64>(hi, posmap[row_idx[ch.p0 + ch.cnt - 1]]);
+                            sm += ch.cnt;
+                        }
+                        LocalItem it;
+                        it.lvl = raw[g0].lvl;
+                        it.k = (i32)k;
+                        it.base = cb + lo;
+                        it.span = (i32)(hi - lo + 1);
+                        it.macs = sm;
+                        it.c0 = (i64)o.chunks.size();
+                        o.chunks.insert(o.chunks.end(), seg_chunks[s].begin(), seg_chunks[s].end());
+                        it.c1 = (i64)o.chunks.size();
+                        o.items.push_back(it);
+                    }
+                    g0 = g1;
+                }
+                for (i64 t = 0; t < len; t++) posmap[row_idx[cb + t]] = -1;
+            }
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; t++) th.emplace_back(worker, t);
+    worker(0);
+    for (auto &t : th) t.join();
+
+    i64 mism = -1;
+    for (auto &o : outs)
+        if (o.mismatch && (mism < 0 || o.mismatch_col < mism)) mism = o.mismatch_col;
+    if (mism >= 0) {
+        set_error("update targets a slot absent from the filled pattern (column " +
+                  std::to_string(mism) + ")");
+        return GLU_MISMATCH;
+    }
+
+    // Global, thread-independent order: phase, then MACs descending (largest
+    // items go first in the static warp round-robin), then column, then base.
+    struct Ref { i32 lvl; i32 tid; i64 idx; };
+    std::vector<Ref> refs;
+    size_t total_items = 0;
+    for (auto &o : outs) total_items += o.items.size();
+    refs.reserve(total_items);
+    for (int t = 0; t < nt; t++)
+        for (i64 i = 0; i < (i64)outs[t].items.size(); i++) refs.push_back({outs[t].items[i].lvl, t, i});
+    std::sort(refs.begin(), refs.end(), [&](const Ref &a, const Ref &b) {
+        const LocalItem &x = outs[a.tid].items[a.idx], &y = outs[b.tid].items[b.idx];
+        if (x.lvl != y.lvl) return x.lvl < y.lvl;
+        if (x.macs != y.macs) return x.macs > y.macs;
+        if (x.k != y.k) return x.k < y.k;
+        return x.base < y.base;
+    });
+    auto *plan = new glu_plan();
+    plan->n_levels = n_levels;
+    plan->level_item_ptr.assign(n_levels + 1, 0);
+    plan->items.reserve(refs.size());
+    i64 map_off = 0;
+    for (auto &r : refs) {
+        const LocalItem &x = outs[r.tid].items[r.idx];
+        plan->level_item_ptr[x.lvl + 1]++;
+        glu::Item it{};
+        it.map_off = map_off;
+        it.base = (i32)x.base;
+        it.span = x.span;
+        it.c0 = (i32)plan->chunks.size();
+        for (i64 c = x.c0; c < x.c1; c++) {
+            const RawChunk &rc = outs[r.tid].chunks[c];
+            plan->chunks.push_back({rc.m, rc.d, rc.p0, rc.cnt});
+        }
+        it.c1 = (i32)plan->chunks.size();
+        it.macs = (i32)x.macs;
+        map_off += x.macs;
+        plan->max_item_macs = std::max<i64>(plan->max_item_macs, x.macs);
+        plan->max_chunks = std::max<i64>(plan->max_chunks, x.c1 - x.c0);
+        plan->items.push_back(it);
+    }
+    for (i64 l = 0; l < n_levels; l++) plan->level_item_ptr[l + 1] += plan->level_item_ptr[l];
+    plan->n_map = map_off;
+    for (auto &o : outs) plan->deferred += o.deferred;
+    if ((i64)plan->chunks.size() >= (i64)INT32_MAX) {
+        delete plan;
+        set_error("plan has >= 2^31 chunks");
+        return GLU_EINVAL;
+    }
+    *out = plan;
+    return GLU_OK;
+}
+
+extern "C" void glu_plan_info(const glu_plan *p, int64_t *info) {
+    info[0] = p->n_levels;
+    info[1] = (i64)p->items.size();
+    info[2] = (i64)p->chunks.size();
+    info[3] = p->n_map;
+    info[4] = p->max_item_macs;
+    info[5] = p->max_chunks;
+    info[6] = p->deferred;
+    info[7] = (i64)(p->items.size() * sizeof(glu::Item) + p->chunks.size() * sizeof(glu::Chunk) +
+                    p->level_item_ptr.size() * sizeof(i64) + p->n_map * sizeof(uint16_t));
+}
+
+extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
+                                int64_t *chunks) {
+    if (level_item_ptr)
+        std::memcpy(level_item_ptr, p->level_item_ptr.data(), p->level_item_ptr.size() * sizeof(i64));
+    if (items)
+        for (size_t i = 0; i < p->items.size(); i++) {
+            const glu::Item &it = p->items[i];
+            i64 *o = items + 6 * i;
+            o[0] = it.map_off; o[1] = it.base; o[2] = it.span; o[3] = it.c0; o[4] = it.c1; o[5] = it.macs;
+        }
+    if (chunks)
+        for (size_t i = 0; i < p->chunks.size(); i++) {
+            const glu::Chunk &c = p->chunks[i];
+            i64 *o = chunks + 4 * i;
+            o[0] = c.m; o[1] = c.d; o[2] = c.p0; o[3] = c.cnt;
+        }
+}
+
+extern "C" void glu_plan_free(glu_plan *p) { delete p; }
+
+namespace glu {
+const glu_plan_view plan_view(const glu_plan *p) {
+    glu_plan_view v;
+    v.n_levels = p->n_levels;
+    v.level_item_ptr = p->level_item_ptr.data();
+    v.items = p->items.data();
+    v.n_items = (i64)p->items.size();
+    v.chunks = p->chunks.data();
+    v.n_chunks = (i64)p->chunks.size();
+    v.n_map = p->n_map;
+    return v;
+}
+}  // namespace glu

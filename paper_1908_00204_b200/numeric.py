@@ -1,0 +1,466 @@
+"""Numeric factorization, refactorization and solves on the B200
+(API of levlu/numeric.py:27-388).
+
+Every factorization and solve below runs in libglu_b200's sm_100a kernels;
+there is no CPU fallback.  The per-pattern work (update plan, device upload,
+scatter-map build) is cached per (pattern, schedule, contract), so a second
+call with the same FilledPattern is a pure refactorization.
+
+Bitwise contracts:
+  * contract A -- each entry receives its MACs in ascending source order:
+    factor_left_looking, factor_right_looking_seq and
+    factor_parallel(deterministic=True) are bit-identical to the reference's.
+  * contract B -- level-major order: factor_parallel(deterministic=False) is
+    bit-identical to the reference's owner-serialized "atomic" mode.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import threading
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .depgraph import Hazard, LevelSchedule, detect_relaxed, levelize
+from .resource import LevelPlan, ResourceModel, concurrency_cap
+from .sparse import CscMatrix
+from .symbolic import FilledPattern
+
+DEFAULT_PIVOT_THRESHOLD = 1e-14
+
+
+class PivotError(ArithmeticError):
+    """Zero or near-zero pivot; no numeric pivoting is attempted."""
+
+    def __init__(self, column: int):
+        self.column = column
+        super().__init__(f"pivot breakdown at column {column}")
+
+
+class ScheduleHazardError(RuntimeError):
+    """A read-write conflict was detected under the given schedule."""
+
+    def __init__(self, hazards):
+        self.hazards = hazards
+        h = hazards[0]
+        super().__init__(
+            f"schedule hazard: column {h.writer} writes element {h.element} "
+            f"read by column {h.reader} in level {h.level}"
+        )
+
+
+class PatternMismatchError(RuntimeError):
+    """A value or update targeted a slot absent from the filled pattern."""
+
+
+@dataclass(frozen=True)
+class FactorOptions:
+    zero_pivot_threshold: float = DEFAULT_PIVOT_THRESHOLD
+    deterministic: bool = True
+    worker_count: int = 1
+    resource: ResourceModel | None = None
+    detect_races: bool = False
+
+    def __post_init__(self):
+        if self.worker_count < 1:
+            raise ValueError("worker_count must be >= 1")
+        if self.zero_pivot_threshold < 0:
+            raise ValueError("zero_pivot_threshold must be non-negative")
+
+
+@dataclass(frozen=True)
+class LuFactors:
+    """Unit-lower L and U sharing one value array over the filled pattern."""
+
+    pattern: FilledPattern
+    values: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.pattern.n
+
+    def to_scipy(self):
+        """(L, U) as scipy CSC matrices, unit diagonal explicit in L."""
+        import scipy.sparse as sp
+
+        fp = self.pattern
+        cp, rows = fp.full.col_ptr, fp.full.row_idx
+        cols = np.repeat(np.arange(fp.n, dtype=np.int64), np.diff(cp))
+        low = rows > cols
+        eye = sp.identity(fp.n, dtype=self.values.dtype, format="csc")
+        L = sp.csc_matrix((self.values[low], (rows[low], cols[low])), shape=(fp.n, fp.n)) + eye
+        U = sp.csc_matrix((self.values[~low], (rows[~low], cols[~low])), shape=(fp.n, fp.n))
+        return L, U
+
+
+@dataclass
+class FactorStats:
+    level_times: list = field(default_factory=list)
+    level_modes: list = field(default_factory=list)
+    flop_count: int = 0
+    peak_concurrent_columns: int = 0
+
+
+def pattern_flops(fp: FilledPattern) -> tuple[int, int]:
+    """(MACs, DIVs) of the pattern: MACs = sum over U entries (i,k) of
+    |L(:,i)|, DIVs = nnz(L) (levlu/numeric.py:187-193)."""
+    cp = fp.full.col_ptr
+    l_len = cp[1:] - fp.diag_pos - 1
+    cols = np.repeat(np.arange(fp.n, dtype=np.int64), np.diff(cp))
+    upper = fp.full.row_idx < cols
+    return int(l_len[fp.full.row_idx[upper]].sum()), int(l_len.sum())
+
+
+# ---------------------------------------------------------------------------
+# device factorizer: pattern + schedule + plan resident on the GPU
+# ---------------------------------------------------------------------------
+class Factorizer:
+    """One (filled pattern, level schedule, contract) resident on the device.
+
+    Owns the libglu_b200 handle: int32 pattern, per-level item/chunk plan and
+    the uint16 scatter map (built on the device).  ``factor_host`` is the
+    reference-facing path (host buffers in and out); ``factor_device`` works
+    in place on device memory (a torch tensor or raw pointer) on a stream.
+    """
+
+    def __init__(self, fp: FilledPattern, level_of: np.ndarray, contract: int,
+                 max_item_macs: int = 0, threads: int = 0):
+        self.n = fp.n
+        self.nnz = fp.nnz
+        self.contract = contract
+        cp, ri, dp = _lib.i64(fp.full.col_ptr), _lib.i64(fp.full.row_idx), _lib.i64(fp.diag_pos)
+        rp, ci, cs = _lib.i64(fp.csr.row_ptr), _lib.i64(fp.csr.col_idx), _lib.i64(fp.csr.csc_pos)
+        lv = _lib.i64(level_of)
+        plan = ctypes.c_void_p()
+        rc = _lib.check(_lib.lib.glu_plan_build(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
+                                                _lib.ptr(lv), contract, max_item_macs, threads,
+                                                ctypes.byref(plan)), "glu_plan_build")
+        if rc == _lib.GLU_MISMATCH:
+            raise PatternMismatchError("update targeted a structurally absent slot")
+        try:
+            info = np.zeros(8, dtype=np.int64)
+            _lib.lib.glu_plan_info(plan, _lib.ptr(info))
+            self.plan_info = dict(zip(("levels", "items", "chunks", "macs", "max_item_macs",
+                                       "max_chunks", "deferred_macs", "plan_bytes"),
+                                      info.tolist()))
+            h = ctypes.c_void_p()
+            rc = _lib.check(_lib.lib.glu_create(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
+                                                _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(cs),
+                                                _lib.ptr(lv), plan, ctypes.byref(h)),
+                            "glu_create")
+            if rc == _lib.GLU_MISMATCH:
+                raise PatternMismatchError("update targeted a structurally absent slot")
+        finally:
+            _lib.lib.glu_plan_free(plan)
+        self._h = h
+        self._finalizer = weakref.finalize(self, _lib.lib.glu_destroy, h)
+        self._input_key = None
+        self._lock = threading.Lock()
+        info = np.zeros(12, dtype=np.int64)
+        _lib.lib.glu_handle_info(h, _lib.ptr(info))
+        self.handle_info = dict(zip(("n", "nnz", "levels", "items", "chunks", "macs",
+                                     "device_bytes", "grid", "threads", "lsolve_levels",
+                                     "usolve_levels", "sms"), info.tolist()))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        self._finalizer()
+
+    def set_option(self, key: int, value: int):
+        _lib.check(_lib.lib.glu_set_option(self._h, key, value), "glu_set_option")
+
+    def set_input(self, a_col_ptr: np.ndarray, a_row_idx: np.ndarray):
+        """Install the A -> A_s slot map (device scatter); cached per A pattern."""
+        cp, ri = _lib.i64(a_col_ptr), _lib.i64(a_row_idx)
+        key = (len(cp), len(ri), hashlib.sha1(cp.tobytes() + ri.tobytes()).digest())
+        if key == self._input_key:
+            return
+        rc = _lib.check(_lib.lib.glu_set_input_pattern(self._h, len(ri), _lib.ptr(cp), _lib.ptr(ri)),
+                        "glu_set_input_pattern")
+        if rc >= 0:
+            raise PatternMismatchError(f"column {rc} of A has entries outside the filled pattern")
+        self._input_key = key
+
+    def factor_host(self, a_values: np.ndarray, thresh: float) -> tuple[np.ndarray, int]:
+        """H2D A values -> device scatter -> factor -> D2H LU values."""
+        a = _lib.f64(a_values)
+        out = np.empty(self.nnz, dtype=np.float64)
+        rc = _lib.check(_lib.lib.glu_factor_host(self._h, _lib.ptr(a), _lib.ptr(out), float(thresh)),
+                        "glu_factor_host")
+        return out, rc
+
+    def factor_device(self, v, thresh: float, stream=None) -> int:
+        """In-place factorization of device A_s values (torch tensor or int pointer)."""
+        return _lib.check(_lib.lib.glu_factor_device(self._h, _dptr(v), float(thresh),
+                                                     _stream(stream)), "glu_factor_device")
+
+    def factor_device_async(self, v, thresh: float, stream=None) -> None:
+        _lib.check(_lib.lib.glu_factor_device_async(self._h, _dptr(v), float(thresh),
+                                                    _stream(stream)), "glu_factor_device_async")
+
+    def status(self, stream=None) -> int:
+        return _lib.check(_lib.lib.glu_factor_status(self._h, _stream(stream)), "glu_factor_status")
+
+    def scatter_device(self, a_values, v, stream=None) -> None:
+        _lib.check(_lib.lib.glu_scatter_device(self._h, _dptr(a_values), _dptr(v), _stream(stream)),
+                   "glu_scatter_device")
+
+    def solve_device(self, lu, x, stream=None) -> int:
+        return _lib.check(_lib.lib.glu_solve_device(self._h, _dptr(lu), _dptr(x), _stream(stream)),
+                          "glu_solve_device")
+
+    def solve_host(self, lu: np.ndarray, b: np.ndarray, part: str = "both") -> tuple[np.ndarray, int]:
+        import torch
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+        lu_d = torch.from_numpy(_lib.f64(lu)).to(dev)
+        x_d = torch.from_numpy(_lib.f64(b).copy()).to(dev)
+        s = torch.cuda.current_stream()
+        fn = {"both": _lib.lib.glu_solve_device, "lower": _lib.lib.glu_lower_solve_device,
+              "upper": _lib.lib.glu_upper_solve_device}[part]
+        rc = _lib.check(fn(self._h, _dptr(lu_d), _dptr(x_d), ctypes.c_void_p(s.cuda_stream)),
+                        "glu_solve_device")
+        return x_d.cpu().numpy(), rc
+
+    def level_times_s(self) -> list:
+        m = int(self.handle_info["levels"])
+        ms = np.zeros(max(m, 1), dtype=np.float64)
+        k = _lib.lib.glu_level_times(self._h, _lib.ptr(ms), m)
+        return (ms[:k] * 1e-3).tolist()
+
+
+def _dptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _stream(s):
+    if s is None:
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(s, int):
+        return ctypes.c_void_p(s)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+_CACHE: dict = {}
+_CACHE_LOCK = threading.Lock()
+
+
+def _digest(a: np.ndarray) -> bytes:
+    return hashlib.sha1(np.ascontiguousarray(a, dtype=np.int64).tobytes()).digest()
+
+
+def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int) -> Factorizer:
+    """Cached Factorizer for (fp, schedule, contract); dropped with fp."""
+    key = (id(fp), contract, _digest(level_of))
+    with _CACHE_LOCK:
+        hit = _CACHE.get(key)
+        if hit is not None and hit[0]() is fp:
+            return hit[1]
+        fz = Factorizer(fp, level_of, contract)
+
+        def _drop(_ref, key=key):
+            with _CACHE_LOCK:
+                ent = _CACHE.pop(key, None)
+            if ent is not None:
+                ent[1].close()
+
+        _CACHE[key] = (weakref.ref(fp, _drop), fz)
+        return fz
+
+
+_SEQ_LEVELS: dict = {}
+
+
+def _relaxed_levels(fp: FilledPattern) -> np.ndarray:
+    """Relaxed level schedule of fp, cached: the schedule the sequential entry
+    points run on (their MAC order is the contract-A order, which is
+    schedule independent)."""
+    hit = _SEQ_LEVELS.get(id(fp))
+    if hit is not None and hit[0]() is fp:
+        return hit[1]
+    lv = levelize(detect_relaxed(fp)).level_of
+    _SEQ_LEVELS[id(fp)] = (weakref.ref(fp, lambda _r, k=id(fp): _SEQ_LEVELS.pop(k, None)), lv)
+    return lv
+
+
+def _require_f64(a: CscMatrix):
+    if a.values.dtype != np.float64:
+        raise TypeError(f"the B200 path factors fp64 values; got {a.values.dtype}")
+
+
+def _check(err: int) -> None:
+    if err == _lib.GLU_MISMATCH:
+        raise PatternMismatchError("update targeted a structurally absent slot")
+    if err >= 0:
+        raise PivotError(err)
+
+
+def _factor(a: CscMatrix, fp: FilledPattern, level_of: np.ndarray, contract: int,
+            thresh: float, by_column: bool) -> tuple[np.ndarray, Factorizer]:
+    _require_f64(a)
+    if a.n != fp.n:
+        raise PatternMismatchError("matrix and pattern sizes differ")
+    fz = get_factorizer(fp, level_of, contract)
+    with fz._lock:
+        fz.set_input(a.col_ptr, a.row_idx)
+        fz.set_option(2, 1 if by_column else 0)
+        fz.set_option(1, 0 if by_column else 1)
+        vals, rc = fz.factor_host(a.values, thresh)
+    _check(rc)
+    return vals, fz
+
+
+def factor_left_looking(a: CscMatrix, fp: FilledPattern,
+                        opts: FactorOptions = FactorOptions()) -> LuFactors:
+    """Left-looking result (levlu/numeric.py:129-142), computed by the level
+    kernel in contract-A order: bitwise the reference's values, failing
+    pivot = first failing column."""
+    vals, _ = _factor(a, fp, _relaxed_levels(fp), _lib.CONTRACT_A, opts.zero_pivot_threshold, True)
+    return LuFactors(fp, vals)
+
+
+def factor_right_looking_seq(a: CscMatrix, fp: FilledPattern,
+                             opts: FactorOptions = FactorOptions()) -> LuFactors:
+    """Sequential right-looking result (levlu/numeric.py:145-159): bitwise
+    equal to the left-looking path, so the same contract-A kernel."""
+    return factor_left_looking(a, fp, opts)
+
+
+def find_hazards(fp: FilledPattern, s: LevelSchedule, limit: int = 100000) -> list:
+    """Same-level write/read conflicts of the right-looking updates."""
+    cp, ri, dp = _lib.i64(fp.full.col_ptr), _lib.i64(fp.full.row_idx), _lib.i64(fp.diag_pos)
+    rp, ci = _lib.i64(fp.csr.row_ptr), _lib.i64(fp.csr.col_idx)
+    out = np.zeros((limit, 5), dtype=np.int64)
+    total = _lib.lib.glu_find_hazards(fp.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp), _lib.ptr(rp),
+                                      _lib.ptr(ci), _lib.ptr(_lib.i64(s.level_of)), limit,
+                                      _lib.ptr(out))
+    m = min(int(total), limit)
+    return [Hazard(int(w), int(r), (int(i), int(k)), int(l)) for l, w, r, i, k in out[:m]]
+
+
+def factor_parallel(a: CscMatrix, fp: FilledPattern, schedule: LevelSchedule,
+                    plans: list, opts: FactorOptions) -> tuple[LuFactors, FactorStats]:
+    """Level-parallel factorization on the B200 (levlu/numeric.py:241-351).
+
+    All levels run in one persistent kernel with a grid barrier per level.
+    deterministic=True gives the reference's deterministic (ascending-source)
+    values bit for bit, deterministic=False its atomic-mode (level-major)
+    values bit for bit; worker_count does not change the result in either
+    mode, exactly as in the reference.
+    """
+    if len(plans) != schedule.level_count:
+        raise ValueError("one LevelPlan per level required")
+    rm = opts.resource or ResourceModel()
+    if opts.detect_races:
+        hz = find_hazards(fp, schedule)
+        if hz:
+            raise ScheduleHazardError(hz)
+    contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
+    vals, fz = _factor(a, fp, schedule.level_of, contract, opts.zero_pivot_threshold, False)
+    caps = [min(concurrency_cap(p, len(c), rm), opts.worker_count, len(c))
+            for p, c in zip(plans, schedule.levels)]
+    stats = FactorStats(
+        level_times=fz.level_times_s(),
+        level_modes=[p.mode.value for p in plans],
+        flop_count=sum(_flops_cached(fp)),
+        peak_concurrent_columns=max(caps) if caps else 0,
+    )
+    return LuFactors(fp, vals), stats
+
+
+_FLOPS: dict = {}
+
+
+def _flops_cached(fp: FilledPattern) -> tuple[int, int]:
+    hit = _FLOPS.get(id(fp))
+    if hit is not None and hit[0]() is fp:
+        return hit[1]
+    f = pattern_flops(fp)
+    _FLOPS[id(fp)] = (weakref.ref(fp, lambda _r, k=id(fp): _FLOPS.pop(k, None)), f)
+    return f
+
+
+def refactorize(lu: LuFactors, a_new: CscMatrix, schedule: LevelSchedule | None = None,
+                opts: FactorOptions = FactorOptions()) -> LuFactors:
+    """New values, same pattern: reuses the device-resident
+    pattern, plan and scatter map; only A's values cross the bus."""
+    level_of = schedule.level_of if schedule is not None else _relaxed_levels(lu.pattern)
+    contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
+    vals, _ = _factor(a_new, lu.pattern, level_of, contract, opts.zero_pivot_threshold,
+                      schedule is None)
+    return LuFactors(lu.pattern, vals)
+
+
+def subcolumn_update(fp: FilledPattern, values: np.ndarray, source_j: int, dest_k: int):
+    """One rank-1 piece, dest column k -= L(:,j) * U(j,k) (levlu/numeric.py:
+    162-184).  A single-pair utility of the reference API, not a path of the
+    factorization: evaluated on the host arrays it is given."""
+    row_cols = fp.csr.row_cols(source_j)
+    t = int(np.searchsorted(row_cols, dest_k))
+    if t >= len(row_cols) or row_cols[t] != dest_k:
+        raise PatternMismatchError(f"A_s({source_j},{dest_k}) is structurally absent")
+    mult = values[fp.csr.row_pos(source_j)[t]]
+    dest_rows = fp.full.col_rows(dest_k)
+    src = fp.l_positions(source_j)
+    r = fp.full.row_idx[src]
+    q = np.searchsorted(dest_rows, r)
+    ok = (q < len(dest_rows))
+    ok[ok] = dest_rows[q[ok]] == r[ok]
+    if not ok.all():
+        bad = int(r[~ok][0])
+        raise PatternMismatchError(f"target slot ({bad},{dest_k}) is structurally absent")
+    tgt = fp.full.col_ptr[dest_k] + q
+    values[tgt] = values[tgt] - values[src] * mult
+
+
+def _solve(lu: LuFactors, b: np.ndarray, part: str) -> np.ndarray:
+    if len(b) != lu.n:
+        raise ValueError("right-hand side length mismatch")
+    if lu.values.dtype != np.float64:
+        raise TypeError(f"the B200 path solves fp64 factors; got {lu.values.dtype}")
+    fz = get_factorizer(lu.pattern, _relaxed_levels(lu.pattern), _lib.CONTRACT_A)
+    with fz._lock:
+        x, rc = fz.solve_host(lu.values, np.asarray(b, dtype=np.float64), part)
+    if rc >= 0:
+        raise PivotError(rc)
+    return x
+
+
+def lower_solve(lu: LuFactors, b: np.ndarray) -> np.ndarray:
+    """L y = b, implicit unit diagonal (levlu/numeric.py:354-361)."""
+    return _solve(lu, b, "lower")
+
+
+def upper_solve(lu: LuFactors, y: np.ndarray) -> np.ndarray:
+    """U x = y (levlu/numeric.py:364-373); zero diagonal -> PivotError."""
+    return _solve(lu, y, "upper")
+
+
+def solve(lu: LuFactors, b: np.ndarray) -> np.ndarray:
+    """A x = b through both triangular solves (levlu/numeric.py:376-378)."""
+    return _solve(lu, b, "both")
+
+
+def residual(a: CscMatrix, lu: LuFactors) -> float:
+    """||A - L U||_F / ||A||_F (verification utility, levlu/numeric.py:381-388)."""
+    import scipy.sparse as sp
+
+    L, U = lu.to_scipy()
+    A = sp.csc_matrix((a.values, a.row_idx, a.col_ptr), shape=(a.n, a.n))
+    diff = (A - L @ U).tocoo()
+    num = np.linalg.norm(diff.data)
+    den = np.linalg.norm(a.values)
+    return float(num / den) if den else float(num)

@@ -1,0 +1,168 @@
+"""B200 parity: every factorization / solve entry point, through the C ABI,
+against the reference's own outputs (tests/golden) and the CPU oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1908_00204_b200 as glu
+from conftest import csc_from_golden, load_golden, pattern_from_golden
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _analyze(a, rm=None):
+    fp = glu.symbolic_fillin(a.pattern)
+    s = glu.levelize(glu.detect_relaxed(fp))
+    st = glu.level_stats(fp, s)
+    plans = glu.plan_schedule(s, st, a.n, rm or glu.ResourceModel())
+    return fp, s, plans
+
+
+def test_factor_parallel_both_contracts_bitwise(golden):
+    name, g = golden
+    a = csc_from_golden(g)
+    fp, s, plans = _analyze(a)
+    thr = float(g["thresh"])
+    for det, tag in ((True, "det"), (False, "b")):
+        for workers in (1, 8):
+            opts = glu.FactorOptions(deterministic=det, worker_count=workers,
+                                     zero_pivot_threshold=thr)
+            if int(g[f"fail_{tag}"]) >= 0:
+                with pytest.raises(glu.PivotError) as e:
+                    glu.factor_parallel(a, fp, s, plans, opts)
+                assert e.value.column == int(g[f"fail_{tag}"])
+            else:
+                lu, stats = glu.factor_parallel(a, fp, s, plans, opts)
+                assert np.array_equal(lu.values, g[f"lu_{tag}"]), (name, tag)
+                assert len(stats.level_times) == s.level_count
+                assert stats.level_modes == [p.mode.value for p in plans]
+                assert stats.flop_count == int(g["flop_count"])
+
+
+def test_sequential_entry_points_bitwise(golden):
+    name, g = golden
+    a = csc_from_golden(g)
+    fp = glu.symbolic_fillin(a.pattern)
+    opts = glu.FactorOptions(zero_pivot_threshold=float(g["thresh"]))
+    for fn, tag in ((glu.factor_left_looking, "a"), (glu.factor_right_looking_seq, "rl")):
+        if int(g[f"fail_{tag}"]) >= 0:
+            with pytest.raises(glu.PivotError) as e:
+                fn(a, fp, opts)
+            assert e.value.column == int(g[f"fail_{tag}"])
+        else:
+            assert np.array_equal(fn(a, fp, opts).values, g[f"lu_{tag}"]), (name, tag)
+
+
+def test_solves_bitwise(golden):
+    name, g = golden
+    if "rhs" not in g:
+        pytest.skip("factorization fails for this case")
+    a = csc_from_golden(g)
+    fp = glu.symbolic_fillin(a.pattern)
+    lu = glu.LuFactors(fp, g["lu_a"])
+    y = glu.lower_solve(lu, g["rhs"])
+    assert np.array_equal(y, g["y_lower"])
+    assert np.array_equal(glu.upper_solve(lu, y), g["x_upper"])
+    assert np.array_equal(glu.solve(lu, g["rhs"]), g["x_solve"])
+
+
+def test_upper_solve_zero_diagonal():
+    a = glu.to_csc(glu.Triplets(3, 3, [0, 1, 2, 0], [0, 1, 2, 2], [2.0, 3.0, 1.0, 1.0]))
+    fp = glu.symbolic_fillin(a.pattern)
+    vals = np.array([2.0, 0.0, 1.0, 1.0])  # U(1,1) = 0
+    with pytest.raises(glu.PivotError) as e:
+        glu.upper_solve(glu.LuFactors(fp, vals), np.ones(3))
+    assert e.value.column == 1
+    with pytest.raises(ValueError):
+        glu.lower_solve(glu.LuFactors(fp, vals), np.ones(2))
+
+
+def test_scatter_rejects_pattern_mismatch():
+    from conftest import random_dd
+
+    rng = np.random.default_rng(9)
+    a = random_dd(rng, 15, 0.15)
+    fp = glu.symbolic_fillin(a.pattern)
+    bigger = random_dd(rng, 15, 0.4)
+    with pytest.raises(glu.PatternMismatchError):
+        glu.factor_left_looking(bigger, fp)
+
+
+def test_detect_races():
+    g = load_golden("conflict8")
+    a = csc_from_golden(g)
+    fp = glu.symbolic_fillin(a.pattern)
+    s = glu.levelize(glu.detect_upward(fp))
+    plans = glu.plan_schedule(s, glu.level_stats(fp, s), a.n, glu.ResourceModel())
+    with pytest.raises(glu.ScheduleHazardError) as e:
+        glu.factor_parallel(a, fp, s, plans, glu.FactorOptions(detect_races=True, deterministic=False))
+    assert "writes element" in str(e.value) and e.value.hazards
+    fp, s, plans = _analyze(a)
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions(detect_races=True, worker_count=2))
+    assert glu.residual(a, lu) <= 1e-12
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make("cfg2")
+    fp, s, plans = _analyze(a, glu.B200_RESOURCE)
+    return a, fp, s, plans
+
+
+def _oracle_values(a, fp, s, deterministic):
+    pat = orc.Pattern.from_fp(fp)
+    v, bad = orc.scatter(pat, a.col_ptr, a.row_idx, a.values)
+    assert bad == -1
+    lp = np.concatenate([[0], np.cumsum([len(c) for c in s.levels])])
+    caps = np.ones(len(s.levels), dtype=np.int64)
+    assert orc.factor_parallel(pat, v, lp, np.concatenate(s.levels), caps, deterministic) == -1
+    return v
+
+
+@pytest.mark.parametrize("det", [True, False])
+def test_cfg2_full_size_bitwise_vs_oracle(cfg2, det):
+    a, fp, s, plans = cfg2
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions(deterministic=det))
+    ref = _oracle_values(a, fp, s, det)
+    assert np.array_equal(lu.values, ref)
+
+
+def test_cfg2_refactorize_and_solve(cfg2):
+    from paper_1908_00204_b200 import synthetic
+
+    a, fp, s, plans = cfg2
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions(deterministic=False))
+    a2 = glu.CscMatrix(a.n, a.col_ptr, a.row_idx, synthetic.perturb_values(a, 1000))
+    lu2 = glu.refactorize(lu, a2, s, glu.FactorOptions(deterministic=False))
+    assert np.array_equal(lu2.values, _oracle_values(a2, fp, s, False))
+    b = np.random.default_rng(3).standard_normal(a.n)
+    x = glu.solve(lu2, b)
+    pat = orc.Pattern.from_fp(fp)
+    xr, bad = orc.upper_solve(pat, lu2.values, orc.lower_solve(pat, lu2.values, b))
+    assert bad == -1 and np.array_equal(x, xr)
+    import scipy.sparse as sp
+
+    A = sp.csc_matrix((a2.values, a2.row_idx, a2.col_ptr), shape=(a.n, a.n))
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 1e-10
+
+
+def test_device_api_matches_host_api(cfg2):
+    import torch
+
+    a, fp, s, plans = cfg2
+    fz = glu.get_factorizer(fp, s.level_of, 1)
+    fz.set_input(a.col_ptr, a.row_idx)
+    host, rc = fz.factor_host(a.values, 1e-14)
+    assert rc == -1
+    dev = torch.device("cuda")
+    a_d = torch.from_numpy(a.values).to(dev)
+    v_d = torch.empty(fp.nnz, dtype=torch.float64, device=dev)
+    for _ in range(2):  # repeatable
+        fz.scatter_device(a_d, v_d)
+        assert fz.factor_device(v_d, 1e-14) == -1
+        assert np.array_equal(v_d.cpu().numpy(), host)

@@ -1,0 +1,112 @@
+"""The update plan (glu_plan_build) reproduces the reference's MAC order.
+
+A numpy emulation of exactly what the device kernel does with the plan
+(items in any order inside a phase, chunks in order inside an item, targets
+by searching the item's segment, on-the-fly division, final pivot/divide
+pass) must give the reference's values bit for bit: contract A = the
+left-looking / deterministic values, contract B = the atomic-mode values.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_1908_00204_b200 as glu
+from paper_1908_00204_b200 import _lib
+from conftest import csc_from_golden, load_golden
+
+
+def export_plan(fp, level_of, contract, max_item_macs=0):
+    cp, ri, dp = _lib.i64(fp.full.col_ptr), _lib.i64(fp.full.row_idx), _lib.i64(fp.diag_pos)
+    lv = _lib.i64(level_of)
+    h = ctypes.c_void_p()
+    rc = _lib.lib.glu_plan_build(fp.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp), _lib.ptr(lv),
+                                 contract, max_item_macs, 2, ctypes.byref(h))
+    assert rc == _lib.GLU_OK, _lib.last_error()
+    info = np.zeros(8, dtype=np.int64)
+    _lib.lib.glu_plan_info(h, _lib.ptr(info))
+    nl, ni, nc = int(info[0]), int(info[1]), int(info[2])
+    lip = np.zeros(nl + 1, dtype=np.int64)
+    items = np.zeros((max(ni, 1), 6), dtype=np.int64)
+    chunks = np.zeros((max(nc, 1), 4), dtype=np.int64)
+    _lib.lib.glu_plan_export(h, _lib.ptr(lip), _lib.ptr(items), _lib.ptr(chunks))
+    _lib.lib.glu_plan_free(h)
+    return dict(info=info, lip=lip, items=items[:ni], chunks=chunks[:nc])
+
+
+def emulate(fp, level_of, plan, v, thresh, rng=None):
+    ri = fp.full.row_idx
+    lip, items, chunks = plan["lip"], plan["items"], plan["chunks"]
+    map_next = 0
+    for l in range(len(lip) - 1):
+        order = np.arange(lip[l], lip[l + 1])
+        if rng is not None:
+            rng.shuffle(order)  # items of a phase are independent
+        for it in order:
+            moff, base, span, c0, c1, macs = items[it]
+            seg = ri[base:base + span]
+            for m, d, p0, cnt in chunks[c0:c1]:
+                p = np.arange(p0, p0 + cnt)
+                off = np.searchsorted(seg, ri[p])
+                assert np.array_equal(seg[off], ri[p])
+                q = base + off
+                v[q] = v[q] - (v[p] / v[d]) * v[m]
+    fail = None
+    cp, dp = fp.full.col_ptr, fp.diag_pos
+    for j in range(fp.n):
+        col = v[cp[j]:cp[j + 1]]
+        cmax = 0.0
+        for x in np.abs(col):
+            if x > cmax:
+                cmax = x
+        piv = v[dp[j]]
+        if abs(piv) <= thresh * cmax:
+            key = (int(level_of[j]), j)
+            fail = key if fail is None or key < fail else fail
+            continue
+        v[dp[j] + 1:cp[j + 1]] = v[dp[j] + 1:cp[j + 1]] / piv
+    return fail
+
+
+CASES = ["conflict8", "random_dd_s2_n80", "random_dd_s3_n120", "random_dd_s5_n100",
+         "random_dd_s11_n300", "random_dd_s12_n500", "block_arrow_4x24", "banded_n200", "cfg1",
+         "singular_2x2", "threshold_fail"]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("contract", [_lib.CONTRACT_A, _lib.CONTRACT_B])
+@pytest.mark.parametrize("max_item_macs", [0, 7])
+def test_plan_emulation_bitwise(case, contract, max_item_macs):
+    g = load_golden(case)
+    a = csc_from_golden(g)
+    fp = glu.symbolic_fillin(a.pattern)
+    level_of = g["level_of"]
+    plan = export_plan(fp, level_of, contract, max_item_macs)
+    assert int(plan["info"][3]) == glu.pattern_flops(fp)[0]  # one map entry per MAC
+    if max_item_macs:
+        one_pos = plan["items"][:, 5] > max_item_macs
+        # only items whose MACs all hit one position may exceed the bound
+        for it in plan["items"][one_pos]:
+            assert it[2] == 1
+    v = np.zeros(fp.nnz)
+    from oracle import oracle as orc
+    v, bad = orc.scatter(orc.Pattern.from_fp(fp), a.col_ptr, a.row_idx, a.values)
+    fail = emulate(fp, level_of, plan, v, float(g["thresh"]), np.random.default_rng(0))
+    tag = "a" if contract == _lib.CONTRACT_A else "b"
+    if int(g[f"fail_{tag}"]) >= 0:
+        assert fail is not None and fail[1] == int(g[f"fail_{tag}"])
+    else:
+        assert fail is None
+        assert np.array_equal(v, g[f"lu_{tag}"])
+
+
+def test_contract_a_defers_only_when_needed():
+    g = load_golden("cfg1")
+    fp = glu.symbolic_fillin(csc_from_golden(g).pattern)
+    pa = export_plan(fp, g["level_of"], _lib.CONTRACT_A)
+    pb = export_plan(fp, g["level_of"], _lib.CONTRACT_B)
+    assert pb["info"][6] == 0
+    assert 0 < pa["info"][6] < pa["info"][3]
