@@ -357,7 +357,7 @@ def run_ours(args):
         pat = orc.Pattern.from_fp(fp)
         ref, bad = orc.scatter(pat, a.col_ptr, a.row_idx, sets[(args.steps - 1) % nsets])
         lp, lc = level_arrays(s)
-        orc.factor_parallel(pat, ref, lp, lc, np.ones(len(lp) - 1, np.int64), contract == 1)
+        orc.factor_parallel(pat, ref, lp, lc, np.ones(len(lp) - 1, np.int64), contract == 0)
         parity = "bitwise" if np.array_equal(ref, lu_last) else "MISMATCH"
         if not args.no_cpu_baseline:
             cpu = cpu_baseline(a, fp, s, args.cpu_budget)

@@ -99,21 +99,29 @@ int64_t glu_find_hazards(int64_t n, const int64_t *col_ptr, const int64_t *row_i
 
 /* ---- update plan: the precomputed scatter schedule -------------------- */
 
-/* Builds the destination-owned update plan for the given level schedule.
-   contract: GLU_CONTRACT_A or GLU_CONTRACT_B.  max_item_macs bounds the
-   MACs one warp task carries (0 = default).  Returns GLU_OK or
-   GLU_MISMATCH when an update targets a slot absent from the pattern
-   (the condition _kernels.py:113-114 reports at run time). */
+/* Builds the destination-owned update plan for the given level schedule
+   (the precomputed replacement of the runtime merge search in
+   _kernels.py:107-115 / :140-148 and of the ownership split of
+   numeric.py:295-315).  contract: GLU_CONTRACT_A or GLU_CONTRACT_B.
+   max_item_macs fixes the MACs one push item carries (0 = adaptive per
+   phase); deep_min is the MAC count from which a target becomes its own
+   register-chained item (0 = default 8).  Returns GLU_OK or GLU_MISMATCH
+   when an update targets a slot absent from the pattern (the condition
+   _kernels.py:113-114 reports at run time). */
 int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                        const int64_t *diag_pos, const int64_t *level_of, int32_t contract,
-                       int64_t max_item_macs, int32_t n_threads, glu_plan **out);
-/* info[0..7] = n_levels, n_items, n_chunks, n_map (= MACs), max_item_macs,
-   max_chunks_per_item, deferred_macs (contract A), plan bytes */
+                       int64_t max_item_macs, int64_t deep_min, int32_t n_threads,
+                       glu_plan **out);
+/* info[0..11] = n_levels, n_items, n_chunks, MACs, max_item_macs,
+   max_chunks_per_item, deferred_macs (contract A), plan bytes, deep items,
+   deep MACs, epochs, push MACs (= uint16 map entries) */
 void glu_plan_info(const glu_plan *p, int64_t *info);
-/* level_item_ptr[n_levels+1]; items[n_items*6] = {map_off, base, span, c0, c1, macs};
-   chunks[n_chunks*4] = {m, d, p0, cnt}  (all slots absolute). */
+/* level_item_ptr[n_levels+1];
+   items[n_items*7]  = {map_off, base, span, c0, c1, macs, kind (0 push, 1 deep)};
+   chunks[n_chunks*5] = {m, d, p0, cnt, epoch_start};
+   deep[deep_macs*3]  = {l, d, m}  (all slots absolute). */
 void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
-                     int64_t *chunks);
+                     int64_t *chunks, int64_t *deep);
 void glu_plan_free(glu_plan *p);
 
 /* ---- device handle ---------------------------------------------------- */

@@ -73,6 +73,7 @@ struct FactorParams {
     const Item *items;
     const Chunk *chunks;
     const uint16_t *map;
+    const glu::DeepRef *deep;
     const i32 *col_ptr;
     const i32 *diag_pos;
     const i32 *level_of;
@@ -91,42 +92,138 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// One item: ordered chunks into one destination segment.  Chunk descriptors,
-// pivots and multipliers of up to 32 chunks are fetched lane-parallel (none of
-// them is written during the phase), then the chunks run in order.
-__device__ __forceinline__ void run_item(const FactorParams &P, int idx, int lane) {
-    const int4 *ip = reinterpret_cast<const int4 *>(P.items + idx);
-    const int4 a = __ldg(ip), b = __ldg(ip + 1);
+// kPush item: ordered chunks into one destination segment.  The chunk
+// descriptors of a window of <= 32 chunks are fetched lane-parallel (with
+// their pivots and multipliers: none of them is written during the phase),
+// then the window's entries are flattened over the lanes 32 at a time.
+// Entries of one epoch hit distinct targets, so a round's read-modify-writes
+// run in parallel; a round that straddles an epoch boundary applies its
+// epochs in order with a warp barrier between them.  The next round's map
+// and L loads are issued before the current round's target RMW.
+struct Round {
+    int q;        // target offset in the segment (-1: lane idle)
+    int ep;       // epoch of the entry inside the window
+    double l;     // A_s(i,j), undivided
+    double pv;    // pivot A_s(j,j)
+    double mu;    // multiplier U(j,k)
+};
+
+__device__ __forceinline__ void load_round(const FactorParams &P, const uint16_t *mp, int rbase,
+                                           int wtot, int lane, int nch, int incl, int p0, int est,
+                                           double piv, double mult, int myep, Round &R) {
+    const int e = rbase + lane;
+    // chunk of entry e: chunks starting in (rbase, rbase+32) split the round
+    const unsigned start_bits = __reduce_or_sync(
+        0xffffffffu, (lane < nch && est > rbase && est < rbase + 32) ? (1u << (est - rbase)) : 0u);
+    const int cfirst = __popc(__ballot_sync(0xffffffffu, lane < nch && est <= rbase)) - 1;
+    const int c = cfirst + __popc(start_bits & ((2u << lane) - 1u));
+    const int cp0 = __shfl_sync(0xffffffffu, p0, c);
+    const int cest = __shfl_sync(0xffffffffu, est, c);
+    R.pv = __shfl_sync(0xffffffffu, piv, c);
+    R.mu = __shfl_sync(0xffffffffu, mult, c);
+    R.ep = __shfl_sync(0xffffffffu, myep, c);
+    R.q = -1;
+    if (e < wtot) {
+        R.q = __ldg(mp + e);
+        R.l = ldv(P.v + cp0 + (e - cest));
+    }
+}
+
+__device__ __forceinline__ void apply_round(double *vb, const Round &R, int lane) {
+    const int lo = __shfl_sync(0xffffffffu, R.ep, 0);
+    const unsigned act = __ballot_sync(0xffffffffu, R.q >= 0);
+    const int hi = __shfl_sync(0xffffffffu, R.ep, 31 - __clz(act));
+    double prod = 0.0;
+    if (R.q >= 0) prod = __dmul_rn(__ddiv_rn(R.l, R.pv), R.mu);
+    if (lo == hi) {
+        if (R.q >= 0) {
+            double *tp = vb + R.q;
+            stv(tp, __dsub_rn(ldv(tp), prod));
+        }
+    } else {
+        for (int ep = lo; ep <= hi; ++ep) {
+            if (R.q >= 0 && R.ep == ep) {
+                double *tp = vb + R.q;
+                stv(tp, __dsub_rn(ldv(tp), prod));
+            }
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void run_push(const FactorParams &P, int4 a, int4 b, int lane) {
     const i64 moff = (i64)(unsigned)a.x | ((i64)a.y << 32);
     double *vb = P.v + a.z;
     const uint16_t *mp = P.map + moff;
     const int c0 = b.x, c1 = b.y;
     const int4 *cp = reinterpret_cast<const int4 *>(P.chunks);
-    for (int cb = c0; cb < c1; cb += 32) {
-        const int nch = min(32, c1 - cb);
+    for (int wb = c0; wb < c1; wb += 32) {
+        const int nch = min(32, c1 - wb);
         int4 ch = make_int4(0, 0, 0, 0);
         double piv = 1.0, mult = 0.0;
         if (lane < nch) {
-            ch = __ldg(cp + cb + lane);
+            ch = __ldg(cp + wb + lane);
             piv = ldv(P.v + ch.y);
             mult = ldv(P.v + ch.x);
         }
-        for (int s = 0; s < nch; ++s) {
-            const int p0 = __shfl_sync(0xffffffffu, ch.z, s);
-            const int cnt = __shfl_sync(0xffffffffu, ch.w, s);
-            const double pv = __shfl_sync(0xffffffffu, piv, s);
-            const double mu = __shfl_sync(0xffffffffu, mult, s);
-            for (int t = lane; t < cnt; t += 32) {
-                const int q = __ldg(mp + t);
-                const double l = ldv(P.v + p0 + t);
-                const double prod = __dmul_rn(__ddiv_rn(l, pv), mu);
-                double *tp = vb + q;
-                stv(tp, __dsub_rn(ldv(tp), prod));
-            }
-            mp += cnt;
-            __syncwarp();
+        const int cnt = ch.w & 0x7fffffff;
+        const bool newep = lane == 0 || (lane < nch && (ch.w & glu::kEpochBit));
+        const unsigned epm = __ballot_sync(0xffffffffu, newep);
+        const int myep = __popc(epm & ((2u << lane) - 1u)) - 1;
+        // inclusive prefix of chunk sizes -> exclusive starts
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
+        }
+        const int est = incl - cnt;
+        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+        Round cur, nxt;
+        load_round(P, mp, 0, wtot, lane, nch, incl, ch.z, est, piv, mult, myep, cur);
+        for (int rb = 0; rb < wtot; rb += 32) {
+            if (rb + 32 < wtot)
+                load_round(P, mp, rb + 32, wtot, lane, nch, incl, ch.z, est, piv, mult, myep, nxt);
+            apply_round(vb, cur, lane);
+            cur = nxt;
+        }
+        mp += wtot;
+    }
+}
+
+// kDeep item: one target, many ordered contributions.  Lanes form 32
+// products at a time (independent roundings); every lane then replays the
+// subtraction chain in order from shuffles, so the target sees exactly the
+// reference's sequence of roundings with one load and one store.
+__device__ __forceinline__ void run_deep(const FactorParams &P, int4 a, int4 b, int lane) {
+    const i64 off = (i64)(unsigned)a.x | ((i64)a.y << 32);
+    const int macs = b.z;
+    const int4 *dr = reinterpret_cast<const int4 *>(P.deep) + off;
+    double *tp = P.v + a.z;
+    double acc = ldv(tp);
+    for (int r = 0; r < macs; r += 32) {
+        double prod = 0.0;
+        if (r + lane < macs) {
+            const int4 c = __ldg(dr + r + lane);
+            prod = __dmul_rn(__ddiv_rn(ldv(P.v + c.x), ldv(P.v + c.y)), ldv(P.v + c.z));
+        }
+        const int cnt = min(32, macs - r);
+        if (cnt == 32) {
+#pragma unroll
+            for (int s = 0; s < 32; ++s) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, prod, s));
+        } else {
+            for (int s = 0; s < cnt; ++s) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, prod, s));
         }
     }
+    if (lane == 0) stv(tp, acc);
+}
+
+__device__ __forceinline__ void run_item(const FactorParams &P, int idx, int lane) {
+    const int4 *ip = reinterpret_cast<const int4 *>(P.items + idx);
+    const int4 a = __ldg(ip), b = __ldg(ip + 1);
+    if (b.w == glu::kDeep) run_deep(P, a, b, lane);
+    else run_push(P, a, b, lane);
 }
 
 // Pivot check + divide of column j (_kernels.py:152-173): cmax over the
@@ -185,11 +282,13 @@ __global__ void build_map_kernel(const Item *items, i64 n_items, const Chunk *ch
     const i64 nwarp = (i64)gridDim.x * (blockDim.x >> 5);
     for (i64 it = w; it < n_items; it += nwarp) {
         const Item I = items[it];
+        if (I.kind != glu::kPush) continue;
         const i32 *seg = row_idx + I.base;
         i64 off = I.map_off;
         for (int c = I.c0; c < I.c1; ++c) {
             const Chunk C = chunks[c];
-            for (int t = lane; t < C.cnt; t += 32) {
+            const int cnt = C.meta & 0x7fffffff;
+            for (int t = lane; t < cnt; t += 32) {
                 const i32 r = row_idx[C.p0 + t];
                 int lo = 0, hi = I.span;
                 while (lo < hi) {
@@ -199,7 +298,7 @@ __global__ void build_map_kernel(const Item *items, i64 n_items, const Chunk *ch
                 if (lo >= I.span || seg[lo] != r) atomicExch(bad, 1);
                 map[off + t] = (uint16_t)lo;
             }
-            off += C.cnt;
+            off += cnt;
         }
     }
 }
@@ -308,6 +407,8 @@ struct glu_handle {
     Item *items = nullptr;
     Chunk *chunks = nullptr;
     uint16_t *map = nullptr;
+    glu::DeepRef *deep = nullptr;
+    i64 n_deep = 0;
     // solves
     i64 l_levels = 0, u_levels = 0;
     i32 *l_lvl_ptr = nullptr, *l_rows = nullptr, *l_ptr = nullptr, *l_col = nullptr, *l_slot = nullptr;
@@ -400,6 +501,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     h->n_items = pv.n_items;
     h->n_chunks = pv.n_chunks;
     h->n_map = pv.n_map;
+    h->n_deep = pv.n_deep;
     if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
         glu::set_error("cudaStreamCreate"); return fail(GLU_ECUDA);
     }
@@ -414,6 +516,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     UP(h->level_item_ptr, to_i32(pv.level_item_ptr, pv.n_levels + 1));
     UP(h->items, std::vector<Item>(pv.items, pv.items + pv.n_items));
     UP(h->chunks, std::vector<Chunk>(pv.chunks, pv.chunks + pv.n_chunks));
+    UP(h->deep, std::vector<glu::DeepRef>(pv.deep, pv.deep + pv.n_deep));
     if (h->n_map > 0) {
         if (cudaMalloc((void **)&h->map, (size_t)h->n_map * sizeof(uint16_t)) != cudaSuccess) {
             glu::set_error("cudaMalloc(scatter map " + std::to_string(h->n_map * 2) + " B)");
@@ -467,7 +570,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
 extern "C" void glu_destroy(glu_handle *h) {
     if (!h) return;
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_item_ptr, h->items,
-                    h->chunks, h->map, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
+                    h->chunks, h->map, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
                     h->bar, h->ifail, h->level_ns, h->d_a, h->d_v, h->d_x};
     for (void *p : ptrs)
@@ -552,6 +655,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.items = h->items;
     P.chunks = h->chunks;
     P.map = h->map;
+    P.deep = h->deep;
     P.col_ptr = h->col_ptr;
     P.diag_pos = h->diag_pos;
     P.level_of = h->level_of;

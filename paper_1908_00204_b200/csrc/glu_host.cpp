@@ -347,11 +347,21 @@ sort:
 // MACs read the same undivided L values; one final pass pivot-checks and
 // divides every column.
 //
-// Work unit ("item"): one destination column segment in one phase, with its
-// ordered list of "chunks" (contiguous runs of one source's L entries).  One
-// warp owns an item, so ordering needs no atomics.  Segments bound the MACs
-// per item (hub columns split over many warps) and keep the target offsets
-// of an item within uint16 range of its base slot.
+// Work units, one warp each, for one destination column k in one phase:
+//   kDeep  a single target that receives >= deep_min MACs in the phase (the
+//          rows/columns of power/ground hubs): its ordered contributions are
+//          listed explicitly, the warp forms 32 products at a time and runs
+//          the subtraction chain in registers -- one load and one store of
+//          the target instead of one L2 round trip per MAC.
+//   kPush  a segment of column k (<= T MACs, <= 65535 positions) with its
+//          ordered chunks (contiguous runs of one source's L entries); lanes
+//          take the chunks' entries 32 at a time.  Chunks are grouped into
+//          epochs of pairwise target-disjoint chunks (kEpochBit marks an
+//          epoch start), so the warp only orders stores where two chunks
+//          really touch the same target.
+// One warp owns every MAC of a target in a phase, so ordering needs no
+// atomics.  T adapts to the phase's total MACs (enough items to fill the
+// grid's warps, 32 <= T <= 1024) unless max_item_macs fixes it.
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -363,15 +373,18 @@ struct RawChunk {
 struct LocalItem {
     i32 lvl;
     i32 k;
-    i64 base;    // absolute slot of the segment start
+    i32 kind;
+    i64 base;    // kPush: absolute slot of the segment start; kDeep: target slot
     i32 span;    // positions covered
     i64 macs;
-    i64 c0, c1;  // chunk range in the thread-local chunk vector
+    i64 c0, c1;  // kPush: chunk range in the thread-local chunk vector;
+                 // kDeep: range in the thread-local deep vector
 };
 
 struct ThreadOut {
     std::vector<LocalItem> items;
-    std::vector<RawChunk> chunks;
+    std::vector<glu::Chunk> chunks;
+    std::vector<glu::DeepRef> deep;
     i64 deferred = 0;
     bool mismatch = false;
     i64 mismatch_col = -1;
@@ -384,18 +397,22 @@ struct glu_plan {
     std::vector<i64> level_item_ptr;
     std::vector<glu::Item> items;
     std::vector<glu::Chunk> chunks;
+    std::vector<glu::DeepRef> deep;
     i64 n_map = 0;
     i64 max_item_macs = 0;
     i64 max_chunks = 0;
     i64 deferred = 0;
+    i64 n_deep_items = 0;
+    i64 n_epochs = 0;
 };
 
 static constexpr i64 kMaxSpan = 65535;
+static constexpr i64 kTargetItemsPerPhase = 2 * 148 * 16;  // two items per resident warp
 
 extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                                   const int64_t *diag_pos, const int64_t *level_of,
-                                  int32_t contract, int64_t max_item_macs, int32_t n_threads,
-                                  glu_plan **out) {
+                                  int32_t contract, int64_t max_item_macs, int64_t deep_min,
+                                  int32_t n_threads, glu_plan **out) {
     *out = nullptr;
     if (contract != GLU_CONTRACT_A && contract != GLU_CONTRACT_B) {
         set_error("contract must be GLU_CONTRACT_A or GLU_CONTRACT_B");
@@ -405,9 +422,22 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         set_error("pattern has >= 2^31 entries; slot indices are int32 on the device");
         return GLU_EINVAL;
     }
-    const i64 T = max_item_macs > 0 ? max_item_macs : 1024;
+    const i64 D = deep_min > 0 ? deep_min : 8;
     i64 n_levels = 0;
     for (i64 j = 0; j < n; j++) n_levels = std::max(n_levels, level_of[j] + 1);
+    // per-phase MAC totals (at the source's level) -> per-phase item size T
+    std::vector<i64> phase_macs(n_levels, 0);
+    for (i64 k = 0; k < n; k++)
+        for (i64 m = col_ptr[k]; m < diag_pos[k]; m++) {
+            const i64 j = row_idx[m];
+            phase_macs[level_of[j]] += col_ptr[j + 1] - diag_pos[j] - 1;
+        }
+    std::vector<i64> Tp(n_levels);
+    for (i64 l = 0; l < n_levels; l++)
+        Tp[l] = max_item_macs > 0
+                    ? max_item_macs
+                    : std::min<i64>(1024, std::max<i64>(32, (phase_macs[l] + kTargetItemsPerPhase - 1) /
+                                                                kTargetItemsPerPhase));
     int nt = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
     nt = (int)std::min<i64>(nt, std::max<i64>(1, n / 64));
     std::vector<ThreadOut> outs(nt);
@@ -418,10 +448,15 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         ThreadOut &o = outs[tid];
         std::vector<i32> posmap(n, -1);
         std::vector<i32> runmax;   // contract A: running max level per position
-        std::vector<i64> hist;     // MACs per position for segmentation
+        std::vector<i64> hist;     // MACs per position in the current phase
+        std::vector<i64> deepidx;  // position -> deep item (local index) or -1
+        std::vector<i64> stamp;    // position -> epoch that last touched it
+        std::vector<i64> seg_of;   // position -> segment index or -1
         std::vector<RawChunk> raw;
-        std::vector<i32> lvl_of_entry;
-        std::vector<i64> order;
+        std::vector<std::vector<glu::Chunk>> seg_chunks;
+        std::vector<std::vector<glu::DeepRef>> deep_lists;
+        std::vector<i64> deep_pos;
+        i64 epoch_ctr = 0;
         while (true) {
             i64 k0 = next.fetch_add(block);
             if (k0 >= n) break;
@@ -475,13 +510,20 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                 // group by phase; stable keeps ascending source order inside a phase
                 std::stable_sort(raw.begin(), raw.end(),
                                  [](const RawChunk &a, const RawChunk &b) { return a.lvl < b.lvl; });
-                if ((i64)hist.size() < len) hist.assign(len, 0);
+                if ((i64)hist.size() < len) {
+                    hist.assign(len, 0);
+                    deepidx.assign(len, -1);
+                    stamp.assign(len, -1);
+                    seg_of.assign(len, -1);
+                }
                 size_t g0 = 0;
                 while (g0 < raw.size()) {
                     size_t g1 = g0;
                     while (g1 < raw.size() && raw[g1].lvl == raw[g0].lvl) g1++;
+                    const i32 lvl = raw[g0].lvl;
+                    const i64 T = Tp[lvl];
                     // MAC histogram over destination positions
-                    i64 pmin = len, pmax = -1, macs = 0;
+                    i64 pmin = len, pmax = -1;
                     for (size_t c = g0; c < g1; c++) {
                         const RawChunk &ch = raw[c];
                         for (i32 t = 0; t < ch.cnt; t++) {
@@ -490,14 +532,22 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                             pmin = std::min<i64>(pmin, pos);
                             pmax = std::max<i64>(pmax, pos);
                         }
-                        macs += ch.cnt;
                     }
-                    // greedy segmentation of [pmin, pmax] into item ranges
+                    // deep targets: positions with >= D MACs in this phase
+                    deep_pos.clear();
+                    for (i64 pos = pmin; pos <= pmax; pos++)
+                        if (hist[pos] >= D) {
+                            deepidx[pos] = (i64)deep_pos.size();
+                            deep_pos.push_back(pos);
+                        }
+                    if ((i64)deep_lists.size() < (i64)deep_pos.size()) deep_lists.resize(deep_pos.size());
+                    for (size_t x = 0; x < deep_pos.size(); x++) deep_lists[x].clear();
+                    // greedy segmentation of the remaining positions into items
                     std::vector<i64> cuts;  // segment starts
                     cuts.push_back(pmin);
                     i64 acc = 0;
                     for (i64 pos = pmin; pos <= pmax; pos++) {
-                        i64 h = hist[pos];
+                        i64 h = deepidx[pos] >= 0 ? 0 : hist[pos];
                         if (h == 0) continue;
                         if ((acc > 0 && acc + h > T) || pos - cuts.back() >= kMaxSpan) {
                             cuts.push_back(pos);
@@ -505,43 +555,89 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                         }
                         acc += h;
                     }
-                    for (i64 pos = pmin; pos <= pmax; pos++) hist[pos] = 0;
                     cuts.push_back(pmax + 1);
                     size_t nseg = cuts.size() - 1;
-                    // split chunks at segment boundaries; emit items
-                    std::vector<std::vector<RawChunk>> seg_chunks(nseg);
+                    {
+                        size_t s = 0;
+                        for (i64 pos = pmin; pos <= pmax; pos++) {
+                            while (pos >= cuts[s + 1]) s++;
+                            seg_of[pos] = (i64)s;
+                        }
+                    }
+                    if (seg_chunks.size() < nseg) seg_chunks.resize(nseg);
+                    for (size_t s = 0; s < nseg; s++) seg_chunks[s].clear();
+                    // split chunks at segment boundaries and around deep targets
                     for (size_t c = g0; c < g1; c++) {
                         const RawChunk &ch = raw[c];
                         i32 t = 0;
-                        size_t s = 0;
                         while (t < ch.cnt) {
                             i32 pos = posmap[row_idx[ch.p0 + t]];
-                            while (pos >= cuts[s + 1]) s++;
+                            if (deepidx[pos] >= 0) {
+                                deep_lists[deepidx[pos]].push_back({ch.p0 + t, ch.d, ch.m, 0});
+                                t++;
+                                continue;
+                            }
+                            const i64 s = seg_of[pos];
                             i32 t1 = t + 1;
-                            while (t1 < ch.cnt && posmap[row_idx[ch.p0 + t1]] < cuts[s + 1]) t1++;
-                            seg_chunks[s].push_back({ch.lvl, ch.m, ch.d, ch.p0 + t, t1 - t});
+                            while (t1 < ch.cnt) {
+                                i32 p2 = posmap[row_idx[ch.p0 + t1]];
+                                if (deepidx[p2] >= 0 || seg_of[p2] != s) break;
+                                t1++;
+                            }
+                            seg_chunks[s].push_back({ch.m, ch.d, ch.p0 + t, t1 - t});
                             t = t1;
                         }
                     }
+                    for (size_t x = 0; x < deep_pos.size(); x++) {
+                        LocalItem it;
+                        it.lvl = lvl;
+                        it.k = (i32)k;
+                        it.kind = glu::kDeep;
+                        it.base = cb + deep_pos[x];
+                        it.span = 1;
+                        it.macs = (i64)deep_lists[x].size();
+                        it.c0 = (i64)o.deep.size();
+                        o.deep.insert(o.deep.end(), deep_lists[x].begin(), deep_lists[x].end());
+                        it.c1 = (i64)o.deep.size();
+                        o.items.push_back(it);
+                    }
                     for (size_t s = 0; s < nseg; s++) {
-                        if (seg_chunks[s].empty()) continue;
-                        // tighten the segment to the positions actually touched
+                        auto &sc = seg_chunks[s];
+                        if (sc.empty()) continue;
+                        // tighten the segment to the positions actually touched; epochs
                         i64 lo = cuts[s + 1], hi = cuts[s] - 1, sm = 0;
-                        for (auto &ch : seg_chunks[s]) {
+                        i64 ep = ++epoch_ctr;
+                        bool first = true;
+                        for (auto &ch : sc) {
                             lo = std::min<i64>(lo, posmap[row_idx[ch.p0]]);
-                            hi = std::max<i64>(hi, posmap[row_idx[ch.p0 + ch.cnt - 1]]);
-                            sm += ch.cnt;
+                            hi = std::max<i64>(hi, posmap[row_idx[ch.p0 + ch.meta - 1]]);
+                            sm += ch.meta;
+                            bool clash = false;
+                            for (i32 t = 0; t < ch.meta && !clash; t++)
+                                clash = stamp[posmap[row_idx[ch.p0 + t]]] == ep;
+                            if (clash) {
+                                ep = ++epoch_ctr;
+                            }
+                            for (i32 t = 0; t < ch.meta; t++) stamp[posmap[row_idx[ch.p0 + t]]] = ep;
+                            if (clash || first) ch.meta |= glu::kEpochBit;
+                            first = false;
                         }
                         LocalItem it;
-                        it.lvl = raw[g0].lvl;
+                        it.lvl = lvl;
                         it.k = (i32)k;
+                        it.kind = glu::kPush;
                         it.base = cb + lo;
                         it.span = (i32)(hi - lo + 1);
                         it.macs = sm;
                         it.c0 = (i64)o.chunks.size();
-                        o.chunks.insert(o.chunks.end(), seg_chunks[s].begin(), seg_chunks[s].end());
+                        o.chunks.insert(o.chunks.end(), sc.begin(), sc.end());
                         it.c1 = (i64)o.chunks.size();
                         o.items.push_back(it);
+                    }
+                    for (i64 pos = pmin; pos <= pmax; pos++) {
+                        hist[pos] = 0;
+                        deepidx[pos] = -1;
+                        seg_of[pos] = -1;
                     }
                     g0 = g1;
                 }
@@ -563,19 +659,24 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         return GLU_MISMATCH;
     }
 
-    // Global, thread-independent order: phase, then MACs descending (largest
-    // items go first in the static warp round-robin), then column, then base.
-    struct Ref { i32 lvl; i32 tid; i64 idx; };
+    // Global, thread-independent order: phase, then estimated cost
+    // descending (the longest items go first in the static warp round-robin;
+    // a deep item's serial chain costs ~8x a push item's MAC), then column,
+    // then base.
+    struct Ref { i32 lvl; i32 tid; i64 idx; i64 cost; };
     std::vector<Ref> refs;
     size_t total_items = 0;
     for (auto &o : outs) total_items += o.items.size();
     refs.reserve(total_items);
     for (int t = 0; t < nt; t++)
-        for (i64 i = 0; i < (i64)outs[t].items.size(); i++) refs.push_back({outs[t].items[i].lvl, t, i});
+        for (i64 i = 0; i < (i64)outs[t].items.size(); i++) {
+            const LocalItem &x = outs[t].items[i];
+            refs.push_back({x.lvl, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs});
+        }
     std::sort(refs.begin(), refs.end(), [&](const Ref &a, const Ref &b) {
+        if (a.lvl != b.lvl) return a.lvl < b.lvl;
+        if (a.cost != b.cost) return a.cost > b.cost;
         const LocalItem &x = outs[a.tid].items[a.idx], &y = outs[b.tid].items[b.idx];
-        if (x.lvl != y.lvl) return x.lvl < y.lvl;
-        if (x.macs != y.macs) return x.macs > y.macs;
         if (x.k != y.k) return x.k < y.k;
         return x.base < y.base;
     });
@@ -588,19 +689,29 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         const LocalItem &x = outs[r.tid].items[r.idx];
         plan->level_item_ptr[x.lvl + 1]++;
         glu::Item it{};
-        it.map_off = map_off;
         it.base = (i32)x.base;
         it.span = x.span;
-        it.c0 = (i32)plan->chunks.size();
-        for (i64 c = x.c0; c < x.c1; c++) {
-            const RawChunk &rc = outs[r.tid].chunks[c];
-            plan->chunks.push_back({rc.m, rc.d, rc.p0, rc.cnt});
-        }
-        it.c1 = (i32)plan->chunks.size();
         it.macs = (i32)x.macs;
-        map_off += x.macs;
+        it.kind = x.kind;
+        if (x.kind == glu::kDeep) {
+            it.map_off = (i64)plan->deep.size();
+            it.c0 = it.c1 = 0;
+            plan->deep.insert(plan->deep.end(), outs[r.tid].deep.begin() + x.c0,
+                              outs[r.tid].deep.begin() + x.c1);
+            plan->n_deep_items++;
+        } else {
+            it.map_off = map_off;
+            it.c0 = (i32)plan->chunks.size();
+            for (i64 c = x.c0; c < x.c1; c++) {
+                const glu::Chunk &ch = outs[r.tid].chunks[c];
+                if (ch.meta & glu::kEpochBit) plan->n_epochs++;
+                plan->chunks.push_back(ch);
+            }
+            it.c1 = (i32)plan->chunks.size();
+            map_off += x.macs;
+            plan->max_chunks = std::max<i64>(plan->max_chunks, x.c1 - x.c0);
+        }
         plan->max_item_macs = std::max<i64>(plan->max_item_macs, x.macs);
-        plan->max_chunks = std::max<i64>(plan->max_chunks, x.c1 - x.c0);
         plan->items.push_back(it);
     }
     for (i64 l = 0; l < n_levels; l++) plan->level_item_ptr[l + 1] += plan->level_item_ptr[l];
@@ -619,29 +730,42 @@ extern "C" void glu_plan_info(const glu_plan *p, int64_t *info) {
     info[0] = p->n_levels;
     info[1] = (i64)p->items.size();
     info[2] = (i64)p->chunks.size();
-    info[3] = p->n_map;
+    info[3] = p->n_map + (i64)p->deep.size();
     info[4] = p->max_item_macs;
     info[5] = p->max_chunks;
     info[6] = p->deferred;
     info[7] = (i64)(p->items.size() * sizeof(glu::Item) + p->chunks.size() * sizeof(glu::Chunk) +
-                    p->level_item_ptr.size() * sizeof(i64) + p->n_map * sizeof(uint16_t));
+                    p->level_item_ptr.size() * sizeof(i64) + p->n_map * sizeof(uint16_t) +
+                    p->deep.size() * sizeof(glu::DeepRef));
+    info[8] = p->n_deep_items;
+    info[9] = (i64)p->deep.size();
+    info[10] = p->n_epochs;
+    info[11] = p->n_map;
 }
 
 extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
-                                int64_t *chunks) {
+                                int64_t *chunks, int64_t *deep) {
     if (level_item_ptr)
         std::memcpy(level_item_ptr, p->level_item_ptr.data(), p->level_item_ptr.size() * sizeof(i64));
     if (items)
         for (size_t i = 0; i < p->items.size(); i++) {
             const glu::Item &it = p->items[i];
-            i64 *o = items + 6 * i;
-            o[0] = it.map_off; o[1] = it.base; o[2] = it.span; o[3] = it.c0; o[4] = it.c1; o[5] = it.macs;
+            i64 *o = items + 7 * i;
+            o[0] = it.map_off; o[1] = it.base; o[2] = it.span; o[3] = it.c0; o[4] = it.c1;
+            o[5] = it.macs; o[6] = it.kind;
         }
     if (chunks)
         for (size_t i = 0; i < p->chunks.size(); i++) {
             const glu::Chunk &c = p->chunks[i];
-            i64 *o = chunks + 4 * i;
-            o[0] = c.m; o[1] = c.d; o[2] = c.p0; o[3] = c.cnt;
+            i64 *o = chunks + 5 * i;
+            o[0] = c.m; o[1] = c.d; o[2] = c.p0; o[3] = c.meta & ~glu::kEpochBit;
+            o[4] = (c.meta & glu::kEpochBit) ? 1 : 0;
+        }
+    if (deep)
+        for (size_t i = 0; i < p->deep.size(); i++) {
+            const glu::DeepRef &r = p->deep[i];
+            i64 *o = deep + 3 * i;
+            o[0] = r.l; o[1] = r.d; o[2] = r.m;
         }
 }
 
@@ -657,6 +781,8 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.chunks = p->chunks.data();
     v.n_chunks = (i64)p->chunks.size();
     v.n_map = p->n_map;
+    v.deep = p->deep.data();
+    v.n_deep = (i64)p->deep.size();
     return v;
 }
 }  // namespace glu

@@ -128,7 +128,7 @@ class Factorizer:
     """
 
     def __init__(self, fp: FilledPattern, level_of: np.ndarray, contract: int,
-                 max_item_macs: int = 0, threads: int = 0):
+                 max_item_macs: int = 0, threads: int = 0, deep_min: int = 0):
         self.n = fp.n
         self.nnz = fp.nnz
         self.contract = contract
@@ -137,15 +137,16 @@ class Factorizer:
         lv = _lib.i64(level_of)
         plan = ctypes.c_void_p()
         rc = _lib.check(_lib.lib.glu_plan_build(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
-                                                _lib.ptr(lv), contract, max_item_macs, threads,
-                                                ctypes.byref(plan)), "glu_plan_build")
+                                                _lib.ptr(lv), contract, max_item_macs, deep_min,
+                                                threads, ctypes.byref(plan)), "glu_plan_build")
         if rc == _lib.GLU_MISMATCH:
             raise PatternMismatchError("update targeted a structurally absent slot")
         try:
-            info = np.zeros(8, dtype=np.int64)
+            info = np.zeros(12, dtype=np.int64)
             _lib.lib.glu_plan_info(plan, _lib.ptr(info))
             self.plan_info = dict(zip(("levels", "items", "chunks", "macs", "max_item_macs",
-                                       "max_chunks", "deferred_macs", "plan_bytes"),
+                                       "max_chunks", "deferred_macs", "plan_bytes", "deep_items",
+                                       "deep_macs", "epochs", "push_macs"),
                                       info.tolist()))
             h = ctypes.c_void_p()
             rc = _lib.check(_lib.lib.glu_create(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
@@ -255,7 +256,9 @@ def _stream(s):
 
 
 _CACHE: dict = {}
-_CACHE_LOCK = threading.Lock()
+# re-entrant: a weakref callback (_drop) can fire from GC while
+# get_factorizer holds the lock and allocates
+_CACHE_LOCK = threading.RLock()
 
 
 def _digest(a: np.ndarray) -> bytes:

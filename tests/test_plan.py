@@ -19,22 +19,23 @@ from paper_1908_00204_b200 import _lib
 from conftest import csc_from_golden, load_golden
 
 
-def export_plan(fp, level_of, contract, max_item_macs=0):
+def export_plan(fp, level_of, contract, max_item_macs=0, deep_min=0):
     cp, ri, dp = _lib.i64(fp.full.col_ptr), _lib.i64(fp.full.row_idx), _lib.i64(fp.diag_pos)
     lv = _lib.i64(level_of)
     h = ctypes.c_void_p()
     rc = _lib.lib.glu_plan_build(fp.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp), _lib.ptr(lv),
-                                 contract, max_item_macs, 2, ctypes.byref(h))
+                                 contract, max_item_macs, deep_min, 2, ctypes.byref(h))
     assert rc == _lib.GLU_OK, _lib.last_error()
-    info = np.zeros(8, dtype=np.int64)
+    info = np.zeros(12, dtype=np.int64)
     _lib.lib.glu_plan_info(h, _lib.ptr(info))
-    nl, ni, nc = int(info[0]), int(info[1]), int(info[2])
+    nl, ni, nc, nd = int(info[0]), int(info[1]), int(info[2]), int(info[9])
     lip = np.zeros(nl + 1, dtype=np.int64)
-    items = np.zeros((max(ni, 1), 6), dtype=np.int64)
-    chunks = np.zeros((max(nc, 1), 4), dtype=np.int64)
-    _lib.lib.glu_plan_export(h, _lib.ptr(lip), _lib.ptr(items), _lib.ptr(chunks))
+    items = np.zeros((max(ni, 1), 7), dtype=np.int64)
+    chunks = np.zeros((max(nc, 1), 5), dtype=np.int64)
+    deep = np.zeros((max(nd, 1), 3), dtype=np.int64)
+    _lib.lib.glu_plan_export(h, _lib.ptr(lip), _lib.ptr(items), _lib.ptr(chunks), _lib.ptr(deep))
     _lib.lib.glu_plan_free(h)
-    return dict(info=info, lip=lip, items=items[:ni], chunks=chunks[:nc])
+    return dict(info=info, lip=lip, items=items[:ni], chunks=chunks[:nc], deep=deep[:nd])
 
 
 def emulate(fp, level_of, plan, v, thresh, rng=None):
@@ -46,13 +47,23 @@ def emulate(fp, level_of, plan, v, thresh, rng=None):
         if rng is not None:
             rng.shuffle(order)  # items of a phase are independent
         for it in order:
-            moff, base, span, c0, c1, macs = items[it]
+            moff, base, span, c0, c1, macs, kind = items[it]
+            if kind == 1:  # deep: one target, ordered contributions
+                for l_, d, m in plan["deep"][moff:moff + macs]:
+                    v[base] = v[base] - (v[l_] / v[d]) * v[m]
+                continue
             seg = ri[base:base + span]
-            for m, d, p0, cnt in chunks[c0:c1]:
+            touched = set()
+            for m, d, p0, cnt, ep in chunks[c0:c1]:
                 p = np.arange(p0, p0 + cnt)
                 off = np.searchsorted(seg, ri[p])
                 assert np.array_equal(seg[off], ri[p])
                 q = base + off
+                # a chunk that re-touches a target of its epoch must open a new one
+                if ep:
+                    touched = set()
+                assert touched.isdisjoint(q.tolist())
+                touched.update(q.tolist())
                 v[q] = v[q] - (v[p] / v[d]) * v[m]
     fail = None
     cp, dp = fp.full.col_ptr, fp.diag_pos
@@ -78,18 +89,21 @@ CASES = ["conflict8", "random_dd_s2_n80", "random_dd_s3_n120", "random_dd_s5_n10
 
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("contract", [_lib.CONTRACT_A, _lib.CONTRACT_B])
-@pytest.mark.parametrize("max_item_macs", [0, 7])
-def test_plan_emulation_bitwise(case, contract, max_item_macs):
+@pytest.mark.parametrize("max_item_macs,deep_min", [(0, 0), (7, 0), (0, 2), (5, 1000)])
+def test_plan_emulation_bitwise(case, contract, max_item_macs, deep_min):
     g = load_golden(case)
     a = csc_from_golden(g)
     fp = glu.symbolic_fillin(a.pattern)
     level_of = g["level_of"]
-    plan = export_plan(fp, level_of, contract, max_item_macs)
-    assert int(plan["info"][3]) == glu.pattern_flops(fp)[0]  # one map entry per MAC
+    plan = export_plan(fp, level_of, contract, max_item_macs, deep_min)
+    assert int(plan["info"][3]) == glu.pattern_flops(fp)[0]  # every MAC planned once
+    assert int(plan["info"][11]) + int(plan["info"][9]) == int(plan["info"][3])
+    push = plan["items"][plan["items"][:, 6] == 0]
+    assert int(push[:, 5].sum()) == int(plan["info"][11])
     if max_item_macs:
-        one_pos = plan["items"][:, 5] > max_item_macs
+        one_pos = push[:, 5] > max_item_macs
         # only items whose MACs all hit one position may exceed the bound
-        for it in plan["items"][one_pos]:
+        for it in push[one_pos]:
             assert it[2] == 1
     v = np.zeros(fp.nnz)
     from oracle import oracle as orc
