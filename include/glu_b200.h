@@ -103,31 +103,34 @@ int64_t glu_find_hazards(int64_t n, const int64_t *col_ptr, const int64_t *row_i
    (the precomputed replacement of the runtime merge search in
    _kernels.py:107-115 / :140-148 and of the ownership split of
    numeric.py:295-315).  contract: GLU_CONTRACT_A or GLU_CONTRACT_B.
-   max_item_macs fixes the MACs one push item carries (0 = adaptive per
-   phase); deep_min is the MAC count from which a target becomes its own
-   register-chained item (0 = default 8).  Returns GLU_OK or GLU_MISMATCH
-   when an update targets a slot absent from the pattern (the condition
-   _kernels.py:113-114 reports at run time). */
+   max_item_macs caps the MACs one push item carries (0 = adaptive per
+   phase, 32..128); deep_min is the MAC count from which a target becomes
+   its own register-chained item (0 = default 8).  Returns GLU_OK or
+   GLU_MISMATCH when an update targets a slot absent from the pattern (the
+   condition _kernels.py:113-114 reports at run time). */
 int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                        const int64_t *diag_pos, const int64_t *level_of, int32_t contract,
                        int64_t max_item_macs, int64_t deep_min, int32_t n_threads,
                        glu_plan **out);
-/* info[0..11] = n_levels, n_items, n_chunks, MACs, max_item_macs,
+/* info[0..15] = n_levels, n_items, n_chunks, MACs, max_item_macs,
    max_chunks_per_item, deferred_macs (contract A), plan bytes, deep items,
-   deep MACs, epochs, push MACs (= uint16 map entries) */
+   deep MACs, epochs, push MACs (= u8 map entries), target-list entries,
+   0, 0, 0 */
 void glu_plan_info(const glu_plan *p, int64_t *info);
 /* level_item_ptr[n_levels+1];
-   items[n_items*7]  = {map_off, base, span, c0, c1, macs, kind (0 push, 1 deep)};
-   chunks[n_chunks*5] = {m, d, p0, cnt, epoch_start};
-   deep[deep_macs*3]  = {l, d, m}  (all slots absolute). */
+   items[n_items*8]   = {map_off, tgt_off, base, c0, nch, ntgt, macs, kind (0 push, 1 deep)};
+   chunks[n_chunks*5] = {m (multiplier slot), j (source column), p0, cnt, epoch_start};
+   deep[deep_macs*3]  = {l, d, m}  (all slots absolute);
+   map8[push_macs]    = per MAC, index into its item's target list;
+   tgt[targets]       = target offsets from the item's base.  Any pointer may be NULL. */
 void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
-                     int64_t *chunks, int64_t *deep);
+                     int64_t *chunks, int64_t *deep, uint8_t *map8, int64_t *tgt);
 void glu_plan_free(glu_plan *p);
 
 /* ---- device handle ---------------------------------------------------- */
 
-/* Uploads pattern, level schedule and plan to the current CUDA device and
-   builds the uint16 scatter map on the device.  Replaces the per-call
+/* Uploads pattern, level schedule and plan (with its u8 scatter map) to the
+   current CUDA device.  Replaces the per-call
    setup of numeric.py:241-317 (caps, workspaces, crew). */
 int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                    const int64_t *diag_pos, const int64_t *row_ptr, const int64_t *col_idx,
@@ -139,6 +142,12 @@ void glu_destroy(glu_handle *h);
    failing-pivot order: 0 = earliest level then min column (factor_parallel,
    numeric.py:279-285), 1 = min column (sequential paths, numeric.py:129-159). */
 int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value);
+/* Diagnostics: glu_set_option(h, 3, first_phase) and (h, 4, n_phases)
+   record, for every item of those phases, 8 words {item | phase << 32,
+   warp, t_start, t_static_loaded, t_wait_done, t_values_loaded,
+   t_stored, 0} (%globaltimer ns) in the next factorization; read them
+   with glu_trace_read (returns the record count). */
+int64_t glu_trace_read(glu_handle *h, int64_t *out, int64_t max_records);
 /* Per-level milliseconds of the last timed factorization; returns count. */
 int64_t glu_level_times(const glu_handle *h, double *ms, int64_t len);
 /* info[0..11]: n, nnz, n_levels, n_items, n_chunks, macs, device bytes,

@@ -46,10 +46,14 @@ namespace {
 
 constexpr int kThreads = 512;  // 16 warps per CTA
 constexpr int kWarps = kThreads / 32;
+constexpr int kLineWords = 32;   // u32 stride between hot words (one 128 B line each)
+constexpr int kColRep = 4;       // replicas of each column's completion counter (spread the pollers)
+constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s: a dependency wait this long is a bug
 
 // ---------------------------------------------------------------------------
-// grid barrier: monotonically increasing arrival counter, release on arrive,
-// acquire on the spin.  Co-residency is guaranteed by the cooperative launch.
+// grid barrier (solve kernel): monotonically increasing arrival counter,
+// release on arrive, acquire on the spin.  Co-residency is guaranteed by the
+// cooperative launch.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int target) {
     __syncthreads();
@@ -64,149 +68,412 @@ __device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int t
     __syncthreads();
 }
 
-__device__ __forceinline__ double ldv(const double *p) { return __ldcg(p); }
-__device__ __forceinline__ void stv(double *p, double x) { __stcg(p, x); }
-
-struct FactorParams {
-    double *v;
-    const i32 *level_item_ptr;
-    const Item *items;
-    const Chunk *chunks;
-    const uint16_t *map;
-    const glu::DeepRef *deep;
-    const i32 *col_ptr;
-    const i32 *diag_pos;
-    const i32 *level_of;
-    i32 n;
-    i32 n_levels;
-    double thresh;
-    unsigned long long *fail;  // min (level << 32 | column) of failing pivots
-    unsigned int *bar;
-    unsigned long long *level_ns;  // optional per-phase end timestamps
-    i32 fail_by_column;            // 1: key = column only (sequential API semantics)
-};
+// L2 residency: the values (A_s, 8 B x nnz, e.g. 34 MB for cfg2) are read
+// and written with an evict_last policy and the plan streams (items, chunks,
+// maps, deep refs: ~1.3 GB for cfg2, read once per factorization) with
+// evict_first, so the plan does not push the values out of the 126 MB L2.
+// Value accesses are .cg (L2, coherent point for the dataflow sync).
+__device__ __forceinline__ uint64_t pol_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ldv(const double *p) {
+    double x;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(x) : "l"(p), "l"(pol_last()));
+    return x;
+}
+__device__ __forceinline__ void stv(double *p, double x) {
+    asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(x), "l"(pol_last())
+                 : "memory");
+}
+// read-only plan streams
+__device__ __forceinline__ int4 ldp(const int4 *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol_first()));
+    return r;
+}
+__device__ __forceinline__ int ldp8(const uint8_t *p) {
+    unsigned short r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+                 : "=h"(r) : "l"(p), "l"(pol_first()));
+    return (int)r;
+}
+__device__ __forceinline__ int ldp16(const uint16_t *p) {
+    unsigned short r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+                 : "=h"(r) : "l"(p), "l"(pol_first()));
+    return (int)r;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-
-// kPush item: ordered chunks into one destination segment.  The chunk
-// descriptors of a window of <= 32 chunks are fetched lane-parallel (with
-// their pivots and multipliers: none of them is written during the phase),
-// then the window's entries are flattened over the lanes 32 at a time.
-// Entries of one epoch hit distinct targets, so a round's read-modify-writes
-// run in parallel; a round that straddles an epoch boundary applies its
-// epochs in order with a warp barrier between them.  The next round's map
-// and L loads are issued before the current round's target RMW.
-struct Round {
-    int q;        // target offset in the segment (-1: lane idle)
-    int ep;       // epoch of the entry inside the window
-    double l;     // A_s(i,j), undivided
-    double pv;    // pivot A_s(j,j)
-    double mu;    // multiplier U(j,k)
+struct FactorParams {
+    double *v;
+    const Item *items;
+    const Chunk *chunks;
+    const uint8_t *map8;
+    const uint16_t *tgt16;
+    const glu::DeepRef *deep;
+    const i32 *col_ptr;
+    const i32 *diag_pos;
+    const i32 *level_of;
+    const i32 *level_need;  // items per phase
+    i32 n;
+    i32 n_items;
+    i32 n_levels;
+    double thresh;
+    unsigned long long *fail;  // min (level << 32 | column) of failing pivots
+    unsigned *done;            // per phase: completed items (stride 8 words)
+    unsigned *col_done;        // per column: completed items into it
+    const i32 *col_total;      // per column: items into it
+    int *err;                  // watchdog flag
+    unsigned long long *level_ns;  // optional per-phase completion timestamps
+    unsigned long long *trace;     // optional per-item timestamps (diagnostics)
+    i32 trace_i0, trace_i1;        // traced item range
+    i32 fail_by_column;            // 1: key = column only (sequential API semantics)
 };
 
-__device__ __forceinline__ void load_round(const FactorParams &P, const uint16_t *mp, int rbase,
-                                           int wtot, int lane, int nch, int incl, int p0, int est,
-                                           double piv, double mult, int myep, Round &R) {
-    const int e = rbase + lane;
-    // chunk of entry e: chunks starting in (rbase, rbase+32) split the round
+// ---------------------------------------------------------------------------
+// Dataflow synchronisation (replaces a grid barrier per level).
+//
+// Items are ordered by phase and dealt round-robin to the warps; a warp runs
+// its items in order and, on entering phase l, waits until every phase < l
+// is complete -- a point-to-point wait instead of a grid-wide barrier, so a
+// warp with nothing to do in phase l runs ahead to its next item and loads
+// its static plan data early.
+//   producer  when a warp leaves phase l it adds the number of items it ran
+//             there to done[l]: fence.acq_rel + fire-and-forget red.add.
+//   consumer  each CTA keeps `known` in shared memory = the number of
+//             leading phases known complete.  At most one warp per CTA polls
+//             at a time: lanes read done[known .. known+31] (relaxed) in one
+//             round trip, compare with the static item counts and advance
+//             `known` over the complete prefix (phases without items are
+//             complete by definition), then fence.acq_rel.  The other warps
+//             of the CTA spin on shared memory.
+// No deadlock: the smallest unfinished item's warp has finished all its
+// earlier items and every item it waits on has a smaller index.  A
+// watchdog turns an endless wait (a bug) into an error instead of a hang.
+// ---------------------------------------------------------------------------
+struct CtaSync {
+    unsigned known;   // phases [0, known) complete
+    int polling;      // a warp of this CTA has a poll in flight
+};
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_add_relaxed(unsigned *p, unsigned x) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+
+// wait until phases [0, w] are complete
+__device__ __noinline__ bool wait_phase_impl(const unsigned *done, const i32 *level_need, int n_levels,
+                                             int *err, int w, int lane, CtaSync *cs) {
+    const unsigned target = (unsigned)w + 1;
+    unsigned long long t0 = 0;
+    volatile unsigned *vk = &cs->known;
+    for (int spin = 0;; ++spin) {
+        if (*vk >= target) break;
+        int got = 0;
+        if (lane == 0) got = atomicCAS(&cs->polling, 0, 1) == 0;
+        got = __shfl_sync(0xffffffffu, got, 0);
+        if (got) {
+            const unsigned k0 = *vk;
+            const unsigned k = k0 + lane;
+            bool ok = true;
+            if (k < (unsigned)n_levels) ok = ld_relaxed(done + (size_t)k * 8) >= (unsigned)__ldg(level_need + k);
+            const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+            const unsigned adv = bad ? __ffs(bad) - 1 : 32;
+            if (lane == 0) {
+                fence_acq_rel_gpu();
+                if (adv) atomicMax(&cs->known, k0 + adv);
+                atomicExch(&cs->polling, 0);
+            }
+            __syncwarp();
+            if (k0 + adv >= target) break;
+        } else {
+            __nanosleep(32);
+        }
+        if ((spin & 255) == 255) {
+            int bad = 0;
+            if (lane == 0) {
+                const unsigned long long t = globaltimer();
+                if (t0 == 0) t0 = t;
+                bad = (t - t0 > kWatchdogNs) || *(volatile int *)err;
+                if (bad) atomicExch(err, 1);
+            }
+            if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+        }
+    }
+    if (lane == 0) asm volatile("fence.acq_rel.cta;" ::: "memory");
+    __syncwarp();
+    return true;
+}
+
+__device__ __forceinline__ bool wait_phase(const FactorParams &P, int w, int lane, CtaSync *cs) {
+    return wait_phase_impl(P.done, P.level_need, P.n_levels, P.err, w, lane, cs);
+}
+
+// Item completion.  A consumer of column k waits until every item into k
+// is counted in col_done[k]; a counted item's stores must be visible first
+// (fence.acq_rel.gpu, then the count).  Fences are expensive (~300 ns), so a
+// warp batches: the item into a column that the NEXT phase reads as a source
+// ("critical", the chain of the deep tail) is released at once; the others
+// queue in shared memory and are released together when the warp leaves the
+// phase (or the queue is full) -- never later than the phase counter, so the
+// dependency order and the deadlock-freedom argument are unchanged.
+struct WarpQ {
+    int col[32];
+};
+
+__device__ __forceinline__ void flush_items(const FactorParams &P, WarpQ *q, int &nq, int lvl,
+                                            unsigned ran, bool phase_end, int lane) {
+    __syncwarp();
+    fence_acq_rel_gpu();
+    for (int x = lane; x < nq * kColRep; x += 32)
+        red_add_relaxed(P.col_done + (size_t)q->col[x / kColRep] * kColRep + (x % kColRep), 1);
+    if (phase_end && lane == 0) {
+        unsigned *ctr = P.done + (size_t)lvl * 8;
+        if (P.level_ns) {
+            const unsigned old = atomicAdd(ctr, ran);
+            if (old + ran == (unsigned)__ldg(P.level_need + lvl)) P.level_ns[lvl + 1] = globaltimer();
+        } else {
+            red_add_relaxed(ctr, ran);
+        }
+    }
+    nq = 0;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void finish_item(const FactorParams &P, WarpQ *q, int &nq, int col,
+                                            bool crit, int lvl, unsigned ran, bool phase_end,
+                                            int lane) {
+    if (crit) {
+        __syncwarp();
+        fence_acq_rel_gpu();
+        if (lane < kColRep) red_add_relaxed(P.col_done + (size_t)col * kColRep + lane, 1);
+    } else {
+        if (lane == 0) q->col[nq] = col;
+        ++nq;
+    }
+    if (phase_end || nq == 32) flush_items(P, q, nq, lvl, ran, phase_end, lane);
+}
+
+// Fine-grained wait of a push item in phase lvl: its source columns complete
+// (every item into them counted) and every earlier-phase item into its own
+// column counted.  Skipped when the CTA already knows phases < lvl complete.
+// Relaxed polling: the values are read .cg from L2 after the wait returns,
+// and the producer fenced its stores before counting.  Backs off in
+// proportion to the items still outstanding.
+__device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool has_src, int j,
+                                          unsigned jneed, int k, unsigned kneed, int lvl,
+                                          CtaSync *cs, int rep) {
+    volatile unsigned *vk = &cs->known;
+    unsigned long long t0 = 0;
+    for (int spin = 0;; ++spin) {
+        __nanosleep(32);
+        if (*vk >= (unsigned)lvl) break;
+        unsigned rem = 0;
+        if (has_src) {
+            const unsigned c = ld_relaxed(P.col_done + (size_t)j * kColRep + rep);
+            rem = c >= jneed ? 0u : jneed - c;
+        }
+        if (lane == 0) {
+            const unsigned c = ld_relaxed(P.col_done + (size_t)k * kColRep + rep);
+            rem = max(rem, c >= kneed ? 0u : kneed - c);
+        }
+        const unsigned mx = __reduce_max_sync(0xffffffffu, rem);
+        if (mx == 0) break;
+        if (mx > 4) __nanosleep(min(mx * 32u, 1024u));
+        if ((spin & 255) == 255) {
+            int bad = 0;
+            if (lane == 0) {
+                const unsigned long long t = globaltimer();
+                if (t0 == 0) t0 = t;
+                bad = (t - t0 > kWatchdogNs) || *(volatile int *)P.err;
+                if (bad) atomicExch(P.err, 1);
+            }
+            if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
+// kPush item: <= 32 ordered chunks into <= 256 distinct targets of one
+// destination column.  Everything static -- the chunk descriptors (one per
+// lane), every entry's chunk and target index (u8 map, up to 8 entries per
+// lane) and the target offsets -- is loaded before the phase wait; after it,
+// ONE round of independent loads fetches the targets, the sources' L
+// values, pivots and multipliers.  The targets are staged in shared memory,
+// the MACs applied there epoch by epoch (entries of one epoch hit distinct
+// targets; only epochs are ordered), and every target written back once.
+constexpr int kR = glu::kMaxItemMacs / 32;  // entries per lane
+
+__device__ __forceinline__ int round_chunk(int rbase, int lane, int nch, int est) {
     const unsigned start_bits = __reduce_or_sync(
         0xffffffffu, (lane < nch && est > rbase && est < rbase + 32) ? (1u << (est - rbase)) : 0u);
     const int cfirst = __popc(__ballot_sync(0xffffffffu, lane < nch && est <= rbase)) - 1;
-    const int c = cfirst + __popc(start_bits & ((2u << lane) - 1u));
-    const int cp0 = __shfl_sync(0xffffffffu, p0, c);
-    const int cest = __shfl_sync(0xffffffffu, est, c);
-    R.pv = __shfl_sync(0xffffffffu, piv, c);
-    R.mu = __shfl_sync(0xffffffffu, mult, c);
-    R.ep = __shfl_sync(0xffffffffu, myep, c);
-    R.q = -1;
-    if (e < wtot) {
-        R.q = __ldg(mp + e);
-        R.l = ldv(P.v + cp0 + (e - cest));
-    }
+    return cfirst + __popc(start_bits & ((2u << lane) - 1u));
 }
 
-__device__ __forceinline__ void apply_round(double *vb, const Round &R, int lane) {
-    const int lo = __shfl_sync(0xffffffffu, R.ep, 0);
-    const unsigned act = __ballot_sync(0xffffffffu, R.q >= 0);
-    const int hi = __shfl_sync(0xffffffffu, R.ep, 31 - __clz(act));
-    double prod = 0.0;
-    if (R.q >= 0) prod = __dmul_rn(__ddiv_rn(R.l, R.pv), R.mu);
-    if (lo == hi) {
-        if (R.q >= 0) {
-            double *tp = vb + R.q;
-            stv(tp, __dsub_rn(ldv(tp), prod));
+__device__ __forceinline__ void stamp(unsigned long long *rec, int k, int lane) {
+    if (rec && lane == 0) rec[k] = globaltimer();
+}
+
+__device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, int4 c, int lane,
+                                         CtaSync *cs, double *sg, unsigned long long *rec) {
+    const i64 moff = (i64)(unsigned)a.x | ((i64)a.y << 32);
+    const i64 toff = (i64)(unsigned)a.z | ((i64)a.w << 32);
+    const int base = b.x, c0 = b.y, nch = b.z, ntgt = b.w, macs = c.x;
+    const int lvl = c.y >> 2;
+    const bool check = *(volatile unsigned *)&cs->known < (unsigned)lvl;
+    const int rep = (blockIdx.x + (threadIdx.x >> 5)) % kColRep;
+    unsigned krem = 0, jrem = 0;
+    if (check && lane == 0) {  // first poll of the own-column dependency, in flight early
+        const unsigned x = ld_relaxed(P.col_done + (size_t)c.z * kColRep + rep);
+        krem = x >= (unsigned)c.w ? 0u : (unsigned)c.w - x;
+    }
+    int4 ch = make_int4(0, 0, 0, 0);
+    if (lane < nch) ch = ldp(reinterpret_cast<const int4 *>(P.chunks) + c0 + lane);
+    const int cnt = ch.w & 0x7fffffff;
+    const bool newep = lane == 0 || (lane < nch && (ch.w & glu::kEpochBit));
+    const unsigned epm = __ballot_sync(0xffffffffu, newep);
+    const int myep = __popc(epm & ((2u << lane) - 1u)) - 1;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    const int est = incl - cnt;
+    const int nr = (macs + 31) >> 5, nt = (ntgt + 31) >> 5;
+    int dslot = 0;
+    unsigned jneed = 0;
+    if (lane < nch) {
+        dslot = __ldg(P.diag_pos + ch.y);
+        jneed = (unsigned)__ldg(P.col_total + ch.y);
+        if (check) {
+            const unsigned x = ld_relaxed(P.col_done + (size_t)ch.y * kColRep + rep);
+            jrem = x >= jneed ? 0u : jneed - x;
         }
+    }
+    int u[kR], ci[kR], to[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        u[r] = -1;
+        to[r] = -1;
+        if (r < nr) {
+            ci[r] = round_chunk(32 * r, lane, nch, est);
+            if (32 * r + lane < macs) u[r] = ldp8(P.map8 + moff + 32 * r + lane);
+        }
+        if (r < nt && 32 * r + lane < ntgt) to[r] = ldp16(P.tgt16 + toff + 32 * r + lane);
+    }
+    stamp(rec, 3, lane);
+    if (__reduce_max_sync(0xffffffffu, max(krem, jrem)) != 0 &&
+        !wait_cols(P, lane, lane < nch, ch.y, jneed, c.z, (unsigned)c.w, lvl, cs, rep))
+        return false;
+    stamp(rec, 4, lane);
+    // one round of independent loads
+    double piv = 1.0, mult = 0.0;
+    if (lane < nch) {
+        piv = ldv(P.v + dslot);
+        mult = ldv(P.v + ch.x);
+    }
+    double t[kR], l[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        if (to[r] >= 0) t[r] = ldv(P.v + base + to[r]);
+        if (r < nr) {
+            const int cp0 = __shfl_sync(0xffffffffu, ch.z, ci[r]);
+            const int cest = __shfl_sync(0xffffffffu, est, ci[r]);
+            if (u[r] >= 0) l[r] = ldv(P.v + cp0 + (32 * r + lane - cest));
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kR; ++r)
+        if (to[r] >= 0) sg[32 * r + lane] = t[r];
+    int ep[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        if (r < nr) {
+            const double pv = __shfl_sync(0xffffffffu, piv, ci[r]);
+            const double mu = __shfl_sync(0xffffffffu, mult, ci[r]);
+            ep[r] = __shfl_sync(0xffffffffu, myep, ci[r]);
+            if (u[r] >= 0) l[r] = __dmul_rn(__ddiv_rn(l[r], pv), mu);  // the product
+        }
+    }
+    __syncwarp();
+    stamp(rec, 5, lane);
+    const int nep = __popc(epm);
+    if (nep == 1) {
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+            if (u[r] >= 0) sg[u[r]] = __dsub_rn(sg[u[r]], l[r]);
     } else {
-        for (int ep = lo; ep <= hi; ++ep) {
-            if (R.q >= 0 && R.ep == ep) {
-                double *tp = vb + R.q;
-                stv(tp, __dsub_rn(ldv(tp), prod));
-            }
+        for (int e = 0; e < nep; ++e) {
+#pragma unroll
+            for (int r = 0; r < kR; ++r)
+                if (u[r] >= 0 && ep[r] == e) sg[u[r]] = __dsub_rn(sg[u[r]], l[r]);
             __syncwarp();
         }
     }
     __syncwarp();
-}
-
-__device__ __forceinline__ void run_push(const FactorParams &P, int4 a, int4 b, int lane) {
-    const i64 moff = (i64)(unsigned)a.x | ((i64)a.y << 32);
-    double *vb = P.v + a.z;
-    const uint16_t *mp = P.map + moff;
-    const int c0 = b.x, c1 = b.y;
-    const int4 *cp = reinterpret_cast<const int4 *>(P.chunks);
-    for (int wb = c0; wb < c1; wb += 32) {
-        const int nch = min(32, c1 - wb);
-        int4 ch = make_int4(0, 0, 0, 0);
-        double piv = 1.0, mult = 0.0;
-        if (lane < nch) {
-            ch = __ldg(cp + wb + lane);
-            piv = ldv(P.v + ch.y);
-            mult = ldv(P.v + ch.x);
-        }
-        const int cnt = ch.w & 0x7fffffff;
-        const bool newep = lane == 0 || (lane < nch && (ch.w & glu::kEpochBit));
-        const unsigned epm = __ballot_sync(0xffffffffu, newep);
-        const int myep = __popc(epm & ((2u << lane) - 1u)) - 1;
-        // inclusive prefix of chunk sizes -> exclusive starts
-        int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int x = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += x;
-        }
-        const int est = incl - cnt;
-        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-        Round cur, nxt;
-        load_round(P, mp, 0, wtot, lane, nch, incl, ch.z, est, piv, mult, myep, cur);
-        for (int rb = 0; rb < wtot; rb += 32) {
-            if (rb + 32 < wtot)
-                load_round(P, mp, rb + 32, wtot, lane, nch, incl, ch.z, est, piv, mult, myep, nxt);
-            apply_round(vb, cur, lane);
-            cur = nxt;
-        }
-        mp += wtot;
-    }
+    for (int r = 0; r < kR; ++r)
+        if (to[r] >= 0) stv(P.v + base + to[r], sg[32 * r + lane]);
+    __syncwarp();
+    stamp(rec, 6, lane);
+    return true;
 }
 
 // kDeep item: one target, many ordered contributions.  Lanes form 32
 // products at a time (independent roundings); every lane then replays the
 // subtraction chain in order from shuffles, so the target sees exactly the
-// reference's sequence of roundings with one load and one store.
-__device__ __forceinline__ void run_deep(const FactorParams &P, int4 a, int4 b, int lane) {
+// reference's sequence of roundings with one load and one store.  The next
+// group's operands are loaded before the current group's chain.
+__device__ __forceinline__ bool run_deep(const FactorParams &P, int4 a, int4 b, int4 c_, int lane,
+                                         CtaSync *cs, int wait_l) {
     const i64 off = (i64)(unsigned)a.x | ((i64)a.y << 32);
-    const int macs = b.z;
+    const int macs = c_.x;
     const int4 *dr = reinterpret_cast<const int4 *>(P.deep) + off;
-    double *tp = P.v + a.z;
+    double *tp = P.v + b.x;
+    // operands of groups g .. g+3 in flight (q0 = current group)
+    int4 r0 = make_int4(0, 0, 0, 0), r1 = r0, r2 = r0, r3 = r0;
+    if (lane < macs) r0 = ldp(dr + lane);
+    if (32 + lane < macs) r1 = ldp(dr + 32 + lane);
+    if (64 + lane < macs) r2 = ldp(dr + 64 + lane);
+    if (96 + lane < macs) r3 = ldp(dr + 96 + lane);
+    if (wait_l >= 0 && !wait_phase(P, wait_l, lane, cs)) return false;
     double acc = ldv(tp);
+    double l0 = 0.0, d0 = 1.0, m0 = 0.0, l1 = 0.0, d1 = 1.0, m1 = 0.0;
+    double l2 = 0.0, d2 = 1.0, m2 = 0.0, l3 = 0.0, d3 = 1.0, m3 = 0.0;
+    if (lane < macs) { l0 = ldv(P.v + r0.x); d0 = ldv(P.v + r0.y); m0 = ldv(P.v + r0.z); }
+    if (32 + lane < macs) { l1 = ldv(P.v + r1.x); d1 = ldv(P.v + r1.y); m1 = ldv(P.v + r1.z); }
+    if (64 + lane < macs) { l2 = ldv(P.v + r2.x); d2 = ldv(P.v + r2.y); m2 = ldv(P.v + r2.z); }
+    if (96 + lane < macs) { l3 = ldv(P.v + r3.x); d3 = ldv(P.v + r3.y); m3 = ldv(P.v + r3.z); }
     for (int r = 0; r < macs; r += 32) {
-        double prod = 0.0;
-        if (r + lane < macs) {
-            const int4 c = __ldg(dr + r + lane);
-            prod = __dmul_rn(__ddiv_rn(ldv(P.v + c.x), ldv(P.v + c.y)), ldv(P.v + c.z));
+        const double prod = __dmul_rn(__ddiv_rn(l0, d0), m0);
+        l0 = l1; d0 = d1; m0 = m1;
+        l1 = l2; d1 = d2; m1 = m2;
+        l2 = l3; d2 = d3; m2 = m3;
+        if (r + 128 + lane < macs) {
+            const int4 rn = ldp(dr + r + 128 + lane);
+            l3 = ldv(P.v + rn.x); d3 = ldv(P.v + rn.y); m3 = ldv(P.v + rn.z);
         }
         const int cnt = min(32, macs - r);
         if (cnt == 32) {
@@ -217,13 +484,7 @@ __device__ __forceinline__ void run_deep(const FactorParams &P, int4 a, int4 b, 
         }
     }
     if (lane == 0) stv(tp, acc);
-}
-
-__device__ __forceinline__ void run_item(const FactorParams &P, int idx, int lane) {
-    const int4 *ip = reinterpret_cast<const int4 *>(P.items + idx);
-    const int4 a = __ldg(ip), b = __ldg(ip + 1);
-    if (b.w == glu::kDeep) run_deep(P, a, b, lane);
-    else run_push(P, a, b, lane);
+    return true;
 }
 
 // Pivot check + divide of column j (_kernels.py:152-173): cmax over the
@@ -257,50 +518,66 @@ __device__ __forceinline__ void divide_column(const FactorParams &P, int j, int 
 
 __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    // consecutive items go to consecutive SMs (a thin phase spreads over the chip)
+    const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     const int nw = gridDim.x * kWarps;
-    unsigned int target = 0;
+    __shared__ double stage[kWarps * glu::kMaxItemMacs];
+    __shared__ CtaSync cs;
+    double *sg = stage + (threadIdx.x >> 5) * glu::kMaxItemMacs;
+    if (threadIdx.x == 0) {
+        cs.known = 0;
+        cs.polling = 0;
+    }
+    __syncthreads();
     if (P.level_ns && blockIdx.x == 0 && threadIdx.x == 0) P.level_ns[0] = globaltimer();
-    for (int l = 0; l < P.n_levels; ++l) {
-        const int i0 = __ldg(P.level_item_ptr + l), i1 = __ldg(P.level_item_ptr + l + 1);
-        for (int it = i0 + gw; it < i1; it += nw) run_item(P, it, lane);
-        target += gridDim.x;
-        grid_barrier(P.bar, target);
-        if (P.level_ns && blockIdx.x == 0 && threadIdx.x == 0) P.level_ns[l + 1] = globaltimer();
+    int cur = -1, coarse = 0, nq = 0;
+    unsigned ran = 0;
+    __shared__ WarpQ wqs[kWarps];
+    WarpQ *wq = wqs + (threadIdx.x >> 5);
+    int4 a = make_int4(0, 0, 0, 0), b = a, c = a;
+    if (gw < P.n_items) {
+        const int4 *ip = reinterpret_cast<const int4 *>(P.items + gw);
+        a = ldp(ip); b = ldp(ip + 1); c = ldp(ip + 2);
     }
-    for (int j = gw; j < P.n; j += nw) divide_column(P, j, lane);
-}
-
-// ---------------------------------------------------------------------------
-// scatter map: for every MAC, the offset of its target row inside the item's
-// destination segment, found once by binary search over the segment's rows.
-// ---------------------------------------------------------------------------
-__global__ void build_map_kernel(const Item *items, i64 n_items, const Chunk *chunks,
-                                 const i32 *row_idx, uint16_t *map, int *bad) {
-    const int lane = threadIdx.x & 31;
-    const i64 w = (i64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const i64 nwarp = (i64)gridDim.x * (blockDim.x >> 5);
-    for (i64 it = w; it < n_items; it += nwarp) {
-        const Item I = items[it];
-        if (I.kind != glu::kPush) continue;
-        const i32 *seg = row_idx + I.base;
-        i64 off = I.map_off;
-        for (int c = I.c0; c < I.c1; ++c) {
-            const Chunk C = chunks[c];
-            const int cnt = C.meta & 0x7fffffff;
-            for (int t = lane; t < cnt; t += 32) {
-                const i32 r = row_idx[C.p0 + t];
-                int lo = 0, hi = I.span;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (seg[mid] < r) lo = mid + 1; else hi = mid;
-                }
-                if (lo >= I.span || seg[lo] != r) atomicExch(bad, 1);
-                map[off + t] = (uint16_t)lo;
-            }
-            off += cnt;
+    for (int it = gw; it < P.n_items; it += nw) {
+        // next item's descriptor in flight while this one runs
+        const int nit = it + nw;
+        int4 na = a, nb = b, nc = make_int4(0, -4, 0, 0);
+        if (nit < P.n_items) {
+            const int4 *ip = reinterpret_cast<const int4 *>(P.items + nit);
+            na = ldp(ip); nb = ldp(ip + 1); nc = ldp(ip + 2);
         }
+        // (nc.y = -4 when there is no next item: a phase end)
+        const int lvl = c.y >> 2;
+        if (lvl != cur) {
+            ran = 0;
+            cur = lvl;
+        }
+        // deep items wait for every earlier phase (coarse), once per phase
+        int wait_l = -1;
+        if ((c.y & 1) && coarse < lvl) {
+            wait_l = lvl - 1;
+            coarse = lvl;
+        }
+        unsigned long long *rec = nullptr;
+        if (P.trace && it >= P.trace_i0 && it < P.trace_i1) {
+            rec = P.trace + 8 * (size_t)(it - P.trace_i0);
+            if (lane == 0) {
+                rec[0] = (unsigned long long)it | ((unsigned long long)lvl << 32);
+                rec[1] = gw;
+                rec[2] = globaltimer();
+            }
+        }
+        const bool ok = (c.y & 1) ? run_deep(P, a, b, c, lane, &cs, wait_l)
+                                  : run_push(P, a, b, c, lane, &cs, sg, rec);
+        if (!ok) return;
+        ++ran;
+        finish_item(P, wq, nq, c.z, (c.y >> 1) & 1, lvl, ran, (nc.y >> 2) != lvl, lane);
+        a = na; b = nb; c = nc;
     }
+    // every phase complete -> pivot check + divide of every column
+    if (P.n_levels > 0 && !wait_phase(P, P.n_levels - 1, lane, &cs)) return;
+    for (int j = gw; j < P.n; j += nw) divide_column(P, j, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -403,10 +680,14 @@ struct glu_handle {
     // pattern
     i32 *col_ptr = nullptr, *row_idx = nullptr, *diag_pos = nullptr, *level_of = nullptr;
     // plan
-    i32 *level_item_ptr = nullptr;
+    i32 *level_need = nullptr;  // per phase: item count
+    i32 *col_total = nullptr;   // per column: items into it
+    unsigned *sync = nullptr;   // done[n_levels*8] | err (+pad) | col_done[n]
+    size_t sync_words = 0;
     Item *items = nullptr;
     Chunk *chunks = nullptr;
-    uint16_t *map = nullptr;
+    uint8_t *map8 = nullptr;
+    uint16_t *tgt16 = nullptr;
     glu::DeepRef *deep = nullptr;
     i64 n_deep = 0;
     // solves
@@ -420,6 +701,9 @@ struct glu_handle {
     unsigned int *bar = nullptr;
     int *ifail = nullptr;
     unsigned long long *level_ns = nullptr;
+    std::vector<i64> level_item_ptr_h;
+    unsigned long long *trace = nullptr;
+    i64 trace_l0 = 0, trace_nl = 0, trace_cap = 0;
     bool time_levels = false;
     bool fail_by_column = false;
     std::vector<double> last_level_ms;
@@ -434,6 +718,20 @@ template <class T>
 i64 track_upload(glu_handle *h, T **dst, const std::vector<T> &src) {
     GLU_CUDA(upload(dst, src));
     h->bytes += (i64)(src.size() * sizeof(T));
+    return GLU_OK;
+}
+
+template <class T>
+i64 upload_raw(glu_handle *h, T **dst, const T *src, i64 count) {
+    *dst = nullptr;
+    if (count <= 0) return GLU_OK;
+    const size_t bytes = (size_t)count * sizeof(T);
+    if (cudaMalloc((void **)dst, bytes) != cudaSuccess) {
+        glu::set_error("cudaMalloc(" + std::to_string(bytes) + " B) for the update plan");
+        return GLU_ECUDA;
+    }
+    GLU_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+    h->bytes += (i64)bytes;
     return GLU_OK;
 }
 
@@ -513,17 +811,24 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     UP(h->row_idx, ri32);
     UP(h->diag_pos, dp32);
     UP(h->level_of, lv32);
-    UP(h->level_item_ptr, to_i32(pv.level_item_ptr, pv.n_levels + 1));
+    {
+        std::vector<i32> need(std::max<i64>(pv.n_levels, 1), 0);
+        for (i64 l = 0; l < pv.n_levels; l++)
+            need[l] = (i32)(pv.level_item_ptr[l + 1] - pv.level_item_ptr[l]);
+        h->level_item_ptr_h.assign(pv.level_item_ptr, pv.level_item_ptr + pv.n_levels + 1);
+        UP(h->level_need, need);
+        h->sync_words = (size_t)std::max<i64>(pv.n_levels, 1) * 8 + kLineWords + (size_t)std::max<i64>(n, 1) * kColRep;
+        UP(h->col_total, std::vector<i32>(pv.col_total, pv.col_total + n));
+        if (cudaMalloc((void **)&h->sync, h->sync_words * sizeof(unsigned)) != cudaSuccess) {
+            glu::set_error("cudaMalloc(sync)");
+            return fail(GLU_ECUDA);
+        }
+    }
     UP(h->items, std::vector<Item>(pv.items, pv.items + pv.n_items));
     UP(h->chunks, std::vector<Chunk>(pv.chunks, pv.chunks + pv.n_chunks));
     UP(h->deep, std::vector<glu::DeepRef>(pv.deep, pv.deep + pv.n_deep));
-    if (h->n_map > 0) {
-        if (cudaMalloc((void **)&h->map, (size_t)h->n_map * sizeof(uint16_t)) != cudaSuccess) {
-            glu::set_error("cudaMalloc(scatter map " + std::to_string(h->n_map * 2) + " B)");
-            return fail(GLU_ECUDA);
-        }
-        h->bytes += h->n_map * 2;
-    }
+    if ((rc = upload_raw(h, &h->map8, pv.map8, pv.n_map)) != GLU_OK) return fail(rc);
+    if ((rc = upload_raw(h, &h->tgt16, pv.tgt16, pv.n_tgt)) != GLU_OK) return fail(rc);
     // solve structures from the CSR view: L rows (cols < i) and U rows (cols > i)
     std::vector<i32> lp(n + 1, 0), lc, ls, up_(n + 1, 0), uc, us;
     for (i64 i = 0; i < n; i++) {
@@ -549,30 +854,16 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     h->grid = std::min(coop_grid((const void *)factor_kernel, h->sm_count),
                        coop_grid((const void *)solve_kernel, h->sm_count));
     if (h->grid <= 0) { glu::set_error("persistent kernel cannot be co-resident"); return fail(GLU_ECUDA); }
-    // build the scatter map on the device
-    if (h->n_map > 0) {
-        int *dbad = h->ifail;
-        if (cudaMemset(dbad, 0, sizeof(int)) != cudaSuccess) { glu::set_error("memset"); return fail(GLU_ECUDA); }
-        build_map_kernel<<<h->sm_count * 8, 256, 0, h->stream>>>(h->items, h->n_items, h->chunks,
-                                                                   h->row_idx, h->map, dbad);
-        int hbad = 0;
-        if (cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
-            cudaStreamSynchronize(h->stream) != cudaSuccess) {
-            glu::set_error(std::string("scatter-map build: ") + cudaGetErrorString(cudaGetLastError()));
-            return fail(GLU_ECUDA);
-        }
-        if (hbad) { glu::set_error("scatter map: target row absent from segment"); return fail(GLU_MISMATCH); }
-    }
     *out = h;
     return GLU_OK;
 }
 
 extern "C" void glu_destroy(glu_handle *h) {
     if (!h) return;
-    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_item_ptr, h->items,
-                    h->chunks, h->map, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
+    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->sync, h->items,
+                    h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->level_ns, h->d_a, h->d_v, h->d_x};
+                    h->bar, h->ifail, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -592,6 +883,20 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             if (h->time_levels && !h->level_ns && h->n_levels > 0)
                 GLU_CUDA(cudaMalloc((void **)&h->level_ns, sizeof(unsigned long long) * (h->n_levels + 1)));
             return GLU_OK;
+        case 3:  // diagnostics: first traced phase
+            h->trace_l0 = std::max<i64>(0, std::min<i64>(value, h->n_levels));
+            return GLU_OK;
+        case 4: {  // diagnostics: number of traced phases (0 = off)
+            h->trace_nl = std::max<i64>(0, std::min<i64>(value, h->n_levels - h->trace_l0));
+            const i64 cnt = h->level_item_ptr_h[h->trace_l0 + h->trace_nl] - h->level_item_ptr_h[h->trace_l0];
+            if (cnt > h->trace_cap) {
+                if (h->trace) cudaFree(h->trace);
+                h->trace = nullptr;
+                GLU_CUDA(cudaMalloc((void **)&h->trace, sizeof(unsigned long long) * 8 * cnt));
+                h->trace_cap = cnt;
+            }
+            return GLU_OK;
+        }
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
             return GLU_OK;
@@ -599,6 +904,14 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             glu::set_error("unknown option");
             return GLU_EINVAL;
     }
+}
+
+extern "C" int64_t glu_trace_read(glu_handle *h, int64_t *out, int64_t max_records) {
+    if (h->trace_nl <= 0 || !h->trace) return 0;
+    const i64 cnt = h->level_item_ptr_h[h->trace_l0 + h->trace_nl] - h->level_item_ptr_h[h->trace_l0];
+    const i64 m = std::min<i64>(cnt, max_records);
+    if (m > 0) GLU_CUDA(cudaMemcpy(out, h->trace, sizeof(unsigned long long) * 8 * m, cudaMemcpyDeviceToHost));
+    return m;
 }
 
 extern "C" int64_t glu_level_times(const glu_handle *h, double *ms, int64_t len) {
@@ -648,24 +961,38 @@ extern "C" int64_t glu_scatter_device(glu_handle *h, const double *a_vals, doubl
 
 static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream_t s) {
     GLU_CUDA(cudaMemsetAsync(h->fail, 0xff, sizeof(unsigned long long), s));
-    GLU_CUDA(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int), s));
+    GLU_CUDA(cudaMemsetAsync(h->sync, 0, h->sync_words * sizeof(unsigned), s));
     FactorParams P;
     P.v = v;
-    P.level_item_ptr = h->level_item_ptr;
     P.items = h->items;
     P.chunks = h->chunks;
-    P.map = h->map;
+    P.map8 = h->map8;
+    P.tgt16 = h->tgt16;
     P.deep = h->deep;
     P.col_ptr = h->col_ptr;
     P.diag_pos = h->diag_pos;
     P.level_of = h->level_of;
+    P.level_need = h->level_need;
     P.n = (i32)h->n;
+    P.n_items = (i32)h->n_items;
     P.n_levels = (i32)h->n_levels;
     P.thresh = thresh;
     P.fail = h->fail;
-    P.bar = h->bar;
+    const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
+    P.done = h->sync;
+    P.col_done = h->sync + nl8 + kLineWords;
+    P.col_total = h->col_total;
+    P.err = (int *)(h->sync + nl8);
     P.level_ns = h->time_levels ? h->level_ns : nullptr;
     P.fail_by_column = h->fail_by_column ? 1 : 0;
+    P.trace = nullptr;
+    P.trace_i0 = P.trace_i1 = 0;
+    if (h->trace_nl > 0 && h->trace) {
+        P.trace = h->trace;
+        P.trace_i0 = (i32)h->level_item_ptr_h[h->trace_l0];
+        P.trace_i1 = (i32)h->level_item_ptr_h[h->trace_l0 + h->trace_nl];
+        GLU_CUDA(cudaMemsetAsync(h->trace, 0, sizeof(unsigned long long) * 8 * (P.trace_i1 - P.trace_i0), s));
+    }
     void *args[] = {&P};
     if (h->time_levels) {
         GLU_CUDA(cudaMemsetAsync(h->level_ns, 0, sizeof(unsigned long long) * (h->n_levels + 1), s));
@@ -677,12 +1004,23 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
 
 static int64_t read_fail(glu_handle *h, cudaStream_t s) {
     unsigned long long key = 0;
+    int err = 0;
+    const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
     GLU_CUDA(cudaMemcpyAsync(&key, h->fail, sizeof(key), cudaMemcpyDeviceToHost, s));
+    GLU_CUDA(cudaMemcpyAsync(&err, h->sync + nl8, sizeof(int),
+                             cudaMemcpyDeviceToHost, s));
     GLU_CUDA(cudaStreamSynchronize(s));
+    if (err) {
+        glu::set_error("factor kernel watchdog: a phase dependency wait exceeded 4 s");
+        return GLU_ECUDA;
+    }
     if (h->time_levels && h->n_levels > 0) {
         std::vector<unsigned long long> ns(h->n_levels + 1);
         GLU_CUDA(cudaMemcpy(ns.data(), h->level_ns, sizeof(unsigned long long) * (h->n_levels + 1),
                             cudaMemcpyDeviceToHost));
+        // phases without items never complete on their own: carry the time forward
+        for (i64 l = 1; l <= h->n_levels; l++)
+            if (ns[l] == 0) ns[l] = ns[l - 1];
         h->last_level_ms.assign(h->n_levels, 0.0);
         for (i64 l = 0; l < h->n_levels; l++) h->last_level_ms[l] = (double)(ns[l + 1] - ns[l]) * 1e-6;
     }

@@ -352,16 +352,18 @@ sort:
 //          rows/columns of power/ground hubs): its ordered contributions are
 //          listed explicitly, the warp forms 32 products at a time and runs
 //          the subtraction chain in registers -- one load and one store of
-//          the target instead of one L2 round trip per MAC.
-//   kPush  a segment of column k (<= T MACs, <= 65535 positions) with its
-//          ordered chunks (contiguous runs of one source's L entries); lanes
-//          take the chunks' entries 32 at a time.  Chunks are grouped into
-//          epochs of pairwise target-disjoint chunks (kEpochBit marks an
-//          epoch start), so the warp only orders stores where two chunks
-//          really touch the same target.
+//          the target instead of one round trip per MAC.
+//   kPush  a set of <= 128 distinct targets of column k (a position range
+//          cut so the item carries <= T MACs in <= 32 chunks), with its
+//          ordered chunks (contiguous runs of one source's L entries).  Per
+//          MAC the plan stores a u8 index into the item's sorted target list
+//          (u16 offsets), so the warp loads every target once into shared
+//          memory, applies the chunks there and writes every target back
+//          once.  Chunks are grouped into epochs of pairwise target-disjoint
+//          chunks (kEpochBit marks an epoch start); only epochs are ordered.
 // One warp owns every MAC of a target in a phase, so ordering needs no
 // atomics.  T adapts to the phase's total MACs (enough items to fill the
-// grid's warps, 32 <= T <= 1024) unless max_item_macs fixes it.
+// grid's warps, 32 <= T <= 128) unless max_item_macs fixes it.
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -374,20 +376,113 @@ struct LocalItem {
     i32 lvl;
     i32 k;
     i32 kind;
-    i64 base;    // kPush: absolute slot of the segment start; kDeep: target slot
-    i32 span;    // positions covered
+    i64 base;    // kPush: slot the target offsets are relative to; kDeep: target slot
     i64 macs;
-    i64 c0, c1;  // kPush: chunk range in the thread-local chunk vector;
-                 // kDeep: range in the thread-local deep vector
+    i64 c0, c1;  // kPush: chunk range (thread-local); kDeep: deep range (thread-local)
+    i64 m0;      // kPush: first map entry (thread-local)
+    i64 t0, t1;  // kPush: target range (thread-local)
 };
 
 struct ThreadOut {
     std::vector<LocalItem> items;
     std::vector<glu::Chunk> chunks;
     std::vector<glu::DeepRef> deep;
+    std::vector<uint8_t> map8;
+    std::vector<uint16_t> tgt16;
     i64 deferred = 0;
     bool mismatch = false;
     i64 mismatch_col = -1;
+};
+
+// Emits the push items of one segment (pieces in MAC order, all targets in
+// column k), bisecting by target position until every item fits
+// (<= T MACs, <= 32 chunks).  A single position that still does not fit
+// becomes a deep item.
+struct PushEmitter {
+    ThreadOut &o;
+    const i64 *row_idx;
+    const std::vector<i32> &posmap;
+    i64 cb;      // column start slot
+    i32 k, lvl;
+    i64 T;
+    std::vector<i32> pos_scratch, stamp;
+
+    i32 pos_of(i32 p) const { return posmap[row_idx[p]]; }
+
+    void emit(std::vector<glu::Chunk> &pieces) {
+        i64 macs = 0;
+        for (auto &c : pieces) macs += c.meta;
+        if (macs == 0) return;
+        if (macs <= T && macs <= glu::kMaxItemMacs && (i64)pieces.size() <= glu::kMaxItemChunks) {
+            make_item(pieces, macs);
+            return;
+        }
+        pos_scratch.clear();
+        for (auto &c : pieces)
+            for (i32 t = 0; t < c.meta; t++) pos_scratch.push_back(pos_of(c.p0 + t));
+        std::sort(pos_scratch.begin(), pos_scratch.end());
+        pos_scratch.erase(std::unique(pos_scratch.begin(), pos_scratch.end()), pos_scratch.end());
+        if (pos_scratch.size() == 1) {  // one target: ordered chain
+            LocalItem it{};
+            it.lvl = lvl; it.k = k; it.kind = glu::kDeep;
+            it.base = cb + pos_scratch[0];
+            it.macs = macs;
+            it.c0 = (i64)o.deep.size();
+            for (auto &c : pieces)
+                for (i32 t = 0; t < c.meta; t++) o.deep.push_back({c.p0 + t, c.d, c.m, 0});
+            it.c1 = (i64)o.deep.size();
+            o.items.push_back(it);
+            return;
+        }
+        const i32 cut = pos_scratch[pos_scratch.size() / 2];
+        std::vector<glu::Chunk> left, right;
+        for (auto &c : pieces) {
+            i32 t = 0;
+            while (t < c.meta && pos_of(c.p0 + t) < cut) t++;
+            if (t > 0) left.push_back({c.m, c.d, c.p0, t});
+            if (t < c.meta) right.push_back({c.m, c.d, c.p0 + t, c.meta - t});
+        }
+        emit(left);
+        emit(right);
+    }
+
+    void make_item(const std::vector<glu::Chunk> &pieces, i64 macs) {
+        pos_scratch.clear();
+        for (auto &c : pieces)
+            for (i32 t = 0; t < c.meta; t++) pos_scratch.push_back(pos_of(c.p0 + t));
+        std::sort(pos_scratch.begin(), pos_scratch.end());
+        pos_scratch.erase(std::unique(pos_scratch.begin(), pos_scratch.end()), pos_scratch.end());
+        const i32 lo = pos_scratch[0];
+        LocalItem it{};
+        it.lvl = lvl; it.k = k; it.kind = glu::kPush;
+        it.base = cb + lo;
+        it.macs = macs;
+        it.t0 = (i64)o.tgt16.size();
+        for (i32 q : pos_scratch) o.tgt16.push_back((uint16_t)(q - lo));
+        it.t1 = (i64)o.tgt16.size();
+        it.m0 = (i64)o.map8.size();
+        it.c0 = (i64)o.chunks.size();
+        stamp.assign(pos_scratch.size(), -1);
+        i32 ep = 0;
+        bool first = true;
+        for (auto c : pieces) {
+            bool clash = false;
+            const size_t mstart = o.map8.size();
+            for (i32 t = 0; t < c.meta; t++) {
+                const i32 u = (i32)(std::lower_bound(pos_scratch.begin(), pos_scratch.end(),
+                                                     pos_of(c.p0 + t)) - pos_scratch.begin());
+                o.map8.push_back((uint8_t)u);
+                clash = clash || stamp[u] == ep;
+            }
+            if (clash) ep++;
+            for (size_t x = mstart; x < o.map8.size(); x++) stamp[o.map8[x]] = ep;
+            if (clash || first) c.meta |= glu::kEpochBit;
+            first = false;
+            o.chunks.push_back(c);
+        }
+        it.c1 = (i64)o.chunks.size();
+        o.items.push_back(it);
+    }
 };
 
 }  // namespace
@@ -398,7 +493,9 @@ struct glu_plan {
     std::vector<glu::Item> items;
     std::vector<glu::Chunk> chunks;
     std::vector<glu::DeepRef> deep;
-    i64 n_map = 0;
+    std::vector<uint8_t> map8;
+    std::vector<uint16_t> tgt16;
+    std::vector<i32> col_total;
     i64 max_item_macs = 0;
     i64 max_chunks = 0;
     i64 deferred = 0;
@@ -407,7 +504,8 @@ struct glu_plan {
 };
 
 static constexpr i64 kMaxSpan = 65535;
-static constexpr i64 kTargetItemsPerPhase = 2 * 148 * 16;  // two items per resident warp
+static constexpr i64 kTargetItemsPerPhase = 148 * 16 / 4;  // a quarter of the resident warps
+static constexpr i64 kMinItemMacs = 32;
 
 extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                                   const int64_t *diag_pos, const int64_t *level_of,
@@ -432,12 +530,17 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
             const i64 j = row_idx[m];
             phase_macs[level_of[j]] += col_ptr[j + 1] - diag_pos[j] - 1;
         }
+    // Item size: every item costs one dependency wait and one round of
+    // loads whatever its size (all of a lane's entries load together), so
+    // items are as large as the warp allows -- except in a phase too small to
+    // give every warp one, where smaller items spread the work.
     std::vector<i64> Tp(n_levels);
     for (i64 l = 0; l < n_levels; l++)
         Tp[l] = max_item_macs > 0
-                    ? max_item_macs
-                    : std::min<i64>(1024, std::max<i64>(32, (phase_macs[l] + kTargetItemsPerPhase - 1) /
-                                                                kTargetItemsPerPhase));
+                    ? std::min<i64>(max_item_macs, glu::kMaxItemMacs)
+                    : std::min<i64>(glu::kMaxItemMacs,
+                                    std::max<i64>(kMinItemMacs, (phase_macs[l] + kTargetItemsPerPhase - 1) /
+                                                                    kTargetItemsPerPhase));
     int nt = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
     nt = (int)std::min<i64>(nt, std::max<i64>(1, n / 64));
     std::vector<ThreadOut> outs(nt);
@@ -450,13 +553,12 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         std::vector<i32> runmax;   // contract A: running max level per position
         std::vector<i64> hist;     // MACs per position in the current phase
         std::vector<i64> deepidx;  // position -> deep item (local index) or -1
-        std::vector<i64> stamp;    // position -> epoch that last touched it
         std::vector<i64> seg_of;   // position -> segment index or -1
         std::vector<RawChunk> raw;
         std::vector<std::vector<glu::Chunk>> seg_chunks;
         std::vector<std::vector<glu::DeepRef>> deep_lists;
         std::vector<i64> deep_pos;
-        i64 epoch_ctr = 0;
+        PushEmitter em{o, row_idx, posmap, 0, 0, 0, 0, {}, {}};
         while (true) {
             i64 k0 = next.fetch_add(block);
             if (k0 >= n) break;
@@ -513,15 +615,18 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                 if ((i64)hist.size() < len) {
                     hist.assign(len, 0);
                     deepidx.assign(len, -1);
-                    stamp.assign(len, -1);
                     seg_of.assign(len, -1);
                 }
+                em.cb = cb;
+                em.k = (i32)k;
                 size_t g0 = 0;
                 while (g0 < raw.size()) {
                     size_t g1 = g0;
                     while (g1 < raw.size() && raw[g1].lvl == raw[g0].lvl) g1++;
                     const i32 lvl = raw[g0].lvl;
                     const i64 T = Tp[lvl];
+                    em.lvl = lvl;
+                    em.T = T;
                     // MAC histogram over destination positions
                     i64 pmin = len, pmax = -1;
                     for (size_t c = g0; c < g1; c++) {
@@ -542,7 +647,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                         }
                     if ((i64)deep_lists.size() < (i64)deep_pos.size()) deep_lists.resize(deep_pos.size());
                     for (size_t x = 0; x < deep_pos.size(); x++) deep_lists[x].clear();
-                    // greedy segmentation of the remaining positions into items
+                    // greedy segmentation of the remaining positions by MACs and span
                     std::vector<i64> cuts;  // segment starts
                     cuts.push_back(pmin);
                     i64 acc = 0;
@@ -589,51 +694,19 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                         }
                     }
                     for (size_t x = 0; x < deep_pos.size(); x++) {
-                        LocalItem it;
+                        LocalItem it{};
                         it.lvl = lvl;
                         it.k = (i32)k;
                         it.kind = glu::kDeep;
                         it.base = cb + deep_pos[x];
-                        it.span = 1;
                         it.macs = (i64)deep_lists[x].size();
                         it.c0 = (i64)o.deep.size();
                         o.deep.insert(o.deep.end(), deep_lists[x].begin(), deep_lists[x].end());
                         it.c1 = (i64)o.deep.size();
                         o.items.push_back(it);
                     }
-                    for (size_t s = 0; s < nseg; s++) {
-                        auto &sc = seg_chunks[s];
-                        if (sc.empty()) continue;
-                        // tighten the segment to the positions actually touched; epochs
-                        i64 lo = cuts[s + 1], hi = cuts[s] - 1, sm = 0;
-                        i64 ep = ++epoch_ctr;
-                        bool first = true;
-                        for (auto &ch : sc) {
-                            lo = std::min<i64>(lo, posmap[row_idx[ch.p0]]);
-                            hi = std::max<i64>(hi, posmap[row_idx[ch.p0 + ch.meta - 1]]);
-                            sm += ch.meta;
-                            bool clash = false;
-                            for (i32 t = 0; t < ch.meta && !clash; t++)
-                                clash = stamp[posmap[row_idx[ch.p0 + t]]] == ep;
-                            if (clash) {
-                                ep = ++epoch_ctr;
-                            }
-                            for (i32 t = 0; t < ch.meta; t++) stamp[posmap[row_idx[ch.p0 + t]]] = ep;
-                            if (clash || first) ch.meta |= glu::kEpochBit;
-                            first = false;
-                        }
-                        LocalItem it;
-                        it.lvl = lvl;
-                        it.k = (i32)k;
-                        it.kind = glu::kPush;
-                        it.base = cb + lo;
-                        it.span = (i32)(hi - lo + 1);
-                        it.macs = sm;
-                        it.c0 = (i64)o.chunks.size();
-                        o.chunks.insert(o.chunks.end(), sc.begin(), sc.end());
-                        it.c1 = (i64)o.chunks.size();
-                        o.items.push_back(it);
-                    }
+                    for (size_t s = 0; s < nseg; s++)
+                        if (!seg_chunks[s].empty()) em.emit(seg_chunks[s]);
                     for (i64 pos = pmin; pos <= pmax; pos++) {
                         hist[pos] = 0;
                         deepidx[pos] = -1;
@@ -663,18 +736,31 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     // descending (the longest items go first in the static warp round-robin;
     // a deep item's serial chain costs ~8x a push item's MAC), then column,
     // then base.
-    struct Ref { i32 lvl; i32 tid; i64 idx; i64 cost; };
+    struct Ref { i32 lvl; i32 crit; i32 tid; i64 idx; i64 cost; };
     std::vector<Ref> refs;
-    size_t total_items = 0;
-    for (auto &o : outs) total_items += o.items.size();
+    size_t total_items = 0, total_map = 0, total_tgt = 0, total_chunks = 0, total_deep = 0;
+    for (auto &o : outs) {
+        total_items += o.items.size();
+        total_map += o.map8.size();
+        total_tgt += o.tgt16.size();
+        total_chunks += o.chunks.size();
+        total_deep += o.deep.size();
+    }
+    if (total_chunks >= (size_t)INT32_MAX) {
+        set_error("plan has >= 2^31 chunks");
+        return GLU_EINVAL;
+    }
     refs.reserve(total_items);
     for (int t = 0; t < nt; t++)
         for (i64 i = 0; i < (i64)outs[t].items.size(); i++) {
             const LocalItem &x = outs[t].items[i];
-            refs.push_back({x.lvl, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs});
+            // critical: the destination is a source column of the next phase
+            const i32 crit = level_of[x.k] == x.lvl + 1 ? 1 : 0;
+            refs.push_back({x.lvl, crit, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs});
         }
     std::sort(refs.begin(), refs.end(), [&](const Ref &a, const Ref &b) {
         if (a.lvl != b.lvl) return a.lvl < b.lvl;
+        if (a.crit != b.crit) return a.crit > b.crit;
         if (a.cost != b.cost) return a.cost > b.cost;
         const LocalItem &x = outs[a.tid].items[a.idx], &y = outs[b.tid].items[b.idx];
         if (x.k != y.k) return x.k < y.k;
@@ -684,44 +770,58 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     plan->n_levels = n_levels;
     plan->level_item_ptr.assign(n_levels + 1, 0);
     plan->items.reserve(refs.size());
-    i64 map_off = 0;
+    plan->chunks.reserve(total_chunks);
+    plan->map8.reserve(total_map);
+    plan->tgt16.reserve(total_tgt);
+    plan->deep.reserve(total_deep);
+    // dataflow dependencies: per item, the items into its column in earlier
+    // phases; per column, the items into it overall
+    std::vector<i32> cnt_k(n, 0), pend_k(n, 0), last_k(n, -1);
     for (auto &r : refs) {
-        const LocalItem &x = outs[r.tid].items[r.idx];
+        const ThreadOut &o = outs[r.tid];
+        const LocalItem &x = o.items[r.idx];
         plan->level_item_ptr[x.lvl + 1]++;
         glu::Item it{};
+        if (last_k[x.k] != x.lvl) {
+            cnt_k[x.k] += pend_k[x.k];
+            pend_k[x.k] = 0;
+            last_k[x.k] = x.lvl;
+        }
+        it.col = x.k;
+        it.need = cnt_k[x.k];
+        pend_k[x.k]++;
         it.base = (i32)x.base;
-        it.span = x.span;
         it.macs = (i32)x.macs;
-        it.kind = x.kind;
+        // phase in the upper bits (dataflow waits); bit 1: critical (signal at once)
+        it.kind = (x.lvl << 2) | (r.crit << 1) | x.kind;
         if (x.kind == glu::kDeep) {
             it.map_off = (i64)plan->deep.size();
-            it.c0 = it.c1 = 0;
-            plan->deep.insert(plan->deep.end(), outs[r.tid].deep.begin() + x.c0,
-                              outs[r.tid].deep.begin() + x.c1);
+            plan->deep.insert(plan->deep.end(), o.deep.begin() + x.c0, o.deep.begin() + x.c1);
             plan->n_deep_items++;
         } else {
-            it.map_off = map_off;
+            it.map_off = (i64)plan->map8.size();
+            plan->map8.insert(plan->map8.end(), o.map8.begin() + x.m0, o.map8.begin() + x.m0 + x.macs);
+            it.tgt_off = (i64)plan->tgt16.size();
+            plan->tgt16.insert(plan->tgt16.end(), o.tgt16.begin() + x.t0, o.tgt16.begin() + x.t1);
+            it.ntgt = (i32)(x.t1 - x.t0);
             it.c0 = (i32)plan->chunks.size();
             for (i64 c = x.c0; c < x.c1; c++) {
-                const glu::Chunk &ch = outs[r.tid].chunks[c];
+                glu::Chunk ch = o.chunks[c];
                 if (ch.meta & glu::kEpochBit) plan->n_epochs++;
+                // pivot slot -> source column (the device waits on it)
+                ch.d = (i32)(std::upper_bound(col_ptr, col_ptr + n + 1, (i64)ch.d) - col_ptr - 1);
                 plan->chunks.push_back(ch);
             }
-            it.c1 = (i32)plan->chunks.size();
-            map_off += x.macs;
+            it.nch = (i32)(x.c1 - x.c0);
             plan->max_chunks = std::max<i64>(plan->max_chunks, x.c1 - x.c0);
         }
         plan->max_item_macs = std::max<i64>(plan->max_item_macs, x.macs);
         plan->items.push_back(it);
     }
     for (i64 l = 0; l < n_levels; l++) plan->level_item_ptr[l + 1] += plan->level_item_ptr[l];
-    plan->n_map = map_off;
+    plan->col_total.resize(n);
+    for (i64 k = 0; k < n; k++) plan->col_total[k] = cnt_k[k] + pend_k[k];
     for (auto &o : outs) plan->deferred += o.deferred;
-    if ((i64)plan->chunks.size() >= (i64)INT32_MAX) {
-        delete plan;
-        set_error("plan has >= 2^31 chunks");
-        return GLU_EINVAL;
-    }
     *out = plan;
     return GLU_OK;
 }
@@ -730,29 +830,31 @@ extern "C" void glu_plan_info(const glu_plan *p, int64_t *info) {
     info[0] = p->n_levels;
     info[1] = (i64)p->items.size();
     info[2] = (i64)p->chunks.size();
-    info[3] = p->n_map + (i64)p->deep.size();
+    info[3] = (i64)p->map8.size() + (i64)p->deep.size();
     info[4] = p->max_item_macs;
     info[5] = p->max_chunks;
     info[6] = p->deferred;
     info[7] = (i64)(p->items.size() * sizeof(glu::Item) + p->chunks.size() * sizeof(glu::Chunk) +
-                    p->level_item_ptr.size() * sizeof(i64) + p->n_map * sizeof(uint16_t) +
-                    p->deep.size() * sizeof(glu::DeepRef));
+                    p->level_item_ptr.size() * sizeof(i64) + p->map8.size() +
+                    p->tgt16.size() * sizeof(uint16_t) + p->deep.size() * sizeof(glu::DeepRef));
     info[8] = p->n_deep_items;
     info[9] = (i64)p->deep.size();
     info[10] = p->n_epochs;
-    info[11] = p->n_map;
+    info[11] = (i64)p->map8.size();
+    info[12] = (i64)p->tgt16.size();
+    info[13] = info[14] = info[15] = 0;
 }
 
 extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
-                                int64_t *chunks, int64_t *deep) {
+                                int64_t *chunks, int64_t *deep, uint8_t *map8, int64_t *tgt) {
     if (level_item_ptr)
         std::memcpy(level_item_ptr, p->level_item_ptr.data(), p->level_item_ptr.size() * sizeof(i64));
     if (items)
         for (size_t i = 0; i < p->items.size(); i++) {
             const glu::Item &it = p->items[i];
-            i64 *o = items + 7 * i;
-            o[0] = it.map_off; o[1] = it.base; o[2] = it.span; o[3] = it.c0; o[4] = it.c1;
-            o[5] = it.macs; o[6] = it.kind;
+            i64 *o = items + 8 * i;
+            o[0] = it.map_off; o[1] = it.tgt_off; o[2] = it.base; o[3] = it.c0; o[4] = it.nch;
+            o[5] = it.ntgt; o[6] = it.macs; o[7] = it.kind & 1;
         }
     if (chunks)
         for (size_t i = 0; i < p->chunks.size(); i++) {
@@ -767,6 +869,9 @@ extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int6
             i64 *o = deep + 3 * i;
             o[0] = r.l; o[1] = r.d; o[2] = r.m;
         }
+    if (map8 && !p->map8.empty()) std::memcpy(map8, p->map8.data(), p->map8.size());
+    if (tgt)
+        for (size_t i = 0; i < p->tgt16.size(); i++) tgt[i] = p->tgt16[i];
 }
 
 extern "C" void glu_plan_free(glu_plan *p) { delete p; }
@@ -780,9 +885,13 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.n_items = (i64)p->items.size();
     v.chunks = p->chunks.data();
     v.n_chunks = (i64)p->chunks.size();
-    v.n_map = p->n_map;
+    v.n_map = (i64)p->map8.size();
     v.deep = p->deep.data();
     v.n_deep = (i64)p->deep.size();
+    v.map8 = p->map8.data();
+    v.tgt16 = p->tgt16.data();
+    v.n_tgt = (i64)p->tgt16.size();
+    v.col_total = p->col_total.data();
     return v;
 }
 }  // namespace glu

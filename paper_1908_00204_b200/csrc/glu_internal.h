@@ -13,17 +13,29 @@ enum ItemKind : int32_t {
     kDeep = 1,  // one target slot with many ordered contributions (hub rows)
 };
 
-// One warp task in one phase.  32 bytes so a warp fetches it with two
-// 16-byte loads.
+constexpr int kMaxItemMacs = 128;   // push item: at most 4 entries per lane
+constexpr int kMaxItemChunks = 32;  // push item: one chunk descriptor per lane
+
+// One warp task in one phase.  48 bytes = three 16-byte loads.
+//   kPush: the MACs of one phase into a set of <= 256 distinct targets of one
+//          destination column k, given as ordered chunks; per MAC a u8 index
+//          into the item's sorted target list (u16 offsets from `base`).
+//          The warp stages the targets in shared memory, applies the chunks
+//          in order and writes each target back once.
+//   kDeep: one target with many ordered contributions (power/ground rows).
 struct alignas(16) Item {
-    int64_t map_off;  // kPush: first uint16 map entry; kDeep: first DeepRef
-    int32_t base;     // kPush: absolute slot of the segment start; kDeep: target slot
-    int32_t span;     // kPush: positions covered by the segment (<= 65535); kDeep: 1
-    int32_t c0, c1;   // kPush: chunk range
+    int64_t map_off;  // kPush: first u8 map entry; kDeep: first DeepRef
+    int64_t tgt_off;  // kPush: first u16 target offset
+    int32_t base;     // kPush: slot the target offsets are relative to; kDeep: target slot
+    int32_t c0;       // kPush: first chunk
+    int32_t nch;      // kPush: chunks (<= kMaxItemChunks)
+    int32_t ntgt;     // kPush: distinct targets (<= kMaxItemMacs)
     int32_t macs;     // MACs carried
-    int32_t kind;     // ItemKind
+    int32_t kind;     // ItemKind | critical << 1 | phase << 2
+    int32_t col;      // destination column k
+    int32_t need;     // items into column k in earlier phases (dataflow dependency)
 };
-static_assert(sizeof(Item) == 32, "Item layout");
+static_assert(sizeof(Item) == 48, "Item layout");
 
 // A contiguous run of one source column's L entries, applied with one
 // multiplier.  16 bytes: one vector load.  meta = cnt | kEpochBit when the
@@ -32,7 +44,7 @@ static_assert(sizeof(Item) == 32, "Item layout");
 constexpr int32_t kEpochBit = int32_t(0x80000000u);
 struct alignas(16) Chunk {
     int32_t m;     // slot of U(j,k): the multiplier
-    int32_t d;     // slot of A_s(j,j): the pivot
+    int32_t d;     // while building: slot of A_s(j,j) (the pivot); in the plan: source column j
     int32_t p0;    // first L slot of the run
     int32_t meta;  // entries in the run | kEpochBit
 };
@@ -54,6 +66,10 @@ struct glu_plan_view {
     int64_t n_map;
     const DeepRef *deep;
     int64_t n_deep;
+    const uint8_t *map8;
+    const uint16_t *tgt16;
+    int64_t n_tgt;
+    const int32_t *col_total;  // per column: items into it (all phases)
 };
 
 const glu_plan_view plan_view(const glu_plan *p);

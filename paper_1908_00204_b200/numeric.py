@@ -142,11 +142,11 @@ class Factorizer:
         if rc == _lib.GLU_MISMATCH:
             raise PatternMismatchError("update targeted a structurally absent slot")
         try:
-            info = np.zeros(12, dtype=np.int64)
+            info = np.zeros(16, dtype=np.int64)
             _lib.lib.glu_plan_info(plan, _lib.ptr(info))
             self.plan_info = dict(zip(("levels", "items", "chunks", "macs", "max_item_macs",
                                        "max_chunks", "deferred_macs", "plan_bytes", "deep_items",
-                                       "deep_macs", "epochs", "push_macs"),
+                                       "deep_macs", "epochs", "push_macs", "targets"),
                                       info.tolist()))
             h = ctypes.c_void_p()
             rc = _lib.check(_lib.lib.glu_create(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),

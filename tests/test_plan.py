@@ -26,45 +26,59 @@ def export_plan(fp, level_of, contract, max_item_macs=0, deep_min=0):
     rc = _lib.lib.glu_plan_build(fp.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp), _lib.ptr(lv),
                                  contract, max_item_macs, deep_min, 2, ctypes.byref(h))
     assert rc == _lib.GLU_OK, _lib.last_error()
-    info = np.zeros(12, dtype=np.int64)
+    info = np.zeros(16, dtype=np.int64)
     _lib.lib.glu_plan_info(h, _lib.ptr(info))
     nl, ni, nc, nd = int(info[0]), int(info[1]), int(info[2]), int(info[9])
+    nm, nt = int(info[11]), int(info[12])
     lip = np.zeros(nl + 1, dtype=np.int64)
-    items = np.zeros((max(ni, 1), 7), dtype=np.int64)
+    items = np.zeros((max(ni, 1), 8), dtype=np.int64)
     chunks = np.zeros((max(nc, 1), 5), dtype=np.int64)
     deep = np.zeros((max(nd, 1), 3), dtype=np.int64)
-    _lib.lib.glu_plan_export(h, _lib.ptr(lip), _lib.ptr(items), _lib.ptr(chunks), _lib.ptr(deep))
+    map8 = np.zeros(max(nm, 1), dtype=np.uint8)
+    tgt = np.zeros(max(nt, 1), dtype=np.int64)
+    _lib.lib.glu_plan_export(h, _lib.ptr(lip), _lib.ptr(items), _lib.ptr(chunks), _lib.ptr(deep),
+                             _lib.ptr(map8), _lib.ptr(tgt))
     _lib.lib.glu_plan_free(h)
-    return dict(info=info, lip=lip, items=items[:ni], chunks=chunks[:nc], deep=deep[:nd])
+    return dict(info=info, lip=lip, items=items[:ni], chunks=chunks[:nc], deep=deep[:nd],
+                map8=map8[:nm], tgt=tgt[:nt])
 
 
 def emulate(fp, level_of, plan, v, thresh, rng=None):
+    """What factor_kernel does with the plan: items of a phase in any order;
+    a push item stages its targets, applies its chunks in order (entries of
+    one epoch must hit distinct targets) and writes every target back once."""
     ri = fp.full.row_idx
-    lip, items, chunks = plan["lip"], plan["items"], plan["chunks"]
-    map_next = 0
+    lip, items, chunks, map8, tgt = plan["lip"], plan["items"], plan["chunks"], plan["map8"], plan["tgt"]
     for l in range(len(lip) - 1):
         order = np.arange(lip[l], lip[l + 1])
         if rng is not None:
             rng.shuffle(order)  # items of a phase are independent
         for it in order:
-            moff, base, span, c0, c1, macs, kind = items[it]
+            moff, toff, base, c0, nch, ntgt, macs, kind = items[it]
             if kind == 1:  # deep: one target, ordered contributions
                 for l_, d, m in plan["deep"][moff:moff + macs]:
                     v[base] = v[base] - (v[l_] / v[d]) * v[m]
                 continue
-            seg = ri[base:base + span]
+            assert nch <= 32 and macs <= 128 and ntgt <= macs
+            slots = base + tgt[toff:toff + ntgt]
+            assert np.all(np.diff(slots) > 0)
+            stage = v[slots].copy()
+            e = moff
             touched = set()
-            for m, d, p0, cnt, ep in chunks[c0:c1]:
+            for m, j, p0, cnt, ep in chunks[c0:c0 + nch]:
+                d = fp.diag_pos[j]
                 p = np.arange(p0, p0 + cnt)
-                off = np.searchsorted(seg, ri[p])
-                assert np.array_equal(seg[off], ri[p])
-                q = base + off
-                # a chunk that re-touches a target of its epoch must open a new one
+                u = map8[e:e + cnt].astype(np.int64)
+                e += cnt
+                # the staged slot is the row the MAC targets
+                assert np.array_equal(ri[slots[u]], ri[p])
                 if ep:
                     touched = set()
-                assert touched.isdisjoint(q.tolist())
-                touched.update(q.tolist())
-                v[q] = v[q] - (v[p] / v[d]) * v[m]
+                assert touched.isdisjoint(u.tolist())
+                touched.update(u.tolist())
+                stage[u] = stage[u] - (v[p] / v[d]) * v[m]
+            assert e == moff + macs
+            v[slots] = stage
     fail = None
     cp, dp = fp.full.col_ptr, fp.diag_pos
     for j in range(fp.n):
@@ -98,13 +112,11 @@ def test_plan_emulation_bitwise(case, contract, max_item_macs, deep_min):
     plan = export_plan(fp, level_of, contract, max_item_macs, deep_min)
     assert int(plan["info"][3]) == glu.pattern_flops(fp)[0]  # every MAC planned once
     assert int(plan["info"][11]) + int(plan["info"][9]) == int(plan["info"][3])
-    push = plan["items"][plan["items"][:, 6] == 0]
-    assert int(push[:, 5].sum()) == int(plan["info"][11])
+    push = plan["items"][plan["items"][:, 7] == 0]
+    assert int(push[:, 6].sum()) == int(plan["info"][11])
+    assert int(push[:, 5].sum()) == int(plan["info"][12])
     if max_item_macs:
-        one_pos = push[:, 5] > max_item_macs
-        # only items whose MACs all hit one position may exceed the bound
-        for it in push[one_pos]:
-            assert it[2] == 1
+        assert np.all(push[:, 6] <= max_item_macs)
     v = np.zeros(fp.nnz)
     from oracle import oracle as orc
     v, bad = orc.scatter(orc.Pattern.from_fp(fp), a.col_ptr, a.row_idx, a.values)

@@ -19,27 +19,26 @@ rc = _lib.lib.glu_plan_build(a.n, _lib.ptr(fp.full.col_ptr), _lib.ptr(fp.full.ro
                              _lib.ptr(fp.diag_pos), _lib.ptr(_lib.i64(s.level_of)), contract, T, D, 0,
                              ctypes.byref(pp))
 print("plan build s", round(time.time() - t, 2), rc)
-info = np.zeros(12, np.int64)
+info = np.zeros(16, np.int64)
 _lib.lib.glu_plan_info(pp, _lib.ptr(info))
 names = ("levels", "items", "chunks", "macs", "max_item_macs", "max_chunks", "deferred", "bytes",
-         "deep_items", "deep_macs", "epochs", "push_macs")
+         "deep_items", "deep_macs", "epochs", "push_macs", "targets")
 print(dict(zip(names, info.tolist())))
 nl, ni, nc, nd = info[0], info[1], info[2], info[9]
-lip = np.zeros(nl + 1, np.int64); items = np.zeros(ni * 7, np.int64); ch = np.zeros(nc * 5, np.int64)
+lip = np.zeros(nl + 1, np.int64); items = np.zeros(ni * 8, np.int64); ch = np.zeros(nc * 5, np.int64)
 dp = np.zeros(max(nd, 1) * 3, np.int64)
-_lib.lib.glu_plan_export(pp, _lib.ptr(lip), _lib.ptr(items), _lib.ptr(ch), _lib.ptr(dp))
-items = items.reshape(-1, 7); ch = ch.reshape(-1, 5)
+_lib.lib.glu_plan_export(pp, _lib.ptr(lip), _lib.ptr(items), _lib.ptr(ch), _lib.ptr(dp), None, None)
+items = items.reshape(-1, 8); ch = ch.reshape(-1, 5)
 ipl = np.diff(lip)
-cs = np.concatenate([[0], np.cumsum(items[:, 5])]); mpl = cs[lip[1:]] - cs[lip[:-1]]
-push = items[items[:, 6] == 0]; deep = items[items[:, 6] == 1]
+cs = np.concatenate([[0], np.cumsum(items[:, 6])]); mpl = cs[lip[1:]] - cs[lip[:-1]]
+push = items[items[:, 7] == 0]; deep = items[items[:, 7] == 1]
 print("items/level pct", np.percentile(ipl, [0, 10, 50, 90, 100]))
 print("macs/level pct", np.percentile(mpl, [0, 10, 50, 90, 100]))
-print("push item macs pct", np.percentile(push[:, 5], [10, 50, 90, 99, 100]))
-print("push chunks/item pct", np.percentile(push[:, 4] - push[:, 3], [10, 50, 90, 99, 100]))
+print("push item macs pct", np.percentile(push[:, 6], [10, 50, 90, 99, 100]))
+print("push chunks/item pct", np.percentile(push[:, 4], [10, 50, 90, 99, 100]))
+print("push targets/item pct", np.percentile(push[:, 5], [10, 50, 90, 99, 100]))
 if len(deep):
-    print("deep item macs pct", np.percentile(deep[:, 5], [10, 50, 90, 99, 100]))
-# epochs per push item
+    print("deep item macs pct", np.percentile(deep[:, 6], [10, 50, 90, 99, 100]))
 ep = np.concatenate([[0], np.cumsum(ch[:, 4])])
-epi = ep[push[:, 4]] - ep[push[:, 3]]
+epi = ep[push[:, 3] + push[:, 4]] - ep[push[:, 3]]
 print("epochs/push item pct", np.percentile(epi, [10, 50, 90, 99, 100]))
-np.savez(f"/tmp/plan_{cfg}_{contract}.npz", lip=lip, items=items, ch=ch)
