@@ -141,6 +141,8 @@ struct FactorParams {
     unsigned long long *level_ns;  // optional per-phase completion timestamps
     unsigned long long *trace;     // optional per-item timestamps (diagnostics)
     i32 trace_i0, trace_i1;        // traced item range
+    i32 prefetch;                  // L2-prefetch the next item's static plan data
+    i32 poll_ns;                   // sleep between dependency polls
     i32 fail_by_column;            // 1: key = column only (sequential API semantics)
 };
 
@@ -165,9 +167,16 @@ struct FactorParams {
 // earlier items and every item it waits on has a smaller index.  A
 // watchdog turns an endless wait (a bug) into an error instead of a hang.
 // ---------------------------------------------------------------------------
+constexpr int kReq = 4;  // dependency requests per waiting warp (distinct columns)
 struct CtaSync {
     unsigned known;   // phases [0, known) complete
     int polling;      // a warp of this CTA has a poll in flight
+    // per-CTA wait service (see wait_cols)
+    int req_col[kWarps * kReq];
+    unsigned req_need[kWarps * kReq];
+    int pending[kWarps];  // 1: the warp's requests await checking
+    int ready[kWarps];    // 1: all of the warp's requests satisfied
+    int wpoll;            // a warp is running the service round
 };
 
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
@@ -276,16 +285,91 @@ __device__ __forceinline__ void finish_item(const FactorParams &P, WarpQ *q, int
 // Fine-grained wait of a push item in phase lvl: its source columns complete
 // (every item into them counted) and every earlier-phase item into its own
 // column counted.  Skipped when the CTA already knows phases < lvl complete.
-// Relaxed polling: the values are read .cg from L2 after the wait returns,
-// and the producer fenced its stores before counting.  Backs off in
-// proportion to the items still outstanding.
+//
+// A per-CTA wait service keeps the polling off the critical path: a release
+// fence (MEMBAR.GPU) waits behind every memory request the SM has in flight
+// (measured: ~265 cycles on a quiet SM, ~1,500-1,900 with neighbour warps
+// polling), so instead of each waiting warp polling global counters, a
+// warp posts its <= kReq (column, count) requests in shared memory and ONE
+// warp of the CTA at a time checks every posted request in a single round
+// of relaxed loads, flagging the satisfied warps.  Relaxed polling is
+// enough: the values are read .cg from L2 after the wait, and the producer
+// fenced its stores before counting.
 __device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool has_src, int j,
                                           unsigned jneed, int k, unsigned kneed, int lvl,
                                           CtaSync *cs, int rep) {
+    const int w = threadIdx.x >> 5;
+    volatile int *vready = cs->ready;
     volatile unsigned *vk = &cs->known;
+    // distinct requests: the own column (lane 0) and every distinct source column
+    const unsigned same = __match_any_sync(0xffffffffu, has_src ? j : -1 - lane);
+    const bool src_lead = has_src && (__ffs(same) - 1) == lane;
+    const bool post_k = lane == 0;
+    const unsigned pm = __ballot_sync(0xffffffffu, src_lead);
+    const int nsrc = __popc(pm);
     unsigned long long t0 = 0;
+    if (nsrc + 1 <= kReq) {
+        const int slot = src_lead ? 1 + __popc(pm & ((1u << lane) - 1u)) : -1;
+        if (post_k) { cs->req_col[w * kReq] = k; cs->req_need[w * kReq] = kneed; }
+        if (slot > 0) { cs->req_col[w * kReq + slot] = j; cs->req_need[w * kReq + slot] = jneed; }
+        if (lane == 0)
+            for (int x = nsrc + 1; x < kReq; ++x) cs->req_col[w * kReq + x] = -1;
+        if (lane == 0) { cs->ready[w] = 0; __threadfence_block(); cs->pending[w] = 1; }
+        __syncwarp();
+        // only the service round clears a posted request (no other exit), so a
+        // round never sees a half-rewritten request
+        for (int spin = 0;; ++spin) {
+            if (vready[w]) break;
+            int got = 0;
+            if (lane == 0) got = atomicCAS(&cs->wpoll, 0, 1) == 0;
+            got = __shfl_sync(0xffffffffu, got, 0);
+            if (got) {
+                // one service round: lanes over (warp, slot) entries, two per
+                // lane; the group leader's single read of pending[] decides for
+                // all four lanes of a warp's entries (a request posted during
+                // the round is left for the next one)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int e = lane + 32 * h, ww = e / kReq;
+                    int pend = 0;
+                    if ((lane % kReq) == 0) pend = ((volatile int *)cs->pending)[ww];
+                    pend = __shfl_sync(0xffffffffu, pend, lane & ~(kReq - 1));
+                    bool ok = true;
+                    if (pend) {
+                        const int cc = ((volatile int *)cs->req_col)[e];
+                        if (cc >= 0)
+                            ok = ld_relaxed(P.col_done + (size_t)cc * kColRep + rep) >=
+                                 ((volatile unsigned *)cs->req_need)[e];
+                    }
+                    const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+                    if ((lane % kReq) == 0 && pend && ((bad >> lane) & ((1u << kReq) - 1u)) == 0) {
+                        cs->pending[ww] = 0;
+                        __threadfence_block();
+                        cs->ready[ww] = 1;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) atomicExch(&cs->wpoll, 0);
+            } else {
+                __nanosleep(P.poll_ns);
+            }
+            if ((spin & 255) == 255) {
+                int bad = 0;
+                if (lane == 0) {
+                    const unsigned long long t = globaltimer();
+                    if (t0 == 0) t0 = t;
+                    bad = (t - t0 > kWatchdogNs) || *(volatile int *)P.err;
+                    if (bad) atomicExch(P.err, 1);
+                }
+                if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+            }
+        }
+        __syncwarp();
+        return true;
+    }
+    // many distinct sources (wide phases): poll directly
     for (int spin = 0;; ++spin) {
-        __nanosleep(32);
+        __nanosleep(P.poll_ns);
         if (*vk >= (unsigned)lvl) break;
         unsigned rem = 0;
         if (has_src) {
@@ -324,6 +408,28 @@ __device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool 
 // targets; only epochs are ordered), and every target written back once.
 constexpr int kR = glu::kMaxItemMacs / 32;  // entries per lane
 
+// L2 prefetch of an item's static plan data (descriptor already loaded):
+// its chunk descriptors, u8 map and target list, or the first deep refs.
+__device__ __forceinline__ void prefetch_item(const FactorParams &P, int4 a, int4 b, int4 c, int lane) {
+    if (c.y < 0 || !P.prefetch) return;
+    const char *p = nullptr;
+    if (c.y & 1) {
+        const i64 off = (i64)(unsigned)a.x | ((i64)a.y << 32);
+        if (lane < 8 && lane * 8 < c.x) p = reinterpret_cast<const char *>(P.deep + off) + lane * 128;
+    } else {
+        const i64 moff = (i64)(unsigned)a.x | ((i64)a.y << 32);
+        const i64 toff = (i64)(unsigned)a.z | ((i64)a.w << 32);
+        if (lane < 5) {
+            if (lane * 128 < b.z * 16) p = reinterpret_cast<const char *>(P.chunks + b.y) + lane * 128;
+        } else if (lane < 7) {
+            if ((lane - 5) * 128 < c.x) p = reinterpret_cast<const char *>(P.map8 + moff) + (lane - 5) * 128;
+        } else if (lane < 10) {
+            if ((lane - 7) * 128 < 2 * b.w) p = reinterpret_cast<const char *>(P.tgt16 + toff) + (lane - 7) * 128;
+        }
+    }
+    if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ int round_chunk(int rbase, int lane, int nch, int est) {
     const unsigned start_bits = __reduce_or_sync(
         0xffffffffu, (lane < nch && est > rbase && est < rbase + 32) ? (1u << (est - rbase)) : 0u);
@@ -336,7 +442,8 @@ __device__ __forceinline__ void stamp(unsigned long long *rec, int k, int lane) 
 }
 
 __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, int4 c, int lane,
-                                         CtaSync *cs, double *sg, unsigned long long *rec) {
+                                         CtaSync *cs, double *sg, unsigned long long *rec, int4 na,
+                                         int4 nb, int4 nc) {
     const i64 moff = (i64)(unsigned)a.x | ((i64)a.y << 32);
     const i64 toff = (i64)(unsigned)a.z | ((i64)a.w << 32);
     const int base = b.x, c0 = b.y, nch = b.z, ntgt = b.w, macs = c.x;
@@ -388,6 +495,7 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
         !wait_cols(P, lane, lane < nch, ch.y, jneed, c.z, (unsigned)c.w, lvl, cs, rep))
         return false;
     stamp(rec, 4, lane);
+    prefetch_item(P, na, nb, nc, lane);
     // one round of independent loads
     double piv = 1.0, mult = 0.0;
     if (lane < nch) {
@@ -446,44 +554,103 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
 // subtraction chain in order from shuffles, so the target sees exactly the
 // reference's sequence of roundings with one load and one store.  The next
 // group's operands are loaded before the current group's chain.
+constexpr int kDeepRing = 8;  // deep-ref groups of 32 in flight (cp.async into shared memory)
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = pred ? 16 : 0;  // src-size 0: zero-fill, no global read
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// kDeep item: one target, many ordered contributions.  Lanes form 32
+// products at a time (independent roundings); every lane then replays the
+// subtraction chain in order from shuffles, so the target sees exactly the
+// reference's sequence of roundings with one load and one store.  Two-stage
+// pipeline so the serial chain never waits on memory: the {l, d, m} refs
+// stream into a shared-memory ring kDeepRing groups ahead (cp.async), the
+// three operands of a group are loaded two groups ahead.
 __device__ __forceinline__ bool run_deep(const FactorParams &P, int4 a, int4 b, int4 c_, int lane,
-                                         CtaSync *cs, int wait_l) {
+                                         CtaSync *cs, int wait_l, int4 *ring, double *sg, int4 na,
+                                         int4 nb, int4 nc, unsigned long long *rec) {
     const i64 off = (i64)(unsigned)a.x | ((i64)a.y << 32);
     const int macs = c_.x;
+    const int ng = (macs + 31) >> 5;
     const int4 *dr = reinterpret_cast<const int4 *>(P.deep) + off;
     double *tp = P.v + b.x;
-    // operands of groups g .. g+3 in flight (q0 = current group)
-    int4 r0 = make_int4(0, 0, 0, 0), r1 = r0, r2 = r0, r3 = r0;
-    if (lane < macs) r0 = ldp(dr + lane);
-    if (32 + lane < macs) r1 = ldp(dr + 32 + lane);
-    if (64 + lane < macs) r2 = ldp(dr + 64 + lane);
-    if (96 + lane < macs) r3 = ldp(dr + 96 + lane);
-    if (wait_l >= 0 && !wait_phase(P, wait_l, lane, cs)) return false;
-    double acc = ldv(tp);
-    double l0 = 0.0, d0 = 1.0, m0 = 0.0, l1 = 0.0, d1 = 1.0, m1 = 0.0;
-    double l2 = 0.0, d2 = 1.0, m2 = 0.0, l3 = 0.0, d3 = 1.0, m3 = 0.0;
-    if (lane < macs) { l0 = ldv(P.v + r0.x); d0 = ldv(P.v + r0.y); m0 = ldv(P.v + r0.z); }
-    if (32 + lane < macs) { l1 = ldv(P.v + r1.x); d1 = ldv(P.v + r1.y); m1 = ldv(P.v + r1.z); }
-    if (64 + lane < macs) { l2 = ldv(P.v + r2.x); d2 = ldv(P.v + r2.y); m2 = ldv(P.v + r2.z); }
-    if (96 + lane < macs) { l3 = ldv(P.v + r3.x); d3 = ldv(P.v + r3.y); m3 = ldv(P.v + r3.z); }
-    for (int r = 0; r < macs; r += 32) {
-        const double prod = __dmul_rn(__ddiv_rn(l0, d0), m0);
-        l0 = l1; d0 = d1; m0 = m1;
-        l1 = l2; d1 = d2; m1 = m2;
-        l2 = l3; d2 = d3; m2 = m3;
-        if (r + 128 + lane < macs) {
-            const int4 rn = ldp(dr + r + 128 + lane);
-            l3 = ldv(P.v + rn.x); d3 = ldv(P.v + rn.y); m3 = ldv(P.v + rn.z);
-        }
-        const int cnt = min(32, macs - r);
-        if (cnt == 32) {
 #pragma unroll
-            for (int s = 0; s < 32; ++s) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, prod, s));
-        } else {
-            for (int s = 0; s < cnt; ++s) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, prod, s));
-        }
+    for (int g = 0; g < kDeepRing; ++g) {
+        cp_async16(ring + g * 32 + lane, dr + min(32 * g + lane, macs - 1), 32 * g + lane < macs);
+        cp_async_commit();
     }
+    if (wait_l >= 0 && !wait_phase(P, wait_l, lane, cs)) {
+        cp_async_wait<0>();
+        return false;
+    }
+    stamp(rec, 3, lane);
+    prefetch_item(P, na, nb, nc, lane);
+    double acc = ldv(tp);
+    // operand sets for groups g % 3 (values loaded three groups ahead)
+    double l0 = 0.0, d0 = 1.0, m0 = 0.0, l1 = 0.0, d1 = 1.0, m1 = 0.0, l2 = 0.0, d2 = 1.0, m2 = 0.0;
+    auto load_group = [&](int grp, double &l, double &d, double &m) {
+        if (32 * grp + lane < macs) {
+            const int4 r = ring[(grp % kDeepRing) * 32 + lane];
+            l = ldv(P.v + r.x); d = ldv(P.v + r.y); m = ldv(P.v + r.z);
+        }
+    };
+    auto refill = [&](int grp) {  // slot of group grp was just consumed: fetch group grp + kDeepRing
+        const int gn = grp + kDeepRing;
+        cp_async16(ring + (grp % kDeepRing) * 32 + lane, dr + min(32 * gn + lane, macs - 1),
+                   32 * gn + lane < macs);
+        cp_async_commit();
+    };
+    cp_async_wait<kDeepRing - 4>();  // groups 0..3 landed
+    __syncwarp();
+    load_group(0, l0, d0, m0);
+    load_group(1, l1, d1, m1);
+    load_group(2, l2, d2, m2);
+    __syncwarp();
+    refill(0); refill(1); refill(2);
+    sg[lane] = __dmul_rn(__ddiv_rn(l0, d0), m0);  // products of group 0
+    load_group(3, l0, d0, m0);
+    __syncwarp();
+    refill(3);
+    // iteration g: products of group g+1 (set (g+1)%3) -> buffer, reload that
+    // set with group g+4, chain group g on lane 0 from shared memory
+    auto step = [&](int g, double &l, double &d, double &m) {
+        if (g + 1 < ng) sg[((g + 1) & 1) * 32 + lane] = __dmul_rn(__ddiv_rn(l, d), m);
+        cp_async_wait<kDeepRing - 1>();  // group g+4 landed
+        __syncwarp();
+        load_group(g + 4, l, d, m);
+        __syncwarp();
+        refill(g + 4);
+        if (lane == 0) {
+            const double2 *pb = reinterpret_cast<const double2 *>(sg + (g & 1) * 32);
+            const int cnt = min(32, macs - 32 * g);
+            if (cnt == 32) {
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) {
+                    const double2 x = pb[s2];
+                    acc = __dsub_rn(acc, x.x);
+                    acc = __dsub_rn(acc, x.y);
+                }
+            } else {
+                for (int s1 = 0; s1 < cnt; ++s1) acc = __dsub_rn(acc, sg[(g & 1) * 32 + s1]);
+            }
+        }
+        __syncwarp();
+    };
+    for (int g = 0; g < ng; g += 3) {
+        step(g, l1, d1, m1);
+        if (g + 1 < ng) step(g + 1, l2, d2, m2);
+        if (g + 2 < ng) step(g + 2, l0, d0, m0);
+    }
+    cp_async_wait<0>();
     if (lane == 0) stv(tp, acc);
+    stamp(rec, 6, lane);
+    if (rec && lane == 0) rec[7] = ng;
     return true;
 }
 
@@ -521,19 +688,26 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     // consecutive items go to consecutive SMs (a thin phase spreads over the chip)
     const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     const int nw = gridDim.x * kWarps;
-    __shared__ double stage[kWarps * glu::kMaxItemMacs];
+    __shared__ __align__(16) double stage[kWarps * glu::kMaxItemMacs];
     __shared__ CtaSync cs;
     double *sg = stage + (threadIdx.x >> 5) * glu::kMaxItemMacs;
     if (threadIdx.x == 0) {
         cs.known = 0;
         cs.polling = 0;
+        cs.wpoll = 0;
+    }
+    if (threadIdx.x < kWarps) {
+        cs.pending[threadIdx.x] = 0;
+        cs.ready[threadIdx.x] = 0;
     }
     __syncthreads();
     if (P.level_ns && blockIdx.x == 0 && threadIdx.x == 0) P.level_ns[0] = globaltimer();
     int cur = -1, coarse = 0, nq = 0;
     unsigned ran = 0;
     __shared__ WarpQ wqs[kWarps];
+    extern __shared__ int4 rings[];  // kWarps * kDeepRing * 32 (dynamic: > 48 KB static limit)
     WarpQ *wq = wqs + (threadIdx.x >> 5);
+    int4 *ring = rings + (threadIdx.x >> 5) * kDeepRing * 32;
     int4 a = make_int4(0, 0, 0, 0), b = a, c = a;
     if (gw < P.n_items) {
         const int4 *ip = reinterpret_cast<const int4 *>(P.items + gw);
@@ -568,11 +742,12 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
                 rec[2] = globaltimer();
             }
         }
-        const bool ok = (c.y & 1) ? run_deep(P, a, b, c, lane, &cs, wait_l)
-                                  : run_push(P, a, b, c, lane, &cs, sg, rec);
+        const bool ok = (c.y & 1) ? run_deep(P, a, b, c, lane, &cs, wait_l, ring, sg, na, nb, nc, rec)
+                                  : run_push(P, a, b, c, lane, &cs, sg, rec, na, nb, nc);
         if (!ok) return;
         ++ran;
         finish_item(P, wq, nq, c.z, (c.y >> 1) & 1, lvl, ran, (nc.y >> 2) != lvl, lane);
+        if (rec && lane == 0 && !(c.y & 1)) rec[7] = globaltimer() | (1ull << 63);
         a = na; b = nb; c = nc;
     }
     // every phase complete -> pivot check + divide of every column
@@ -706,6 +881,8 @@ struct glu_handle {
     i64 trace_l0 = 0, trace_nl = 0, trace_cap = 0;
     bool time_levels = false;
     bool fail_by_column = false;
+    bool prefetch = false;
+    int poll_ns = 32;
     std::vector<double> last_level_ms;
     // host-API staging
     double *d_a = nullptr, *d_v = nullptr, *d_x = nullptr;
@@ -763,9 +940,14 @@ void solve_levels(i64 n, const std::vector<i32> &ptr, const std::vector<i32> &co
     n_levels = nl;
 }
 
-int coop_grid(const void *kernel, int sm_count) {
+constexpr size_t kFactorDynSmem = sizeof(int4) * kWarps * kDeepRing * 32;
+
+int coop_grid(const void *kernel, int sm_count, size_t dyn_smem = 0) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0) != cudaSuccess)
+    if (dyn_smem > 0 &&
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem) != cudaSuccess)
+        return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, dyn_smem) != cudaSuccess)
         return 0;
     per_sm = std::min(per_sm, 1);
     return per_sm * sm_count;
@@ -851,7 +1033,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         cudaMalloc((void **)&h->ifail, sizeof(int)) != cudaSuccess) {
         glu::set_error("cudaMalloc(scratch)"); return fail(GLU_ECUDA);
     }
-    h->grid = std::min(coop_grid((const void *)factor_kernel, h->sm_count),
+    h->grid = std::min(coop_grid((const void *)factor_kernel, h->sm_count, kFactorDynSmem),
                        coop_grid((const void *)solve_kernel, h->sm_count));
     if (h->grid <= 0) { glu::set_error("persistent kernel cannot be co-resident"); return fail(GLU_ECUDA); }
     *out = h;
@@ -897,6 +1079,12 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             }
             return GLU_OK;
         }
+        case 5:  // tuning: L2 prefetch of the next item's plan data (default on)
+            h->prefetch = value != 0;
+            return GLU_OK;
+        case 6:  // tuning: nanoseconds between dependency polls
+            h->poll_ns = (int)std::max<int64_t>(0, std::min<int64_t>(value, 100000));
+            return GLU_OK;
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
             return GLU_OK;
@@ -987,6 +1175,8 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.fail_by_column = h->fail_by_column ? 1 : 0;
     P.trace = nullptr;
     P.trace_i0 = P.trace_i1 = 0;
+    P.prefetch = h->prefetch ? 1 : 0;
+    P.poll_ns = h->poll_ns;
     if (h->trace_nl > 0 && h->trace) {
         P.trace = h->trace;
         P.trace_i0 = (i32)h->level_item_ptr_h[h->trace_l0];
@@ -998,7 +1188,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         GLU_CUDA(cudaMemsetAsync(h->level_ns, 0, sizeof(unsigned long long) * (h->n_levels + 1), s));
     }
     GLU_CUDA(cudaLaunchCooperativeKernel((const void *)factor_kernel, dim3(h->grid), dim3(kThreads),
-                                         args, 0, s));
+                                         args, kFactorDynSmem, s));
     return GLU_OK;
 }
 

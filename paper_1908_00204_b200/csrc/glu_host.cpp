@@ -758,8 +758,13 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
             const i32 crit = level_of[x.k] == x.lvl + 1 ? 1 : 0;
             refs.push_back({x.lvl, crit, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs});
         }
+    // inside a phase: deep chains first (the longest serial work), then the
+    // items the next phase waits for, then by cost
     std::sort(refs.begin(), refs.end(), [&](const Ref &a, const Ref &b) {
         if (a.lvl != b.lvl) return a.lvl < b.lvl;
+        const bool da = outs[a.tid].items[a.idx].kind == glu::kDeep;
+        const bool db = outs[b.tid].items[b.idx].kind == glu::kDeep;
+        if (da != db) return da;
         if (a.crit != b.crit) return a.crit > b.crit;
         if (a.cost != b.cost) return a.cost > b.cost;
         const LocalItem &x = outs[a.tid].items[a.idx], &y = outs[b.tid].items[b.idx];

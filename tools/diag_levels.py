@@ -1,6 +1,6 @@
 """Per-level GPU timing of one factorization (globaltimer stamps written by
 the persistent kernel) next to the plan's per-level items / MACs."""
-import sys, time, json, pathlib
+import os, sys, time, json, pathlib
 import numpy as np
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
@@ -20,6 +20,10 @@ ad = torch.from_numpy(a.values).to(dev)
 v = torch.empty(fp.nnz, dtype=torch.float64, device=dev)
 st = torch.cuda.current_stream()
 fz.set_option(1, 0)
+if "GLU_POLL" in os.environ:
+    fz.set_option(6, int(os.environ["GLU_POLL"]))
+if "GLU_PREFETCH" in os.environ:
+    fz.set_option(5, int(os.environ["GLU_PREFETCH"]))
 for _ in range(3):
     fz.scatter_device(ad, v, st); fz.factor_device(v, 1e-14, st)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -29,7 +33,7 @@ tot = e0.elapsed_time(e1)
 fz.set_option(1, 1)
 fz.scatter_device(ad, v, st); rc = fz.factor_device(v, 1e-14, st)
 lt = np.array(fz.level_times_s()) * 1e3
-out = ROOT / "gpurun_out" / f"levels_{cfg}_{contract}.npz"
+out = ROOT / "gpurun_out" / f"levels_{cfg}_{contract}{os.environ.get('TAG', '')}.npz"
 out.parent.mkdir(exist_ok=True)
 np.savez(out, level_ms=lt, total_ms=tot)
 print(json.dumps({"cfg": cfg, "contract": contract, "rc": rc, "total_ms": tot,

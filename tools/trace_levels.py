@@ -16,6 +16,9 @@ fp = glu.symbolic_fillin(a.pattern)
 s = glu.levelize(glu.detect_relaxed(fp))
 fz = glu.Factorizer(fp, s.level_of, contract)
 fz.set_input(a.col_ptr, a.row_idx)
+import os
+if 'GLU_POLL' in os.environ:
+    fz.set_option(6, int(os.environ['GLU_POLL']))
 dev = torch.device("cuda", 0)
 ad = torch.from_numpy(a.values).to(dev)
 v = torch.empty(fp.nnz, dtype=torch.float64, device=dev)
@@ -53,4 +56,17 @@ for l0, nl in ranges:
               "apply_store_us(med/max)": [float(np.median(r[:, 6] - r[:, 5])) / 1e3, float((r[:, 6] - r[:, 5]).max()) / 1e3],
               "last_store_us": round((r[:, 6].max() - t0) / 1e3, 2),
               "phase_len_us": round(lt[l] / 1e3, 2)}))
-np.savez(ROOT / "gpurun_out" / f"trace_{cfg}_{contract}.npz", **out)
+np.savez(ROOT / "gpurun_out" / f"trace_{cfg}_{contract}{os.environ.get('TAG', '')}.npz", **out)
+# deep items of the traced phases
+for key in list(out):
+    if not key.startswith("r"):
+        continue
+    rec = out[key]
+    dp = rec[(rec[:, 7] > 0)]
+    if len(dp):
+        g = dp[:, 7]
+        tot = (dp[:, 6] - dp[:, 4]) / 1e3
+        print(json.dumps({"range": key, "deep_items": int(len(dp)), "groups_max": int(g.max()),
+                          "loop_us_max": float(tot.max()), "us_per_group_med": float(np.median(tot / g)),
+                          "first_group_us_med": float(np.median(dp[:, 5] - dp[:, 4]) / 1e3),
+                          "setup_us_med": float(np.median(dp[:, 4] - dp[:, 3]) / 1e3)}))
