@@ -105,17 +105,24 @@ int64_t glu_find_hazards(int64_t n, const int64_t *col_ptr, const int64_t *row_i
    numeric.py:295-315).  contract: GLU_CONTRACT_A or GLU_CONTRACT_B.
    max_item_macs caps the MACs one push item carries (0 = adaptive per
    phase, 32..128); deep_min is the MAC count from which a target becomes
-   its own register-chained item (0 = default 8).  Returns GLU_OK or
-   GLU_MISMATCH when an update targets a slot absent from the pattern (the
-   condition _kernels.py:113-114 reports at run time). */
+   its own register-chained item (0 = default 8).  tail_max: the trailing
+   columns that are each alone in the last phases (a near-dense separator
+   block) go to the thread-block-cluster tail kernel, up to tail_max of them
+   (0 = no tail; glu_tail_capacity() gives the device's limit).  Returns
+   GLU_OK or GLU_MISMATCH when an update targets a slot absent from the
+   pattern (the condition _kernels.py:113-114 reports at run time). */
 int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                        const int64_t *diag_pos, const int64_t *level_of, int32_t contract,
-                       int64_t max_item_macs, int64_t deep_min, int32_t n_threads,
-                       glu_plan **out);
+                       int64_t max_item_macs, int64_t deep_min, int64_t tail_max,
+                       int32_t n_threads, glu_plan **out);
+/* Largest dense tail (columns) the current device's cluster kernel holds in
+   distributed shared memory; 0 without a CUDA device. */
+int64_t glu_tail_capacity(void);
 /* info[0..15] = n_levels, n_items, n_chunks, MACs, max_item_macs,
    max_chunks_per_item, deferred_macs (contract A), plan bytes, deep items,
    deep MACs, epochs, push MACs (= u8 map entries), target-list entries,
-   0, 0, 0 */
+   tail start column t0 (n: no tail), tail MACs, 0.  MACs (info[3]) counts
+   push + deep + tail MACs. */
 void glu_plan_info(const glu_plan *p, int64_t *info);
 /* level_item_ptr[n_levels+1];
    items[n_items*8]   = {map_off, tgt_off, base, c0, nch, ntgt, macs, kind (0 push, 1 deep)};

@@ -45,7 +45,8 @@ SIGNATURES = {
     "glu_levelize": (_i64, [_i64, _p, _p, _p, _p, _p]),
     "glu_scatter_values": (_i64, [_i64, _p, _p, _p, _p, _p, _p]),
     "glu_find_hazards": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _i64, _p]),
-    "glu_plan_build": (_i64, [_i64, _p, _p, _p, _p, _i32, _i64, _i64, _i32, _pp]),
+    "glu_plan_build": (_i64, [_i64, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _i32, _pp]),
+    "glu_tail_capacity": (_i64, []),
     "glu_plan_info": (None, [_p, _p]),
     "glu_trace_read": (_i64, [_p, _p, _i64]),
     "glu_plan_export": (None, [_p, _p, _p, _p, _p, _p, _p]),

@@ -17,6 +17,7 @@
 // glu_host.cpp).  Values are read and written through L2 (ld/st.cg) so the
 // grid barrier's release/acquire makes one phase's writes visible to the
 // next without L1 invalidation.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -132,6 +133,7 @@ struct FactorParams {
     i32 n;
     i32 n_items;
     i32 n_levels;
+    i32 n_div;              // columns the final pass divides (the dense tail divides its own)
     double thresh;
     unsigned long long *fail;  // min (level << 32 | column) of failing pivots
     unsigned *done;            // per phase: completed items (stride 8 words)
@@ -752,7 +754,320 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     }
     // every phase complete -> pivot check + divide of every column
     if (P.n_levels > 0 && !wait_phase(P, P.n_levels - 1, lane, &cs)) return;
-    for (int j = gw; j < P.n; j += nw) divide_column(P, j, lane);
+    for (int j = gw; j < P.n_div; j += nw) divide_column(P, j, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Dense tail: one thread-block cluster factors the trailing m x m block
+// (columns t0..n-1, each alone in one of the last m phases) in distributed
+// shared memory, as a blocked right-looking LU with panels of b columns.
+// CTA c of C owns panels c, c+C, ... (all m tail rows of their columns,
+// dense, plus a structure bitmask).  For panel p (sources s0..s1-1):
+//   * the owner of panel p+1 first applies panel p to it, factors it
+//     (source by source, __syncthreads between sources) and publishes its
+//     divided L columns and structure to a double-buffered global slot
+//     (lookahead: the critical path never waits for trailing updates);
+//   * every CTA applies panel p to its later columns: the panel rows of a
+//     column first (a b x b triangular sweep, one warp per column), then
+//     every row below the panel with the target held in a register across
+//     the b sources;
+//   * one cluster barrier per panel.
+// Per target the MACs are the reference's: A(i,q) -= (A(i,s) / A(s,s)) *
+// A(s,q), three roundings, ascending source s (= ascending phase here), and
+// only where L(i,s) and U(s,q) are in the pattern -- bitwise identical to
+// the sparse path for both contracts.  Finally every CTA writes its columns
+// back (undivided) and pivot-checks/divides them.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+constexpr int kTailThreads = 512;
+constexpr int kTailB = 16;  // largest panel width (register arrays)
+constexpr int kTailMaxLocal = 256;  // owned columns per CTA
+
+struct TailParams {
+    double *v;
+    const i32 *col_ptr, *row_idx, *diag_pos, *level_of;
+    i32 t0, m, mpad, mw, b, np, ncl;
+    i32 gstride;  // doubles per panel slot: b x mpad divided L values, then mpad u32 row words
+                  // (bit k of row i: L(i, s0 + k) in the pattern)
+    double *G;    // 2 slots
+    double thresh;
+    unsigned long long *fail;
+    i32 fail_by_column;
+};
+
+__device__ __forceinline__ bool mbit(const unsigned long long *mk, int i) {
+    return (mk[i >> 6] >> (i & 63)) & 1ull;
+}
+// bits [s, s+len) of a row mask, len <= 16
+__device__ __forceinline__ unsigned mbits(const unsigned long long *mk, int s, int len) {
+    const int w = s >> 6, o = s & 63;
+    unsigned long long x = mk[w] >> o;
+    if (o + len > 64) x |= mk[w + 1] << (64 - o);
+    return (unsigned)(x & ((1ull << len) - 1ull));
+}
+
+__device__ __forceinline__ void divide_column_t(const TailParams &T, int j, int lane) {
+    const int lo = __ldg(T.col_ptr + j), hi = __ldg(T.col_ptr + j + 1);
+    const int d = __ldg(T.diag_pos + j);
+    double cmax = 0.0;
+    for (int p = lo + lane; p < hi; p += 32) {
+        const double av = fabs(ldv(T.v + p));
+        if (av > cmax) cmax = av;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double x = __shfl_xor_sync(0xffffffffu, cmax, o);
+        if (x > cmax) cmax = x;
+    }
+    const double piv = ldv(T.v + d);
+    if (fabs(piv) <= __dmul_rn(T.thresh, cmax)) {
+        if (lane == 0) {
+            const unsigned long long key =
+                T.fail_by_column ? (unsigned long long)j
+                                 : (((unsigned long long)__ldg(T.level_of + j)) << 32) | (unsigned)j;
+            atomicMin(T.fail, key);
+        }
+        return;
+    }
+    for (int p = d + 1 + lane; p < hi; p += 32) stv(T.v + p, __ddiv_rn(ldv(T.v + p), piv));
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
+    extern __shared__ __align__(16) double tsm[];
+    __shared__ double tri[kTailB * kTailB];   // panel rows' divided L values (row-major [i][s])
+    __shared__ unsigned tribits[kTailB];      // L structure of panel row i over the panel sources
+    __shared__ int qtab[kTailMaxLocal];       // local column -> tail column (M: none)
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), c = (int)cl.block_rank();
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = nt >> 5;
+    const int B = T.b, M = T.m;
+    double *cols = tsm;
+    unsigned long long *mk = reinterpret_cast<unsigned long long *>(tsm + (size_t)T.ncl * T.mpad);
+    const int npl = c < T.np ? (T.np - c + C - 1) / C : 0;  // owned panels
+    const int ncol = min(npl * B, T.ncl);
+    // owned column q -> local index (owner = (q / B) % C); the divisions run
+    // once here, the loops read the table
+    auto xloc = [&](int q) { return ((q / B) / C) * B + (q % B); };
+    for (int x = tid; x < kTailMaxLocal; x += nt) {
+        const int q = x < ncol ? ((x / B) * C + c) * B + (x % B) : M;
+        qtab[x] = q < M ? q : M;
+    }
+    __syncthreads();
+    auto qglob = [&](int x) { return qtab[x]; };
+    for (int x = 0; x < ncol; ++x) {
+        if (qglob(x) >= M) break;
+        for (int i = tid; i < T.mpad; i += nt) cols[(size_t)x * T.mpad + i] = 0.0;
+        for (int w = tid; w < T.mw; w += nt) mk[x * T.mw + w] = 0ull;
+    }
+    __syncthreads();
+    for (int x = 0; x < ncol; ++x) {
+        const int q = qglob(x);
+        if (q >= M) break;
+        const int j = T.t0 + q;
+        const int lo = __ldg(T.col_ptr + j), hi = __ldg(T.col_ptr + j + 1);
+        for (int p = lo + tid; p < hi; p += nt) {
+            const int r = __ldg(T.row_idx + p) - T.t0;
+            if (r >= 0) {
+                cols[(size_t)x * T.mpad + r] = ldv(T.v + p);
+                atomicOr(&mk[x * T.mw + (r >> 6)], 1ull << (r & 63));
+            }
+        }
+    }
+    __syncthreads();
+    const int ia = tid, ib = tid + nt;  // this thread's rows (m <= 2 * nt)
+
+    // Owner: factor panel pp in place (its columns already hold every update
+    // from earlier panels) and publish the divided L columns + structure.
+    auto factor_panel = [&](int pp) {
+        const int s0 = pp * B, s1 = min(s0 + B, M);
+        const int xb0 = xloc(s0);  // the panel's columns are consecutive local columns
+        double *g = T.G + (size_t)(pp & 1) * T.gstride;
+        unsigned *grow = reinterpret_cast<unsigned *>(g + (size_t)B * T.mpad);
+        unsigned bra = 0, brb = 0;
+        for (int s = s0; s < s1; ++s) {
+            const int k = s - s0, xs = xb0 + k;
+            const double *cs = cols + (size_t)xs * T.mpad;
+            const unsigned long long *ms = mk + xs * T.mw;
+            const double piv = cs[s];
+            double la = 0.0, lb = 0.0;
+            const bool ba = ia > s && ia < M && mbit(ms, ia), bb = ib > s && ib < M && mbit(ms, ib);
+            if (ba) { la = __ddiv_rn(cs[ia], piv); __stcg(g + (size_t)k * T.mpad + ia, la); bra |= 1u << k; }
+            if (bb) { lb = __ddiv_rn(cs[ib], piv); __stcg(g + (size_t)k * T.mpad + ib, lb); brb |= 1u << k; }
+#pragma unroll 4
+            for (int q = s + 1; q < s1; ++q) {
+                const int xq = xb0 + (q - s0);
+                if (!mbit(mk + xq * T.mw, s)) continue;
+                double *cq = cols + (size_t)xq * T.mpad;
+                const double mult = cq[s];
+                if (ba) cq[ia] = __dsub_rn(cq[ia], __dmul_rn(la, mult));
+                if (bb) cq[ib] = __dsub_rn(cq[ib], __dmul_rn(lb, mult));
+            }
+            __syncthreads();
+        }
+        if (ia < M) __stcg(grow + ia, bra);
+        if (ib < M) __stcg(grow + ib, brb);
+    };
+
+    // Apply panel p to the owned columns with local index in [xa, xb) that lie
+    // beyond the panel.
+    auto apply_panel = [&](int p, int xa, int xb) {
+        const int s0 = p * B, s1 = min(s0 + B, M), bp = s1 - s0;
+        const double *g = T.G + (size_t)(p & 1) * T.gstride;
+        const unsigned *grow = reinterpret_cast<const unsigned *>(g + (size_t)B * T.mpad);
+        // the b x b triangle of divided L values among the panel rows (loads
+        // are unconditional: entries outside the pattern are never used)
+        for (int e = tid; e < kTailB * kTailB; e += nt) {
+            const int i = e / kTailB, k = e % kTailB;  // panel row s0+i, source s0+k
+            tri[e] = (i < bp && k < i) ? __ldcg(g + (size_t)k * T.mpad + s0 + i) : 0.0;
+        }
+        if (tid < kTailB) tribits[tid] = tid < bp ? __ldcg(grow + s0 + tid) : 0u;
+        // this thread's rows below the panel: structure word + divided L values
+        double la[kTailB], lb[kTailB];
+        const unsigned bitsa = (ia >= s1 && ia < M) ? __ldcg(grow + ia) : 0u;
+        const unsigned bitsb = (ib >= s1 && ib < M) ? __ldcg(grow + ib) : 0u;
+        const bool ra = ia < T.mpad, rb = ib < T.mpad;
+#pragma unroll
+        for (int k = 0; k < kTailB; ++k) {
+            la[k] = (ra && k < bp) ? __ldcg(g + (size_t)k * T.mpad + ia) : 0.0;
+            lb[k] = (rb && k < bp) ? __ldcg(g + (size_t)k * T.mpad + ib) : 0.0;
+        }
+        __syncthreads();
+        // (A) panel rows of each column: a warp per column, lane = panel row
+        for (int x = xa + wid; x < xb; x += nwarp) {
+            if (qglob(x) < s1) continue;
+            double *cq = cols + (size_t)x * T.mpad;
+            const unsigned ub = mbits(mk + x * T.mw, s0, bp);
+            const unsigned lbits = lane < bp ? tribits[lane] : 0u;
+            for (int k = 0; k + 1 < bp; ++k) {
+                const double mult = cq[s0 + k];
+                if (((ub >> k) & 1u) && lane > k && lane < bp && ((lbits >> k) & 1u))
+                    cq[s0 + lane] = __dsub_rn(cq[s0 + lane], __dmul_rn(tri[lane * kTailB + k], mult));
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        // (B) rows below the panel, target in a register across the b sources
+        for (int x = xa; x < xb; ++x) {
+            if (qglob(x) < s1) continue;
+            double *cq = cols + (size_t)x * T.mpad;
+            const unsigned ub = mbits(mk + x * T.mw, s0, bp);
+            const unsigned ua = ub & bitsa, ubb = ub & bitsb;
+            if (ua) {
+                double t = cq[ia];
+#pragma unroll
+                for (int k = 0; k < kTailB; ++k)
+                    if ((ua >> k) & 1u) t = __dsub_rn(t, __dmul_rn(la[k], cq[s0 + k]));
+                cq[ia] = t;
+            }
+            if (ubb) {
+                double t = cq[ib];
+#pragma unroll
+                for (int k = 0; k < kTailB; ++k)
+                    if ((ubb >> k) & 1u) t = __dsub_rn(t, __dmul_rn(lb[k], cq[s0 + k]));
+                cq[ib] = t;
+            }
+        }
+        __syncthreads();
+    };
+
+    if (T.np > 0 && c == 0) factor_panel(0);
+    cl.sync();
+    for (int p = 0; p < T.np; ++p) {
+        const int pn = p + 1;
+        const bool own_next = pn < T.np && (pn % C) == c;
+        if (own_next) {  // lookahead: the next panel first
+            const int xn = xloc(pn * B);
+            apply_panel(p, xn, min(xn + B, ncol));
+            factor_panel(pn);
+            const int xl = xn + B;
+            apply_panel(p, 0, xn);
+            apply_panel(p, xl, ncol);
+        } else {
+            apply_panel(p, 0, ncol);
+        }
+        cl.sync();
+    }
+    for (int x = 0; x < ncol; ++x) {
+        const int q = qglob(x);
+        if (q >= M) break;
+        const int j = T.t0 + q;
+        const int lo = __ldg(T.col_ptr + j), hi = __ldg(T.col_ptr + j + 1);
+        for (int p = lo + tid; p < hi; p += nt) {
+            const int r = __ldg(T.row_idx + p) - T.t0;
+            if (r >= 0) stv(T.v + p, cols[(size_t)x * T.mpad + r]);
+        }
+    }
+    __syncthreads();
+    for (int x = wid; x < ncol; x += nwarp)
+        if (qglob(x) < M) divide_column_t(T, T.t0 + qglob(x), lane);
+}
+
+struct TailShape;
+int tail_gstride(const TailShape &t);
+struct TailShape {
+    int C = 0, b = 0, np = 0;
+    size_t smem = 0;
+    int mpad = 0, mw = 0, ncl = 0;
+};
+
+int tail_gstride(const TailShape &t) {
+    return (int)((((size_t)t.b * t.mpad + (size_t)t.mpad / 2 + 1) + 31) & ~(size_t)31);
+}
+
+TailShape tail_shape(int m, int C, int b) {
+    TailShape t;
+    t.C = C;
+    t.b = b;
+    t.mpad = (m + 1) & ~1;
+    t.mw = (m + 63) / 64;
+    t.np = (m + b - 1) / b;
+    t.ncl = ((t.np + C - 1) / C) * b;
+    t.smem = (size_t)t.ncl * t.mpad * sizeof(double) + (size_t)t.ncl * t.mw * sizeof(unsigned long long);
+    return t;
+}
+
+// Largest launchable cluster whose shared memory holds an m-column tail, with
+// the widest panel that fits (m <= 0: report the capacity only).
+TailShape pick_tail(int m, int *cap_out) {
+    int dev = 0, optin = 0;
+    TailShape best;
+    if (cap_out) *cap_out = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return best;
+    const size_t budget = (size_t)optin - sizeof(double) * kTailB * kTailB - 4 * kTailB - 1024;
+    cudaFuncSetAttribute((const void *)tail_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute((const void *)tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    for (int C : {16, 8, 4, 2}) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(C);
+        cfg.blockDim = dim3(kTailThreads);
+        cfg.dynamicSmemBytes = budget;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, (const void *)tail_kernel, &cfg) != cudaSuccess ||
+            nclusters < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        int cap = 0;
+        auto fits = [&](int mm, int bb) {
+            const TailShape t = tail_shape(mm, C, bb);
+            return t.smem <= budget && t.ncl <= kTailMaxLocal;
+        };
+        while (cap + 1 <= 2 * kTailThreads && fits(cap + 1, 4)) ++cap;
+        if (cap_out && cap > *cap_out) *cap_out = cap;
+        if (m > 0)
+            for (int b : {16, 8, 4})
+                if (fits(m, b)) return tail_shape(m, C, b);
+    }
+    return best;
 }
 
 // ---------------------------------------------------------------------------
@@ -857,6 +1172,9 @@ struct glu_handle {
     // plan
     i32 *level_need = nullptr;  // per phase: item count
     i32 *col_total = nullptr;   // per column: items into it
+    i64 tail_t0 = 0;            // dense cluster tail: columns [tail_t0, n)
+    TailShape tail;
+    double *tail_g = nullptr;
     unsigned *sync = nullptr;   // done[n_levels*8] | err (+pad) | col_done[n]
     size_t sync_words = 0;
     Item *items = nullptr;
@@ -957,6 +1275,17 @@ int coop_grid(const void *kernel, int sm_count, size_t dyn_smem = 0) {
 
 extern "C" const char *glu_version(void) { return "glu_b200 0.1 sm_100a"; }
 
+extern "C" int64_t glu_tail_capacity(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return 0;
+    }
+    int cap = 0;
+    pick_tail(0, &cap);
+    return cap;
+}
+
 extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                               const int64_t *diag_pos, const int64_t *row_ptr,
                               const int64_t *col_idx, const int64_t *csc_pos,
@@ -1001,6 +1330,21 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         UP(h->level_need, need);
         h->sync_words = (size_t)std::max<i64>(pv.n_levels, 1) * 8 + kLineWords + (size_t)std::max<i64>(n, 1) * kColRep;
         UP(h->col_total, std::vector<i32>(pv.col_total, pv.col_total + n));
+        h->tail_t0 = pv.tail_t0;
+        const i64 m = n - pv.tail_t0;
+        if (m > 0) {
+            h->tail = pick_tail((int)m, nullptr);
+            if (h->tail.C == 0) {
+                glu::set_error("dense tail of " + std::to_string(m) +
+                               " columns exceeds this device's cluster capacity (glu_tail_capacity)");
+                return fail(GLU_EINVAL);
+            }
+            const size_t gstride = (size_t)tail_gstride(h->tail);
+            if (cudaMalloc((void **)&h->tail_g, 2 * gstride * sizeof(double)) != cudaSuccess) {
+                glu::set_error("cudaMalloc(tail buffer)");
+                return fail(GLU_ECUDA);
+            }
+        }
         if (cudaMalloc((void **)&h->sync, h->sync_words * sizeof(unsigned)) != cudaSuccess) {
             glu::set_error("cudaMalloc(sync)");
             return fail(GLU_ECUDA);
@@ -1042,7 +1386,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
 
 extern "C" void glu_destroy(glu_handle *h) {
     if (!h) return;
-    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->sync, h->items,
+    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->sync, h->tail_g, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
                     h->bar, h->ifail, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x};
@@ -1164,6 +1508,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.n = (i32)h->n;
     P.n_items = (i32)h->n_items;
     P.n_levels = (i32)h->n_levels;
+    P.n_div = (i32)h->tail_t0;
     P.thresh = thresh;
     P.fail = h->fail;
     const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
@@ -1189,6 +1534,39 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     }
     GLU_CUDA(cudaLaunchCooperativeKernel((const void *)factor_kernel, dim3(h->grid), dim3(kThreads),
                                          args, kFactorDynSmem, s));
+    if (h->tail_t0 < h->n) {
+        TailParams T;
+        T.v = v;
+        T.col_ptr = h->col_ptr;
+        T.row_idx = h->row_idx;
+        T.diag_pos = h->diag_pos;
+        T.level_of = h->level_of;
+        T.t0 = (i32)h->tail_t0;
+        T.m = (i32)(h->n - h->tail_t0);
+        T.mpad = h->tail.mpad;
+        T.mw = h->tail.mw;
+        T.b = h->tail.b;
+        T.np = h->tail.np;
+        T.ncl = h->tail.ncl;
+        T.gstride = tail_gstride(h->tail);
+        T.G = h->tail_g;
+        T.thresh = thresh;
+        T.fail = h->fail;
+        T.fail_by_column = h->fail_by_column ? 1 : 0;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = h->tail.C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(h->tail.C);
+        cfg.blockDim = dim3(kTailThreads);
+        cfg.dynamicSmemBytes = h->tail.smem;
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        GLU_CUDA(cudaLaunchKernelEx(&cfg, tail_kernel, T));
+    }
     return GLU_OK;
 }
 

@@ -496,6 +496,7 @@ struct glu_plan {
     std::vector<uint8_t> map8;
     std::vector<uint16_t> tgt16;
     std::vector<i32> col_total;
+    i64 tail_t0 = 0, tail_macs = 0;
     i64 max_item_macs = 0;
     i64 max_chunks = 0;
     i64 deferred = 0;
@@ -507,10 +508,28 @@ static constexpr i64 kMaxSpan = 65535;
 static constexpr i64 kTargetItemsPerPhase = 148 * 16 / 4;  // a quarter of the resident warps
 static constexpr i64 kMinItemMacs = 32;
 
+// Dense tail: the longest suffix of columns t0..n-1 that are each alone in
+// their phase, in index order, and are the last phases of the schedule (at
+// most tail_max columns, at least kTailMin).  Its MACs are left to the
+// cluster tail kernel (glu_device.cu), which applies them column by column
+// -- ascending source order, i.e. both contracts' order -- after every MAC
+// of the plan (all from earlier phases and lower sources) is done.
+static constexpr i64 kTailMin = 16;
+
+static i64 find_tail(i64 n, const int64_t *level_of, i64 n_levels, i64 tail_max) {
+    if (tail_max <= 0 || n == 0) return n;
+    std::vector<i64> size(n_levels, 0);
+    for (i64 j = 0; j < n; j++) size[level_of[j]]++;
+    i64 j = n - 1;
+    while (j >= 0 && n - j <= tail_max && size[level_of[j]] == 1 && level_of[j] == n_levels - (n - j)) j--;
+    const i64 t0 = j + 1;
+    return n - t0 >= kTailMin ? t0 : n;
+}
+
 extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                                   const int64_t *diag_pos, const int64_t *level_of,
                                   int32_t contract, int64_t max_item_macs, int64_t deep_min,
-                                  int32_t n_threads, glu_plan **out) {
+                                  int64_t tail_max, int32_t n_threads, glu_plan **out) {
     *out = nullptr;
     if (contract != GLU_CONTRACT_A && contract != GLU_CONTRACT_B) {
         set_error("contract must be GLU_CONTRACT_A or GLU_CONTRACT_B");
@@ -523,12 +542,15 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     const i64 D = deep_min > 0 ? deep_min : 8;
     i64 n_levels = 0;
     for (i64 j = 0; j < n; j++) n_levels = std::max(n_levels, level_of[j] + 1);
+    const i64 t0 = find_tail(n, level_of, n_levels, tail_max);
     // per-phase MAC totals (at the source's level) -> per-phase item size T
     std::vector<i64> phase_macs(n_levels, 0);
+    i64 tail_macs = 0;
     for (i64 k = 0; k < n; k++)
         for (i64 m = col_ptr[k]; m < diag_pos[k]; m++) {
             const i64 j = row_idx[m];
-            phase_macs[level_of[j]] += col_ptr[j + 1] - diag_pos[j] - 1;
+            if (j >= t0) tail_macs += col_ptr[j + 1] - diag_pos[j] - 1;
+            else phase_macs[level_of[j]] += col_ptr[j + 1] - diag_pos[j] - 1;
         }
     // Item size: every item costs one dependency wait and one round of
     // loads whatever its size (all of a lane's entries load together), so
@@ -577,6 +599,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                 bool bad = false;
                 for (i64 m = cb; m < diag_pos[k] && !bad; m++) {
                     i64 j = row_idx[m];
+                    if (j >= t0) break;  // tail sources: the cluster tail kernel
                     i64 lo = diag_pos[j] + 1, hi = col_ptr[j + 1];
                     if (lo >= hi) continue;
                     i32 lj = (i32)level_of[j];
@@ -773,6 +796,8 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     });
     auto *plan = new glu_plan();
     plan->n_levels = n_levels;
+    plan->tail_t0 = t0;
+    plan->tail_macs = tail_macs;
     plan->level_item_ptr.assign(n_levels + 1, 0);
     plan->items.reserve(refs.size());
     plan->chunks.reserve(total_chunks);
@@ -835,7 +860,7 @@ extern "C" void glu_plan_info(const glu_plan *p, int64_t *info) {
     info[0] = p->n_levels;
     info[1] = (i64)p->items.size();
     info[2] = (i64)p->chunks.size();
-    info[3] = (i64)p->map8.size() + (i64)p->deep.size();
+    info[3] = (i64)p->map8.size() + (i64)p->deep.size() + p->tail_macs;
     info[4] = p->max_item_macs;
     info[5] = p->max_chunks;
     info[6] = p->deferred;
@@ -847,7 +872,9 @@ extern "C" void glu_plan_info(const glu_plan *p, int64_t *info) {
     info[10] = p->n_epochs;
     info[11] = (i64)p->map8.size();
     info[12] = (i64)p->tgt16.size();
-    info[13] = info[14] = info[15] = 0;
+    info[13] = p->tail_t0;
+    info[14] = p->tail_macs;
+    info[15] = 0;
 }
 
 extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
@@ -897,6 +924,7 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.tgt16 = p->tgt16.data();
     v.n_tgt = (i64)p->tgt16.size();
     v.col_total = p->col_total.data();
+    v.tail_t0 = p->tail_t0;
     return v;
 }
 }  // namespace glu

@@ -70,6 +70,7 @@ struct glu_plan_view {
     const uint16_t *tgt16;
     int64_t n_tgt;
     const int32_t *col_total;  // per column: items into it (all phases)
+    int64_t tail_t0;           // columns >= tail_t0: dense cluster tail (n: none)
 };
 
 const glu_plan_view plan_view(const glu_plan *p);

@@ -128,7 +128,8 @@ class Factorizer:
     """
 
     def __init__(self, fp: FilledPattern, level_of: np.ndarray, contract: int,
-                 max_item_macs: int = 0, threads: int = 0, deep_min: int = 0):
+                 max_item_macs: int = 0, threads: int = 0, deep_min: int = 0,
+                 tail_max: int | None = None):
         self.n = fp.n
         self.nnz = fp.nnz
         self.contract = contract
@@ -138,6 +139,7 @@ class Factorizer:
         plan = ctypes.c_void_p()
         rc = _lib.check(_lib.lib.glu_plan_build(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
                                                 _lib.ptr(lv), contract, max_item_macs, deep_min,
+                                                _tail_capacity() if tail_max is None else tail_max,
                                                 threads, ctypes.byref(plan)), "glu_plan_build")
         if rc == _lib.GLU_MISMATCH:
             raise PatternMismatchError("update targeted a structurally absent slot")
@@ -146,7 +148,8 @@ class Factorizer:
             _lib.lib.glu_plan_info(plan, _lib.ptr(info))
             self.plan_info = dict(zip(("levels", "items", "chunks", "macs", "max_item_macs",
                                        "max_chunks", "deferred_macs", "plan_bytes", "deep_items",
-                                       "deep_macs", "epochs", "push_macs", "targets"),
+                                       "deep_macs", "epochs", "push_macs", "targets", "tail_t0",
+                                       "tail_macs"),
                                       info.tolist()))
             h = ctypes.c_void_p()
             rc = _lib.check(_lib.lib.glu_create(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
@@ -235,6 +238,17 @@ class Factorizer:
         ms = np.zeros(max(m, 1), dtype=np.float64)
         k = _lib.lib.glu_level_times(self._h, _lib.ptr(ms), m)
         return (ms[:k] * 1e-3).tolist()
+
+
+_TAIL_CAP = None
+
+
+def _tail_capacity() -> int:
+    """Dense-tail columns the device's cluster kernel can hold (queried once)."""
+    global _TAIL_CAP
+    if _TAIL_CAP is None:
+        _TAIL_CAP = int(_lib.lib.glu_tail_capacity())
+    return _TAIL_CAP
 
 
 def _dptr(x):

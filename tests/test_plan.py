@@ -19,12 +19,12 @@ from paper_1908_00204_b200 import _lib
 from conftest import csc_from_golden, load_golden
 
 
-def export_plan(fp, level_of, contract, max_item_macs=0, deep_min=0):
+def export_plan(fp, level_of, contract, max_item_macs=0, deep_min=0, tail_max=0):
     cp, ri, dp = _lib.i64(fp.full.col_ptr), _lib.i64(fp.full.row_idx), _lib.i64(fp.diag_pos)
     lv = _lib.i64(level_of)
     h = ctypes.c_void_p()
     rc = _lib.lib.glu_plan_build(fp.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp), _lib.ptr(lv),
-                                 contract, max_item_macs, deep_min, 2, ctypes.byref(h))
+                                 contract, max_item_macs, deep_min, tail_max, 2, ctypes.byref(h))
     assert rc == _lib.GLU_OK, _lib.last_error()
     info = np.zeros(16, dtype=np.int64)
     _lib.lib.glu_plan_info(h, _lib.ptr(info))
@@ -79,6 +79,20 @@ def emulate(fp, level_of, plan, v, thresh, rng=None):
                 stage[u] = stage[u] - (v[p] / v[d]) * v[m]
             assert e == moff + macs
             v[slots] = stage
+    # dense tail: columns >= t0, one source column at a time in index order
+    t0 = int(plan["info"][13])
+    cp_, dp_ = fp.full.col_ptr, fp.diag_pos
+    for j in range(t0, fp.n):
+        lrows = ri[dp_[j] + 1:cp_[j + 1]]
+        for t in range(fp.csr.row_ptr[j], fp.csr.row_ptr[j + 1]):
+            k = fp.csr.col_idx[t]
+            if k <= j:
+                continue
+            m = fp.csr.csc_pos[t]
+            rows_k = ri[cp_[k]:cp_[k + 1]]
+            q = cp_[k] + np.searchsorted(rows_k, lrows)
+            p = np.arange(dp_[j] + 1, cp_[j + 1])
+            v[q] = v[q] - (v[p] / v[dp_[j]]) * v[m]
     fail = None
     cp, dp = fp.full.col_ptr, fp.diag_pos
     for j in range(fp.n):
@@ -103,15 +117,16 @@ CASES = ["conflict8", "random_dd_s2_n80", "random_dd_s3_n120", "random_dd_s5_n10
 
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("contract", [_lib.CONTRACT_A, _lib.CONTRACT_B])
-@pytest.mark.parametrize("max_item_macs,deep_min", [(0, 0), (7, 0), (0, 2), (5, 1000)])
-def test_plan_emulation_bitwise(case, contract, max_item_macs, deep_min):
+@pytest.mark.parametrize("max_item_macs,deep_min,tail_max", [(0, 0, 0), (7, 0, 0), (0, 2, 0),
+                                                              (5, 1000, 0), (0, 0, 1000)])
+def test_plan_emulation_bitwise(case, contract, max_item_macs, deep_min, tail_max):
     g = load_golden(case)
     a = csc_from_golden(g)
     fp = glu.symbolic_fillin(a.pattern)
     level_of = g["level_of"]
-    plan = export_plan(fp, level_of, contract, max_item_macs, deep_min)
+    plan = export_plan(fp, level_of, contract, max_item_macs, deep_min, tail_max)
     assert int(plan["info"][3]) == glu.pattern_flops(fp)[0]  # every MAC planned once
-    assert int(plan["info"][11]) + int(plan["info"][9]) == int(plan["info"][3])
+    assert int(plan["info"][11]) + int(plan["info"][9]) + int(plan["info"][14]) == int(plan["info"][3])
     push = plan["items"][plan["items"][:, 7] == 0]
     assert int(push[:, 6].sum()) == int(plan["info"][11])
     assert int(push[:, 5].sum()) == int(plan["info"][12])

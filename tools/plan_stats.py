@@ -16,13 +16,14 @@ s = glu.levelize(glu.detect_relaxed(fp))
 t = time.time()
 pp = ctypes.c_void_p()
 rc = _lib.lib.glu_plan_build(a.n, _lib.ptr(fp.full.col_ptr), _lib.ptr(fp.full.row_idx),
-                             _lib.ptr(fp.diag_pos), _lib.ptr(_lib.i64(s.level_of)), contract, T, D, 0,
+                             _lib.ptr(fp.diag_pos), _lib.ptr(_lib.i64(s.level_of)), contract, T, D,
+                             int(sys.argv[5]) if len(sys.argv) > 5 else 0, 0,
                              ctypes.byref(pp))
 print("plan build s", round(time.time() - t, 2), rc)
 info = np.zeros(16, np.int64)
 _lib.lib.glu_plan_info(pp, _lib.ptr(info))
 names = ("levels", "items", "chunks", "macs", "max_item_macs", "max_chunks", "deferred", "bytes",
-         "deep_items", "deep_macs", "epochs", "push_macs", "targets")
+         "deep_items", "deep_macs", "epochs", "push_macs", "targets", "tail_t0", "tail_macs")
 print(dict(zip(names, info.tolist())))
 nl, ni, nc, nd = info[0], info[1], info[2], info[9]
 lip = np.zeros(nl + 1, np.int64); items = np.zeros(ni * 8, np.int64); ch = np.zeros(nc * 5, np.int64)
