@@ -342,13 +342,11 @@ def run_ours(args):
     # parity spot check of the last step vs the CPU oracle (rank 0), and the
     # final gather of per-rank checksums (the only collective)
     lu_last = v.cpu().numpy()
-    import hashlib
+    from paper_1908_00204_b200 import batch as glu_batch
 
-    digest = int.from_bytes(hashlib.sha256(lu_last.tobytes()).digest()[:8], "little") >> 1
-    if world > 1:
-        g = torch.tensor([digest], dtype=torch.int64, device=dev)
-        allg = [torch.zeros_like(g) for _ in range(world)]
-        torch.distributed.all_gather(allg, g)
+    last_set = rank * nsets + (args.steps - 1) % nsets  # global value-set id
+    if world > 1:  # (set id, status, LU checksum) of every rank: the only collective
+        glu_batch.gather_results([last_set], [fz.status(stream)], [glu_batch.set_digest(lu_last)])
     parity = None
     cpu = None
     if rank == 0:

@@ -181,11 +181,19 @@ int64_t glu_factor_device(glu_handle *h, double *v, double thresh, void *stream)
 int64_t glu_factor_device_async(glu_handle *h, double *v, double thresh, void *stream);
 int64_t glu_factor_status(glu_handle *h, void *stream);
 
-/* Batch refactorization: `batch` value sets stored batch-minor
-   (v[slot*batch + b]) on the device; fail_cols (host, batch) receives
-   GLU_OK or the failing column per matrix. */
+/* Batch refactorization (many value sets on one pattern: the Newton /
+   transient steps the reference re-calls factor_parallel for).
+   v (device) holds `batch` A_s-slot value sets batch-major (set b at
+   v + b * nnz), factored in place in stream order; fail_cols (host, batch)
+   receives GLU_OK or the failing pivot column per set.  Returns GLU_OK or
+   an error code. */
 int64_t glu_factor_batch_device(glu_handle *h, int64_t batch, double *v, double thresh,
                                 int64_t *fail_cols, void *stream);
+/* Host-buffer batch: a_vals [batch][nz] (A values in the pattern given to
+   glu_set_input_pattern) in, LU values [batch][nnz] out, per-set status in
+   fail_cols. */
+int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const double *a_vals, double *lu_out,
+                              double thresh, int64_t *fail_cols);
 
 /* numeric.py:354-378 solve: x (device, n) holds b on entry, x on exit.
    lu (device) are factor values. Returns GLU_OK or the column of a zero

@@ -62,6 +62,7 @@ SIGNATURES = {
     "glu_factor_device_async": (_i64, [_p, _p, _dbl, _p]),
     "glu_factor_status": (_i64, [_p, _p]),
     "glu_factor_batch_device": (_i64, [_p, _i64, _p, _dbl, _p, _p]),
+    "glu_factor_batch_host": (_i64, [_p, _i64, _p, _p, _dbl, _p]),
     "glu_solve_device": (_i64, [_p, _p, _p, _p]),
     "glu_lower_solve_device": (_i64, [_p, _p, _p, _p]),
     "glu_upper_solve_device": (_i64, [_p, _p, _p, _p]),

@@ -837,6 +837,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     __shared__ double tri[kTailB * kTailB];   // panel rows' divided L values (row-major [i][s])
     __shared__ unsigned tribits[kTailB];      // L structure of panel row i over the panel sources
     __shared__ int qtab[kTailMaxLocal];       // local column -> tail column (M: none)
+    __shared__ double urow[2][kTailB];        // factor_panel: U(s, panel) broadcast
+    __shared__ unsigned ubits[2];
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks(), c = (int)cl.block_rank();
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = nt >> 5;
@@ -878,34 +880,75 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
 
     // Owner: factor panel pp in place (its columns already hold every update
     // from earlier panels) and publish the divided L columns + structure.
+    // The panel lives in registers while it is factored: each thread holds
+    // its rows of the b panel columns; per source one __syncthreads, through
+    // which the owner of row s broadcasts U(s, panel) and its structure.
     auto factor_panel = [&](int pp) {
-        const int s0 = pp * B, s1 = min(s0 + B, M);
+        const int s0 = pp * B, s1 = min(s0 + B, M), bp = s1 - s0;
         const int xb0 = xloc(s0);  // the panel's columns are consecutive local columns
         double *g = T.G + (size_t)(pp & 1) * T.gstride;
         unsigned *grow = reinterpret_cast<unsigned *>(g + (size_t)B * T.mpad);
-        unsigned bra = 0, brb = 0;
-        for (int s = s0; s < s1; ++s) {
-            const int k = s - s0, xs = xb0 + k;
-            const double *cs = cols + (size_t)xs * T.mpad;
-            const unsigned long long *ms = mk + xs * T.mw;
-            const double piv = cs[s];
-            double la = 0.0, lb = 0.0;
-            const bool ba = ia > s && ia < M && mbit(ms, ia), bb = ib > s && ib < M && mbit(ms, ib);
-            if (ba) { la = __ddiv_rn(cs[ia], piv); __stcg(g + (size_t)k * T.mpad + ia, la); bra |= 1u << k; }
-            if (bb) { lb = __ddiv_rn(cs[ib], piv); __stcg(g + (size_t)k * T.mpad + ib, lb); brb |= 1u << k; }
-#pragma unroll 4
-            for (int q = s + 1; q < s1; ++q) {
-                const int xq = xb0 + (q - s0);
-                if (!mbit(mk + xq * T.mw, s)) continue;
-                double *cq = cols + (size_t)xq * T.mpad;
-                const double mult = cq[s];
-                if (ba) cq[ia] = __dsub_rn(cq[ia], __dmul_rn(la, mult));
-                if (bb) cq[ib] = __dsub_rn(cq[ib], __dmul_rn(lb, mult));
+        double ra[kTailB], rb[kTailB];
+        unsigned pa = 0, pb = 0;  // bit k: row ia / ib is in panel column s0+k
+#pragma unroll
+        for (int k = 0; k < kTailB; ++k) {
+            ra[k] = 0.0;
+            rb[k] = 0.0;
+            if (k < bp) {
+                const double *cq = cols + (size_t)(xb0 + k) * T.mpad;
+                const unsigned long long *mq = mk + (xb0 + k) * T.mw;
+                if (ia < M) { ra[k] = cq[ia]; pa |= (unsigned)mbit(mq, ia) << k; }
+                if (ib < M) { rb[k] = cq[ib]; pb |= (unsigned)mbit(mq, ib) << k; }
             }
-            __syncthreads();
+        }
+        unsigned bra = 0, brb = 0;
+#pragma unroll
+        for (int k = 0; k < kTailB; ++k) {
+            if (k < bp) {
+                const int s = s0 + k;
+                double *ur = urow[k & 1];
+                if (ia == s) {
+#pragma unroll
+                    for (int kk = 0; kk < kTailB; ++kk) ur[kk] = ra[kk];
+                    ubits[k & 1] = pa;
+                }
+                if (ib == s) {
+#pragma unroll
+                    for (int kk = 0; kk < kTailB; ++kk) ur[kk] = rb[kk];
+                    ubits[k & 1] = pb;
+                }
+                __syncthreads();
+                const double piv = ur[k];
+                const unsigned ub = ubits[k & 1];
+                const bool ba = ia > s && ia < M && ((pa >> k) & 1u);
+                const bool bb = ib > s && ib < M && ((pb >> k) & 1u);
+                double la = 0.0, lb = 0.0;
+                if (ba) { la = __ddiv_rn(ra[k], piv); __stcg(g + (size_t)k * T.mpad + ia, la); bra |= 1u << k; }
+                if (bb) { lb = __ddiv_rn(rb[k], piv); __stcg(g + (size_t)k * T.mpad + ib, lb); brb |= 1u << k; }
+                // branch-free: every product is formed, the subtraction is
+                // selected only where L(i,s) and U(s,q) are in the pattern
+                const unsigned ma = ba ? ub : 0u, mb = bb ? ub : 0u;
+#pragma unroll
+                for (int kk = k + 1; kk < kTailB; ++kk) {
+                    const double u = ur[kk];
+                    const double ta = __dsub_rn(ra[kk], __dmul_rn(la, u));
+                    const double tb = __dsub_rn(rb[kk], __dmul_rn(lb, u));
+                    ra[kk] = ((ma >> kk) & 1u) ? ta : ra[kk];
+                    rb[kk] = ((mb >> kk) & 1u) ? tb : rb[kk];
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kTailB; ++k) {
+            if (k < bp) {
+                double *cq = cols + (size_t)(xb0 + k) * T.mpad;
+                if (ia < M) cq[ia] = ra[k];
+                if (ib < M) cq[ib] = rb[k];
+            }
         }
         if (ia < M) __stcg(grow + ia, bra);
         if (ib < M) __stcg(grow + ib, brb);
+        __syncthreads();
     };
 
     // Apply panel p to the owned columns with local index in [xa, xb) that lie
@@ -952,19 +995,28 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
             double *cq = cols + (size_t)x * T.mpad;
             const unsigned ub = mbits(mk + x * T.mw, s0, bp);
             const unsigned ua = ub & bitsa, ubb = ub & bitsb;
-            if (ua) {
-                double t = cq[ia];
+            if (ua | ubb) {  // branch-free inner chain (selected subtractions)
+                double u[kTailB];
 #pragma unroll
-                for (int k = 0; k < kTailB; ++k)
-                    if ((ua >> k) & 1u) t = __dsub_rn(t, __dmul_rn(la[k], cq[s0 + k]));
-                cq[ia] = t;
-            }
-            if (ubb) {
-                double t = cq[ib];
+                for (int k = 0; k < kTailB; ++k) u[k] = k < bp ? cq[s0 + k] : 0.0;
+                if (ua) {
+                    double t = cq[ia];
 #pragma unroll
-                for (int k = 0; k < kTailB; ++k)
-                    if ((ubb >> k) & 1u) t = __dsub_rn(t, __dmul_rn(lb[k], cq[s0 + k]));
-                cq[ib] = t;
+                    for (int k = 0; k < kTailB; ++k) {
+                        const double r = __dsub_rn(t, __dmul_rn(la[k], u[k]));
+                        t = ((ua >> k) & 1u) ? r : t;
+                    }
+                    cq[ia] = t;
+                }
+                if (ubb) {
+                    double t = cq[ib];
+#pragma unroll
+                    for (int k = 0; k < kTailB; ++k) {
+                        const double r = __dsub_rn(t, __dmul_rn(lb[k], u[k]));
+                        t = ((ubb >> k) & 1u) ? r : t;
+                    }
+                    cq[ib] = t;
+                }
             }
         }
         __syncthreads();
@@ -1035,7 +1087,9 @@ TailShape pick_tail(int m, int *cap_out) {
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
         return best;
-    const size_t budget = (size_t)optin - sizeof(double) * kTailB * kTailB - 4 * kTailB - 1024;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, (const void *)tail_kernel) != cudaSuccess) return best;
+    const size_t budget = (size_t)optin - fa.sharedSizeBytes;  // dynamic = opt-in limit - static
     cudaFuncSetAttribute((const void *)tail_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute((const void *)tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
     for (int C : {16, 8, 4, 2}) {
@@ -1175,6 +1229,8 @@ struct glu_handle {
     i64 tail_t0 = 0;            // dense cluster tail: columns [tail_t0, n)
     TailShape tail;
     double *tail_g = nullptr;
+    unsigned long long *fail_batch = nullptr;
+    i64 fail_batch_cap = 0;
     unsigned *sync = nullptr;   // done[n_levels*8] | err (+pad) | col_done[n]
     size_t sync_words = 0;
     Item *items = nullptr;
@@ -1386,7 +1442,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
 
 extern "C" void glu_destroy(glu_handle *h) {
     if (!h) return;
-    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->sync, h->tail_g, h->items,
+    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
                     h->bar, h->ifail, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x};
@@ -1491,8 +1547,10 @@ extern "C" int64_t glu_scatter_device(glu_handle *h, const double *a_vals, doubl
     return GLU_OK;
 }
 
-static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream_t s) {
-    GLU_CUDA(cudaMemsetAsync(h->fail, 0xff, sizeof(unsigned long long), s));
+static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream_t s,
+                             unsigned long long *fail = nullptr) {
+    if (!fail) fail = h->fail;
+    GLU_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
     GLU_CUDA(cudaMemsetAsync(h->sync, 0, h->sync_words * sizeof(unsigned), s));
     FactorParams P;
     P.v = v;
@@ -1510,7 +1568,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.n_levels = (i32)h->n_levels;
     P.n_div = (i32)h->tail_t0;
     P.thresh = thresh;
-    P.fail = h->fail;
+    P.fail = fail;
     const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
     P.done = h->sync;
     P.col_done = h->sync + nl8 + kLineWords;
@@ -1551,7 +1609,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         T.gstride = tail_gstride(h->tail);
         T.G = h->tail_g;
         T.thresh = thresh;
-        T.fail = h->fail;
+        T.fail = fail;
         T.fail_by_column = h->fail_by_column ? 1 : 0;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
@@ -1612,13 +1670,69 @@ extern "C" int64_t glu_factor_status(glu_handle *h, void *stream) {
     return read_fail(h, (cudaStream_t)stream);
 }
 
+static int64_t ensure_staging(glu_handle *h);
+
+// Batch refactorization (cfg5: many value sets on one pattern, e.g. the
+// Newton / transient steps of a circuit simulation).  Value sets are
+// batch-major (set b at v + b * nnz); every set is factored in stream order
+// by the same resident plan, each with its own failure slot, and the
+// statuses are read back once for the whole batch.
+static int64_t ensure_batch(glu_handle *h, int64_t batch) {
+    if (batch <= h->fail_batch_cap) return GLU_OK;
+    if (h->fail_batch) cudaFree(h->fail_batch);
+    h->fail_batch = nullptr;
+    GLU_CUDA(cudaMalloc((void **)&h->fail_batch, sizeof(unsigned long long) * batch));
+    h->fail_batch_cap = batch;
+    return GLU_OK;
+}
+
+static int64_t batch_status(glu_handle *h, int64_t batch, int64_t *fail_cols, cudaStream_t s) {
+    std::vector<unsigned long long> keys((size_t)batch);
+    int err = 0;
+    const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
+    GLU_CUDA(cudaMemcpyAsync(keys.data(), h->fail_batch, sizeof(unsigned long long) * batch,
+                             cudaMemcpyDeviceToHost, s));
+    GLU_CUDA(cudaMemcpyAsync(&err, h->sync + nl8, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GLU_CUDA(cudaStreamSynchronize(s));
+    if (err) {
+        glu::set_error("factor kernel watchdog: a phase dependency wait exceeded 4 s");
+        return GLU_ECUDA;
+    }
+    for (int64_t b = 0; b < batch; b++)
+        fail_cols[b] = keys[b] == ~0ull ? GLU_OK : (int64_t)(keys[b] & 0xffffffffull);
+    return GLU_OK;
+}
+
 extern "C" int64_t glu_factor_batch_device(glu_handle *h, int64_t batch, double *v, double thresh,
                                            int64_t *fail_cols, void *stream) {
-    // batch-minor layout: run the single-matrix kernel per value set on a
-    // strided view is not possible; batched kernel arrives with the batch plan.
-    (void)h; (void)batch; (void)v; (void)thresh; (void)fail_cols; (void)stream;
-    glu::set_error("glu_factor_batch_device: not implemented yet");
-    return GLU_EINVAL;
+    if (batch < 0 || (batch > 0 && (!v || !fail_cols))) { glu::set_error("bad batch arguments"); return GLU_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    i64 rc = ensure_batch(h, std::max<int64_t>(batch, 1));
+    if (rc != GLU_OK) return rc;
+    for (int64_t b = 0; b < batch; b++)
+        if ((rc = launch_factor(h, v + b * h->nnz, thresh, s, h->fail_batch + b)) != GLU_OK) return rc;
+    return batch_status(h, batch, fail_cols, s);
+}
+
+extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const double *a_vals,
+                                         double *lu_out, double thresh, int64_t *fail_cols) {
+    if (h->nz < 0) { glu::set_error("glu_set_input_pattern not called"); return GLU_EINVAL; }
+    if (batch < 0 || (batch > 0 && (!a_vals || !lu_out || !fail_cols))) {
+        glu::set_error("bad batch arguments");
+        return GLU_EINVAL;
+    }
+    i64 rc = ensure_staging(h);
+    if (rc != GLU_OK) return rc;
+    if ((rc = ensure_batch(h, std::max<int64_t>(batch, 1))) != GLU_OK) return rc;
+    cudaStream_t s = h->stream;
+    // one set in flight on the device staging buffers; copies are stream-ordered
+    for (int64_t b = 0; b < batch; b++) {
+        GLU_CUDA(cudaMemcpyAsync(h->d_a, a_vals + b * h->nz, sizeof(double) * h->nz, cudaMemcpyHostToDevice, s));
+        if ((rc = glu_scatter_device(h, h->d_a, h->d_v, s)) != GLU_OK) return rc;
+        if ((rc = launch_factor(h, h->d_v, thresh, s, h->fail_batch + b)) != GLU_OK) return rc;
+        GLU_CUDA(cudaMemcpyAsync(lu_out + b * h->nnz, h->d_v, sizeof(double) * h->nnz, cudaMemcpyDeviceToHost, s));
+    }
+    return batch_status(h, batch, fail_cols, s);
 }
 
 static int64_t launch_solve(glu_handle *h, const double *lu, double *x, bool upper, cudaStream_t s) {

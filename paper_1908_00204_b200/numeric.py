@@ -200,6 +200,29 @@ class Factorizer:
                         "glu_factor_host")
         return out, rc
 
+    def factor_batch_host(self, a_values: np.ndarray, thresh: float) -> tuple[np.ndarray, np.ndarray]:
+        """B value sets (rows, in the input pattern's CSC order) -> (LU values
+        [B, nnz], per-set status: -1 or the failing pivot column)."""
+        a = np.ascontiguousarray(a_values, dtype=np.float64)
+        if a.ndim != 2:
+            raise ValueError("a_values must be [batch, nz]")
+        out = np.empty((a.shape[0], self.nnz), dtype=np.float64)
+        fails = np.empty(a.shape[0], dtype=np.int64)
+        _lib.check(_lib.lib.glu_factor_batch_host(self._h, a.shape[0], _lib.ptr(a), _lib.ptr(out),
+                                                  float(thresh), _lib.ptr(fails)),
+                   "glu_factor_batch_host")
+        return out, fails
+
+    def factor_batch_device(self, v, thresh: float, stream=None) -> np.ndarray:
+        """In-place factorization of a [B, nnz] device tensor of A_s values;
+        returns the per-set status (-1 or the failing pivot column)."""
+        batch = int(v.shape[0])
+        fails = np.empty(max(batch, 1), dtype=np.int64)
+        _lib.check(_lib.lib.glu_factor_batch_device(self._h, batch, _dptr(v), float(thresh),
+                                                    _lib.ptr(fails), _stream(stream)),
+                   "glu_factor_batch_device")
+        return fails[:batch]
+
     def factor_device(self, v, thresh: float, stream=None) -> int:
         """In-place factorization of device A_s values (torch tensor or int pointer)."""
         return _lib.check(_lib.lib.glu_factor_device(self._h, _dptr(v), float(thresh),
@@ -419,6 +442,32 @@ def refactorize(lu: LuFactors, a_new: CscMatrix, schedule: LevelSchedule | None 
     vals, _ = _factor(a_new, lu.pattern, level_of, contract, opts.zero_pivot_threshold,
                       schedule is None)
     return LuFactors(lu.pattern, vals)
+
+
+def refactorize_batch(lu: LuFactors, a_pattern: CscMatrix, values: np.ndarray,
+                      schedule: LevelSchedule | None = None,
+                      opts: FactorOptions = FactorOptions()) -> tuple[np.ndarray, np.ndarray]:
+    """Refactor B value sets on lu's pattern in one call (the cfg5 batch:
+    Newton / transient steps).  Row b of `values` holds A's values in
+    a_pattern's CSC order (a_pattern.values is ignored).  Returns
+    (LU values [B, nnz], status [B]) where status[b] is -1 or the column at
+    which set b's pivot broke down (the PivotError the reference would
+    raise for that set, numeric.py:27-35)."""
+    _require_f64(a_pattern)
+    if a_pattern.n != lu.n:
+        raise PatternMismatchError("matrix and pattern sizes differ")
+    vals = np.ascontiguousarray(values, dtype=np.float64)
+    if vals.ndim != 2 or vals.shape[1] != len(a_pattern.row_idx):
+        raise ValueError("values must be [batch, nz(A)]")
+    level_of = schedule.level_of if schedule is not None else _relaxed_levels(lu.pattern)
+    contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
+    fz = get_factorizer(lu.pattern, level_of, contract)
+    with fz._lock:
+        fz.set_input(a_pattern.col_ptr, a_pattern.row_idx)
+        fz.set_option(2, 1 if schedule is None else 0)
+        fz.set_option(1, 0)
+        out, fails = fz.factor_batch_host(vals, opts.zero_pivot_threshold)
+    return out, fails
 
 
 def subcolumn_update(fp: FilledPattern, values: np.ndarray, source_j: int, dest_k: int):

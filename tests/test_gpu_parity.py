@@ -166,3 +166,48 @@ def test_device_api_matches_host_api(cfg2):
         fz.scatter_device(a_d, v_d)
         assert fz.factor_device(v_d, 1e-14) == -1
         assert np.array_equal(v_d.cpu().numpy(), host)
+
+
+def _cfg1_batch():
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a)
+    vals = np.stack([synthetic.perturb_values(a, 1000 + b) for b in range(5)])
+    vals[2] = 0.0  # singular set: pivot breakdown inside the batch
+    return a, fp, s, plans, vals
+
+
+@pytest.mark.parametrize("det", [True, False])
+def test_refactorize_batch_bitwise_per_set(det):
+    a, fp, s, plans, vals = _cfg1_batch()
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions(deterministic=det))
+    out, fails = glu.refactorize_batch(lu, a, vals, s, glu.FactorOptions(deterministic=det))
+    pat = orc.Pattern.from_fp(fp)
+    lp = np.concatenate([[0], np.cumsum([len(c) for c in s.levels])])
+    for b in range(len(vals)):
+        ref, bad = orc.scatter(pat, a.col_ptr, a.row_idx, vals[b])
+        rc = orc.factor_parallel(pat, ref, lp, np.concatenate(s.levels),
+                                 np.ones(len(lp) - 1, np.int64), det)
+        assert int(fails[b]) == rc
+        if rc == -1:
+            assert np.array_equal(out[b], ref)
+    assert fails[2] >= 0
+
+
+def test_batch_device_matches_single_calls():
+    import torch
+
+    a, fp, s, plans, vals = _cfg1_batch()
+    fz = glu.get_factorizer(fp, s.level_of, 1)
+    fz.set_input(a.col_ptr, a.row_idx)
+    dev = torch.device("cuda")
+    v = torch.empty((len(vals), fp.nnz), dtype=torch.float64, device=dev)
+    for b in range(len(vals)):
+        fz.scatter_device(torch.from_numpy(vals[b]).to(dev), v[b])
+    fails = fz.factor_batch_device(v, 1e-14)
+    for b in range(len(vals)):
+        single, rc = fz.factor_host(vals[b], 1e-14)
+        assert int(fails[b]) == rc
+        if rc == -1:
+            assert np.array_equal(v[b].cpu().numpy(), single)
