@@ -155,6 +155,11 @@ int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value);
    t_stored, 0} (%globaltimer ns) in the next factorization; read them
    with glu_trace_read (returns the record count). */
 int64_t glu_trace_read(glu_handle *h, int64_t *out, int64_t max_records);
+/* Diagnostics: glu_set_option(h, 8, n) records CUDA events (on the launch
+   stream) around the factor kernel and the dense-tail kernel of the next n
+   factorizations; after a synchronize, glu_kernel_times writes
+   {factor_kernel ms, tail_kernel ms} per launch and returns the count. */
+int64_t glu_kernel_times(glu_handle *h, double *ms, int64_t max_launches);
 /* Per-level milliseconds of the last timed factorization; returns count. */
 int64_t glu_level_times(const glu_handle *h, double *ms, int64_t len);
 /* info[0..11]: n, nnz, n_levels, n_items, n_chunks, macs, device bytes,

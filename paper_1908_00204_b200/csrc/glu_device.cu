@@ -1231,6 +1231,9 @@ struct glu_handle {
     double *tail_g = nullptr;
     unsigned long long *fail_batch = nullptr;
     i64 fail_batch_cap = 0;
+    // optional per-launch kernel timing: a ring of event triples
+    std::vector<cudaEvent_t> kev;
+    i64 kev_slots = 0, kev_next = 0;
     unsigned *sync = nullptr;   // done[n_levels*8] | err (+pad) | col_done[n]
     size_t sync_words = 0;
     Item *items = nullptr;
@@ -1449,6 +1452,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
+    for (cudaEvent_t e : h->kev) cudaEventDestroy(e);
     delete h;
 }
 
@@ -1485,6 +1489,15 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
         case 6:  // tuning: nanoseconds between dependency polls
             h->poll_ns = (int)std::max<int64_t>(0, std::min<int64_t>(value, 100000));
             return GLU_OK;
+        case 8: {  // diagnostics: record kernel times of the next `value` launches (ring)
+            for (cudaEvent_t e : h->kev) cudaEventDestroy(e);
+            h->kev.clear();
+            h->kev_slots = std::max<int64_t>(0, value);
+            h->kev_next = 0;
+            h->kev.resize(3 * h->kev_slots);
+            for (auto &e : h->kev) GLU_CUDA(cudaEventCreate(&e));
+            return GLU_OK;
+        }
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
             return GLU_OK;
@@ -1492,6 +1505,18 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             glu::set_error("unknown option");
             return GLU_EINVAL;
     }
+}
+
+extern "C" int64_t glu_kernel_times(glu_handle *h, double *ms, int64_t max_launches) {
+    const i64 m = std::min<i64>({max_launches, h->kev_slots, h->kev_next});
+    for (i64 k = 0; k < m; k++) {
+        float a = 0.f, b = 0.f;
+        GLU_CUDA(cudaEventElapsedTime(&a, h->kev[3 * k], h->kev[3 * k + 1]));
+        GLU_CUDA(cudaEventElapsedTime(&b, h->kev[3 * k + 1], h->kev[3 * k + 2]));
+        ms[2 * k] = a;
+        ms[2 * k + 1] = b;
+    }
+    return m;
 }
 
 extern "C" int64_t glu_trace_read(glu_handle *h, int64_t *out, int64_t max_records) {
@@ -1590,8 +1615,15 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     if (h->time_levels) {
         GLU_CUDA(cudaMemsetAsync(h->level_ns, 0, sizeof(unsigned long long) * (h->n_levels + 1), s));
     }
+    cudaEvent_t *ke = nullptr;
+    if (h->kev_slots > 0) {
+        ke = &h->kev[3 * (h->kev_next % h->kev_slots)];
+        h->kev_next++;
+        GLU_CUDA(cudaEventRecord(ke[0], s));
+    }
     GLU_CUDA(cudaLaunchCooperativeKernel((const void *)factor_kernel, dim3(h->grid), dim3(kThreads),
                                          args, kFactorDynSmem, s));
+    if (ke) GLU_CUDA(cudaEventRecord(ke[1], s));
     if (h->tail_t0 < h->n) {
         TailParams T;
         T.v = v;
@@ -1625,6 +1657,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         cfg.numAttrs = 1;
         GLU_CUDA(cudaLaunchKernelEx(&cfg, tail_kernel, T));
     }
+    if (ke) GLU_CUDA(cudaEventRecord(ke[2], s));
     return GLU_OK;
 }
 
