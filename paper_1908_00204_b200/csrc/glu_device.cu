@@ -789,7 +789,8 @@ struct TailParams {
     i32 t0, m, mpad, mw, b, np, ncl;
     i32 gstride;  // doubles per panel slot: b x mpad divided L values, then mpad u32 row words
                   // (bit k of row i: L(i, s0 + k) in the pattern)
-    double *G;    // 2 slots
+    double *G;    // one slot per panel
+    unsigned *ready;  // per panel: published (zeroed before each launch)
     double thresh;
     unsigned long long *fail;
     i32 fail_by_column;
@@ -839,6 +840,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     __shared__ int qtab[kTailMaxLocal];       // local column -> tail column (M: none)
     __shared__ double urow[2][kTailB];        // factor_panel: U(s, panel) broadcast
     __shared__ unsigned ubits[2];
+    // the cluster guarantees the C CTAs are co-resident (the panel flags rely on it)
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks(), c = (int)cl.block_rank();
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = nt >> 5;
@@ -886,7 +888,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     auto factor_panel = [&](int pp) {
         const int s0 = pp * B, s1 = min(s0 + B, M), bp = s1 - s0;
         const int xb0 = xloc(s0);  // the panel's columns are consecutive local columns
-        double *g = T.G + (size_t)(pp & 1) * T.gstride;
+        double *g = T.G + (size_t)pp * T.gstride;
         unsigned *grow = reinterpret_cast<unsigned *>(g + (size_t)B * T.mpad);
         double ra[kTailB], rb[kTailB];
         unsigned pa = 0, pb = 0;  // bit k: row ia / ib is in panel column s0+k
@@ -955,7 +957,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     // beyond the panel.
     auto apply_panel = [&](int p, int xa, int xb) {
         const int s0 = p * B, s1 = min(s0 + B, M), bp = s1 - s0;
-        const double *g = T.G + (size_t)(p & 1) * T.gstride;
+        const double *g = T.G + (size_t)p * T.gstride;
         const unsigned *grow = reinterpret_cast<const unsigned *>(g + (size_t)B * T.mpad);
         // the b x b triangle of divided L values among the panel rows (loads
         // are unconditional: entries outside the pattern are never used)
@@ -1022,22 +1024,49 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         __syncthreads();
     };
 
-    if (T.np > 0 && c == 0) factor_panel(0);
-    cl.sync();
+    // Panel p is published once (its own G slot) with a release flag; a CTA
+    // waits only for the flag of the panel it applies next -- no cluster-wide
+    // barrier, so nobody waits for another CTA's trailing updates.
+    auto publish = [&](int pp) {
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(T.ready + pp), "r"(1u) : "memory");
+        }
+    };
+    auto await = [&](int pp) {
+        if (tid == 0) {
+            unsigned f;
+            do {
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(T.ready + pp) : "memory");
+            } while (f == 0);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncthreads();
+    };
+    int x_last = ncol;  // last owned column: no panel beyond it concerns this CTA
+    while (x_last > 0 && qtab[x_last - 1] >= M) --x_last;
+    const int qmax = x_last > 0 ? qtab[x_last - 1] : -1;
+    if (T.np > 0 && c == 0) {
+        factor_panel(0);
+        publish(0);
+    }
     for (int p = 0; p < T.np; ++p) {
+        if (p * B > qmax) break;  // no owned column beyond this panel
+        await(p);
         const int pn = p + 1;
         const bool own_next = pn < T.np && (pn % C) == c;
         if (own_next) {  // lookahead: the next panel first
             const int xn = xloc(pn * B);
             apply_panel(p, xn, min(xn + B, ncol));
             factor_panel(pn);
+            publish(pn);
             const int xl = xn + B;
             apply_panel(p, 0, xn);
             apply_panel(p, xl, ncol);
         } else {
             apply_panel(p, 0, ncol);
         }
-        cl.sync();
     }
     for (int x = 0; x < ncol; ++x) {
         const int q = qglob(x);
@@ -1399,7 +1428,8 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
                 return fail(GLU_EINVAL);
             }
             const size_t gstride = (size_t)tail_gstride(h->tail);
-            if (cudaMalloc((void **)&h->tail_g, 2 * gstride * sizeof(double)) != cudaSuccess) {
+            if (cudaMalloc((void **)&h->tail_g, (size_t)h->tail.np * gstride * sizeof(double) +
+                                                    sizeof(unsigned) * (h->tail.np + 32)) != cudaSuccess) {
                 glu::set_error("cudaMalloc(tail buffer)");
                 return fail(GLU_ECUDA);
             }
@@ -1640,6 +1670,8 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         T.ncl = h->tail.ncl;
         T.gstride = tail_gstride(h->tail);
         T.G = h->tail_g;
+        T.ready = reinterpret_cast<unsigned *>(h->tail_g + (size_t)h->tail.np * T.gstride);
+        GLU_CUDA(cudaMemsetAsync(T.ready, 0, sizeof(unsigned) * h->tail.np, s));
         T.thresh = thresh;
         T.fail = fail;
         T.fail_by_column = h->fail_by_column ? 1 : 0;
