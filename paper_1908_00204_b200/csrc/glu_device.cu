@@ -858,6 +858,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     }
     __syncthreads();
     auto qglob = [&](int x) { return qtab[x]; };
+    int nvalid = ncol;  // owned columns that exist (the last panel may be short)
+    while (nvalid > 0 && qtab[nvalid - 1] >= M) --nvalid;
     for (int x = 0; x < ncol; ++x) {
         if (qglob(x) >= M) break;
         for (int i = tid; i < T.mpad; i += nt) cols[(size_t)x * T.mpad + i] = 0.0;
@@ -991,36 +993,70 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
             }
         }
         __syncthreads();
-        // (B) rows below the panel, target in a register across the b sources
-        for (int x = xa; x < xb; ++x) {
-            if (qglob(x) < s1) continue;
+        // (B) rows below the panel, target in a register across the b sources;
+        // two columns at a time so each thread carries independent chains
+        auto colB = [&](int x, double *u, unsigned &ub_out) {
+            double *cq = cols + (size_t)x * T.mpad;
+            ub_out = mbits(mk + x * T.mw, s0, bp);
+#pragma unroll
+            for (int k = 0; k < kTailB; ++k) u[k] = k < bp ? cq[s0 + k] : 0.0;
+        };
+        int x = xa;
+        xb = min(xb, nvalid);
+        while (x < xb && qglob(x) < s1) ++x;  // owned columns beyond the panel are contiguous
+        for (; x + 1 < xb; x += 2) {
+            double *c0 = cols + (size_t)x * T.mpad, *c1 = cols + (size_t)(x + 1) * T.mpad;
+            const unsigned u0 = mbits(mk + x * T.mw, s0, bp), u1 = mbits(mk + (x + 1) * T.mw, s0, bp);
+            const unsigned a0 = u0 & bitsa, a1 = u1 & bitsa, b0 = u0 & bitsb, b1 = u1 & bitsb;
+            if (a0 | a1) {
+                double t0 = c0[ia], t1 = c1[ia];
+#pragma unroll
+                for (int k = 0; k < kTailB; ++k) {
+                    const double r0 = __dsub_rn(t0, __dmul_rn(la[k], c0[s0 + k]));
+                    const double r1 = __dsub_rn(t1, __dmul_rn(la[k], c1[s0 + k]));
+                    t0 = ((a0 >> k) & 1u) ? r0 : t0;
+                    t1 = ((a1 >> k) & 1u) ? r1 : t1;
+                }
+                c0[ia] = t0;
+                c1[ia] = t1;
+            }
+            if (b0 | b1) {
+                double t0 = c0[ib], t1 = c1[ib];
+#pragma unroll
+                for (int k = 0; k < kTailB; ++k) {
+                    const double r0 = __dsub_rn(t0, __dmul_rn(lb[k], c0[s0 + k]));
+                    const double r1 = __dsub_rn(t1, __dmul_rn(lb[k], c1[s0 + k]));
+                    t0 = ((b0 >> k) & 1u) ? r0 : t0;
+                    t1 = ((b1 >> k) & 1u) ? r1 : t1;
+                }
+                c0[ib] = t0;
+                c1[ib] = t1;
+            }
+        }
+        for (; x < xb; ++x) {
             double *cq = cols + (size_t)x * T.mpad;
             const unsigned ub = mbits(mk + x * T.mw, s0, bp);
             const unsigned ua = ub & bitsa, ubb = ub & bitsb;
-            if (ua | ubb) {  // branch-free inner chain (selected subtractions)
-                double u[kTailB];
+            if (ua) {
+                double t = cq[ia];
 #pragma unroll
-                for (int k = 0; k < kTailB; ++k) u[k] = k < bp ? cq[s0 + k] : 0.0;
-                if (ua) {
-                    double t = cq[ia];
-#pragma unroll
-                    for (int k = 0; k < kTailB; ++k) {
-                        const double r = __dsub_rn(t, __dmul_rn(la[k], u[k]));
-                        t = ((ua >> k) & 1u) ? r : t;
-                    }
-                    cq[ia] = t;
+                for (int k = 0; k < kTailB; ++k) {
+                    const double r = __dsub_rn(t, __dmul_rn(la[k], cq[s0 + k]));
+                    t = ((ua >> k) & 1u) ? r : t;
                 }
-                if (ubb) {
-                    double t = cq[ib];
+                cq[ia] = t;
+            }
+            if (ubb) {
+                double t = cq[ib];
 #pragma unroll
-                    for (int k = 0; k < kTailB; ++k) {
-                        const double r = __dsub_rn(t, __dmul_rn(lb[k], u[k]));
-                        t = ((ubb >> k) & 1u) ? r : t;
-                    }
-                    cq[ib] = t;
+                for (int k = 0; k < kTailB; ++k) {
+                    const double r = __dsub_rn(t, __dmul_rn(lb[k], cq[s0 + k]));
+                    t = ((ubb >> k) & 1u) ? r : t;
                 }
+                cq[ib] = t;
             }
         }
+        (void)colB;
         __syncthreads();
     };
 
@@ -1044,9 +1080,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         }
         __syncthreads();
     };
-    int x_last = ncol;  // last owned column: no panel beyond it concerns this CTA
-    while (x_last > 0 && qtab[x_last - 1] >= M) --x_last;
-    const int qmax = x_last > 0 ? qtab[x_last - 1] : -1;
+    const int qmax = nvalid > 0 ? qtab[nvalid - 1] : -1;  // no panel beyond it concerns this CTA
     if (T.np > 0 && c == 0) {
         factor_panel(0);
         publish(0);
