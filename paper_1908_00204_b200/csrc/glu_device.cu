@@ -132,6 +132,8 @@ struct FactorParams {
     const i32 *level_need;  // items per phase
     i32 n;
     i32 n_items;
+    i32 n_express;          // items [0, n_express) are dealt to CTAs [0, express_R)
+    i32 express_R;
     i32 n_levels;
     i32 n_div;              // columns the final pass divides (the dense tail divides its own)
     double thresh;
@@ -704,6 +706,21 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     }
     __syncthreads();
     if (P.level_ns && blockIdx.x == 0 && threadIdx.x == 0) P.level_ns[0] = globaltimer();
+    // queue of this warp: the express items on the first express_R CTAs, the
+    // rest on the others; consecutive items on consecutive SMs in each
+    int q_lo = 0, q_hi = P.n_items, g0 = gw, qstride = nw;
+    if (P.express_R > 0) {
+        const int R = P.express_R, wslot = threadIdx.x >> 5;
+        if ((int)blockIdx.x < R) {
+            q_hi = P.n_express;
+            g0 = wslot * R + blockIdx.x;
+            qstride = R * kWarps;
+        } else {
+            q_lo = P.n_express;
+            g0 = q_lo + wslot * ((int)gridDim.x - R) + ((int)blockIdx.x - R);
+            qstride = ((int)gridDim.x - R) * kWarps;
+        }
+    }
     int cur = -1, coarse = 0, nq = 0;
     unsigned ran = 0;
     __shared__ WarpQ wqs[kWarps];
@@ -711,15 +728,15 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     WarpQ *wq = wqs + (threadIdx.x >> 5);
     int4 *ring = rings + (threadIdx.x >> 5) * kDeepRing * 32;
     int4 a = make_int4(0, 0, 0, 0), b = a, c = a;
-    if (gw < P.n_items) {
-        const int4 *ip = reinterpret_cast<const int4 *>(P.items + gw);
+    if (g0 < q_hi) {
+        const int4 *ip = reinterpret_cast<const int4 *>(P.items + g0);
         a = ldp(ip); b = ldp(ip + 1); c = ldp(ip + 2);
     }
-    for (int it = gw; it < P.n_items; it += nw) {
+    for (int it = g0; it < q_hi; it += qstride) {
         // next item's descriptor in flight while this one runs
-        const int nit = it + nw;
+        const int nit = it + qstride;
         int4 na = a, nb = b, nc = make_int4(0, -4, 0, 0);
-        if (nit < P.n_items) {
+        if (nit < q_hi) {
             const int4 *ip = reinterpret_cast<const int4 *>(P.items + nit);
             na = ldp(ip); nb = ldp(ip + 1); nc = ldp(ip + 2);
         }
@@ -1290,6 +1307,7 @@ struct glu_handle {
     i32 *level_need = nullptr;  // per phase: item count
     i32 *col_total = nullptr;   // per column: items into it
     i64 tail_t0 = 0;            // dense cluster tail: columns [tail_t0, n)
+    i64 n_express = 0, express_R = 0;
     TailShape tail;
     double *tail_g = nullptr;
     unsigned long long *fail_batch = nullptr;
@@ -1453,6 +1471,8 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         h->sync_words = (size_t)std::max<i64>(pv.n_levels, 1) * 8 + kLineWords + (size_t)std::max<i64>(n, 1) * kColRep;
         UP(h->col_total, std::vector<i32>(pv.col_total, pv.col_total + n));
         h->tail_t0 = pv.tail_t0;
+        h->n_express = pv.n_express;
+        h->express_R = pv.express_R;
         const i64 m = n - pv.tail_t0;
         if (m > 0) {
             h->tail = pick_tail((int)m, nullptr);
@@ -1654,6 +1674,8 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.level_need = h->level_need;
     P.n = (i32)h->n;
     P.n_items = (i32)h->n_items;
+    P.n_express = (i32)h->n_express;
+    P.express_R = (i32)std::min<i64>(h->express_R, h->grid - 1);
     P.n_levels = (i32)h->n_levels;
     P.n_div = (i32)h->tail_t0;
     P.thresh = thresh;

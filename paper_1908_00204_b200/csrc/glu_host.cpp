@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -497,6 +498,7 @@ struct glu_plan {
     std::vector<uint16_t> tgt16;
     std::vector<i32> col_total;
     i64 tail_t0 = 0, tail_macs = 0;
+    i64 n_express = 0, express_R = 0;  // express queue: items [0, n_express) on the first express_R SMs
     i64 max_item_macs = 0;
     i64 max_chunks = 0;
     i64 deferred = 0;
@@ -759,7 +761,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     // descending (the longest items go first in the static warp round-robin;
     // a deep item's serial chain costs ~8x a push item's MAC), then column,
     // then base.
-    struct Ref { i32 lvl; i32 crit; i32 tid; i64 idx; i64 cost; };
+    struct Ref { i32 lvl; i32 crit; i32 tid; i64 idx; i64 cost; i32 need; };
     std::vector<Ref> refs;
     size_t total_items = 0, total_map = 0, total_tgt = 0, total_chunks = 0, total_deep = 0;
     for (auto &o : outs) {
@@ -779,7 +781,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
             const LocalItem &x = outs[t].items[i];
             // critical: the destination is a source column of the next phase
             const i32 crit = level_of[x.k] == x.lvl + 1 ? 1 : 0;
-            refs.push_back({x.lvl, crit, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs});
+            refs.push_back({x.lvl, crit, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs, 0});
         }
     // inside a phase: deep chains first (the longest serial work), then the
     // items the next phase waits for, then by cost
@@ -794,32 +796,64 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         if (x.k != y.k) return x.k < y.k;
         return x.base < y.base;
     });
+    // dataflow dependencies (on the phase-sorted order): per item, the items
+    // into its column in earlier phases; per column, the items into it overall
+    std::vector<i32> cnt_k(n, 0), pend_k(n, 0), last_k(n, -1);
+    for (auto &r : refs) {
+        const LocalItem &x = outs[r.tid].items[r.idx];
+        if (last_k[x.k] != x.lvl) {
+            cnt_k[x.k] += pend_k[x.k];
+            pend_k[x.k] = 0;
+            last_k[x.k] = x.lvl;
+        }
+        r.need = cnt_k[x.k];
+        pend_k[x.k]++;
+    }
+    // Express queue: in thin phases, the items into columns that are sources
+    // within the next K phases (the critical chain and the items one or two
+    // hops behind it) go to a separate list that the kernel deals to a few
+    // reserved SMs.  A release fence waits behind every memory request its SM
+    // has in flight, so the critical chain fences on quiet SMs while the bulk
+    // of each phase runs on the others.
+    i64 express_R = 0, express_K = 3, express_max = 3000;  // off unless GLU_EXPRESS_R is set
+    if (const char *e = std::getenv("GLU_EXPRESS_R")) express_R = std::atoll(e);
+    if (const char *e = std::getenv("GLU_EXPRESS_K")) express_K = std::atoll(e);
+    if (const char *e = std::getenv("GLU_EXPRESS_MAX")) express_max = std::atoll(e);
+    i64 n_express = 0;
+    if (express_R > 0) {
+        std::vector<i64> per_phase(n_levels, 0);
+        for (auto &r : refs) per_phase[r.lvl]++;
+        auto is_express = [&](const Ref &r) {
+            const LocalItem &x = outs[r.tid].items[r.idx];
+            return x.kind == glu::kPush && per_phase[x.lvl] <= express_max &&
+                   level_of[x.k] - x.lvl <= express_K;
+        };
+        std::stable_partition(refs.begin(), refs.end(), is_express);
+        for (auto &r : refs) {
+            if (!is_express(r)) break;
+            n_express++;
+        }
+        if (n_express == 0) express_R = 0;
+    }
     auto *plan = new glu_plan();
     plan->n_levels = n_levels;
     plan->tail_t0 = t0;
     plan->tail_macs = tail_macs;
+    plan->n_express = n_express;
+    plan->express_R = express_R;
     plan->level_item_ptr.assign(n_levels + 1, 0);
     plan->items.reserve(refs.size());
     plan->chunks.reserve(total_chunks);
     plan->map8.reserve(total_map);
     plan->tgt16.reserve(total_tgt);
     plan->deep.reserve(total_deep);
-    // dataflow dependencies: per item, the items into its column in earlier
-    // phases; per column, the items into it overall
-    std::vector<i32> cnt_k(n, 0), pend_k(n, 0), last_k(n, -1);
     for (auto &r : refs) {
         const ThreadOut &o = outs[r.tid];
         const LocalItem &x = o.items[r.idx];
         plan->level_item_ptr[x.lvl + 1]++;
         glu::Item it{};
-        if (last_k[x.k] != x.lvl) {
-            cnt_k[x.k] += pend_k[x.k];
-            pend_k[x.k] = 0;
-            last_k[x.k] = x.lvl;
-        }
         it.col = x.k;
-        it.need = cnt_k[x.k];
-        pend_k[x.k]++;
+        it.need = r.need;
         it.base = (i32)x.base;
         it.macs = (i32)x.macs;
         // phase in the upper bits (dataflow waits); bit 1: critical (signal at once)
@@ -874,16 +908,23 @@ extern "C" void glu_plan_info(const glu_plan *p, int64_t *info) {
     info[12] = (i64)p->tgt16.size();
     info[13] = p->tail_t0;
     info[14] = p->tail_macs;
-    info[15] = 0;
+    info[15] = p->n_express;
 }
 
 extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
                                 int64_t *chunks, int64_t *deep, uint8_t *map8, int64_t *tgt) {
     if (level_item_ptr)
         std::memcpy(level_item_ptr, p->level_item_ptr.data(), p->level_item_ptr.size() * sizeof(i64));
+    // items in phase order (the express queue sits in front of the device
+    // array); level_item_ptr indexes this order
+    std::vector<i64> order(p->items.size());
+    for (size_t i = 0; i < order.size(); i++) order[i] = (i64)i;
+    std::stable_sort(order.begin(), order.end(), [&](i64 x, i64 y) {
+        return (p->items[x].kind >> 2) < (p->items[y].kind >> 2);
+    });
     if (items)
         for (size_t i = 0; i < p->items.size(); i++) {
-            const glu::Item &it = p->items[i];
+            const glu::Item &it = p->items[order[i]];
             i64 *o = items + 8 * i;
             o[0] = it.map_off; o[1] = it.tgt_off; o[2] = it.base; o[3] = it.c0; o[4] = it.nch;
             o[5] = it.ntgt; o[6] = it.macs; o[7] = it.kind & 1;
@@ -925,6 +966,8 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.n_tgt = (i64)p->tgt16.size();
     v.col_total = p->col_total.data();
     v.tail_t0 = p->tail_t0;
+    v.n_express = p->n_express;
+    v.express_R = p->express_R;
     return v;
 }
 }  // namespace glu

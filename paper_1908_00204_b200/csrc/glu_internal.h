@@ -71,6 +71,8 @@ struct glu_plan_view {
     int64_t n_tgt;
     const int32_t *col_total;  // per column: items into it (all phases)
     int64_t tail_t0;           // columns >= tail_t0: dense cluster tail (n: none)
+    int64_t n_express;         // items [0, n_express): express queue
+    int64_t express_R;         // SMs reserved for the express queue
 };
 
 const glu_plan_view plan_view(const glu_plan *p);

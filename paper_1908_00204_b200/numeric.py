@@ -149,7 +149,7 @@ class Factorizer:
             self.plan_info = dict(zip(("levels", "items", "chunks", "macs", "max_item_macs",
                                        "max_chunks", "deferred_macs", "plan_bytes", "deep_items",
                                        "deep_macs", "epochs", "push_macs", "targets", "tail_t0",
-                                       "tail_macs"),
+                                       "tail_macs", "express_items"),
                                       info.tolist()))
             h = ctypes.c_void_p()
             rc = _lib.check(_lib.lib.glu_create(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
