@@ -136,8 +136,10 @@ struct FactorParams {
     i32 express_R;
     i32 n_levels;
     i32 n_div;              // columns the final pass divides (the dense tail divides its own)
+    i32 nb;                 // value sets factored by this launch (batch-major, set_stride apart)
+    long long set_stride;
     double thresh;
-    unsigned long long *fail;  // min (level << 32 | column) of failing pivots
+    unsigned long long *fail;  // per value set: min (level << 32 | column) of failing pivots
     unsigned *done;            // per phase: completed items (stride 8 words)
     unsigned *col_done;        // per column: completed items into it
     const i32 *col_total;      // per column: items into it
@@ -500,20 +502,24 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
         return false;
     stamp(rec, 4, lane);
     prefetch_item(P, na, nb, nc, lane);
+    // value phase, once per value set of the launch (batch: the static part,
+    // the dependency wait and the release are shared by all sets)
+    for (int bs = 0; bs < P.nb; ++bs) {
+    double *V = P.v + (size_t)bs * P.set_stride;
     // one round of independent loads
     double piv = 1.0, mult = 0.0;
     if (lane < nch) {
-        piv = ldv(P.v + dslot);
-        mult = ldv(P.v + ch.x);
+        piv = ldv(V + dslot);
+        mult = ldv(V + ch.x);
     }
     double t[kR], l[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
-        if (to[r] >= 0) t[r] = ldv(P.v + base + to[r]);
+        if (to[r] >= 0) t[r] = ldv(V + base + to[r]);
         if (r < nr) {
             const int cp0 = __shfl_sync(0xffffffffu, ch.z, ci[r]);
             const int cest = __shfl_sync(0xffffffffu, est, ci[r]);
-            if (u[r] >= 0) l[r] = ldv(P.v + cp0 + (32 * r + lane - cest));
+            if (u[r] >= 0) l[r] = ldv(V + cp0 + (32 * r + lane - cest));
         }
     }
 #pragma unroll
@@ -530,7 +536,7 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
         }
     }
     __syncwarp();
-    stamp(rec, 5, lane);
+    if (bs == 0) stamp(rec, 5, lane);
     const int nep = __popc(epm);
     if (nep == 1) {
 #pragma unroll
@@ -547,7 +553,9 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < kR; ++r)
-        if (to[r] >= 0) stv(P.v + base + to[r], sg[32 * r + lane]);
+        if (to[r] >= 0) stv(V + base + to[r], sg[32 * r + lane]);
+    __syncwarp();
+    }
     __syncwarp();
     stamp(rec, 6, lane);
     return true;
@@ -583,25 +591,32 @@ __device__ __forceinline__ bool run_deep(const FactorParams &P, int4 a, int4 b, 
     const int macs = c_.x;
     const int ng = (macs + 31) >> 5;
     const int4 *dr = reinterpret_cast<const int4 *>(P.deep) + off;
-    double *tp = P.v + b.x;
+    auto issue_ring = [&]() {
 #pragma unroll
-    for (int g = 0; g < kDeepRing; ++g) {
-        cp_async16(ring + g * 32 + lane, dr + min(32 * g + lane, macs - 1), 32 * g + lane < macs);
-        cp_async_commit();
-    }
+        for (int g = 0; g < kDeepRing; ++g) {
+            cp_async16(ring + g * 32 + lane, dr + min(32 * g + lane, macs - 1), 32 * g + lane < macs);
+            cp_async_commit();
+        }
+    };
+    issue_ring();
     if (wait_l >= 0 && !wait_phase(P, wait_l, lane, cs)) {
         cp_async_wait<0>();
         return false;
     }
     stamp(rec, 3, lane);
     prefetch_item(P, na, nb, nc, lane);
+    // once per value set of the launch (the refs stream again for each)
+    for (int bs = 0; bs < P.nb; ++bs) {
+    if (bs > 0) issue_ring();
+    double *V = P.v + (size_t)bs * P.set_stride;
+    double *tp = V + b.x;
     double acc = ldv(tp);
     // operand sets for groups g % 3 (values loaded three groups ahead)
     double l0 = 0.0, d0 = 1.0, m0 = 0.0, l1 = 0.0, d1 = 1.0, m1 = 0.0, l2 = 0.0, d2 = 1.0, m2 = 0.0;
     auto load_group = [&](int grp, double &l, double &d, double &m) {
         if (32 * grp + lane < macs) {
             const int4 r = ring[(grp % kDeepRing) * 32 + lane];
-            l = ldv(P.v + r.x); d = ldv(P.v + r.y); m = ldv(P.v + r.z);
+            l = ldv(V + r.x); d = ldv(V + r.y); m = ldv(V + r.z);
         }
     };
     auto refill = [&](int grp) {  // slot of group grp was just consumed: fetch group grp + kDeepRing
@@ -653,6 +668,8 @@ __device__ __forceinline__ bool run_deep(const FactorParams &P, int4 a, int4 b, 
     }
     cp_async_wait<0>();
     if (lane == 0) stv(tp, acc);
+    __syncwarp();
+    }
     stamp(rec, 6, lane);
     if (rec && lane == 0) rec[7] = ng;
     return true;
@@ -661,7 +678,10 @@ __device__ __forceinline__ bool run_deep(const FactorParams &P, int4 a, int4 b, 
 // Pivot check + divide of column j (_kernels.py:152-173): cmax over the
 // whole column with the reference's `av > cmax` rule (NaN never wins),
 // failure if |piv| <= thresh * cmax, else L(:,j) /= piv.
-__device__ __forceinline__ void divide_column(const FactorParams &P, int j, int lane) {
+__device__ __forceinline__ void divide_column(const FactorParams &Pin, int j, int lane, int bs) {
+    FactorParams P = Pin;  // value set bs
+    P.v = Pin.v + (size_t)bs * Pin.set_stride;
+    P.fail = Pin.fail + bs;
     const int lo = __ldg(P.col_ptr + j), hi = __ldg(P.col_ptr + j + 1);
     const int d = __ldg(P.diag_pos + j);
     double cmax = 0.0;
@@ -771,7 +791,8 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     }
     // every phase complete -> pivot check + divide of every column
     if (P.n_levels > 0 && !wait_phase(P, P.n_levels - 1, lane, &cs)) return;
-    for (int j = gw; j < P.n_div; j += nw) divide_column(P, j, lane);
+    for (int bs = 0; bs < P.nb; ++bs)
+        for (int j = gw; j < P.n_div; j += nw) divide_column(P, j, lane, bs);
 }
 
 // ---------------------------------------------------------------------------
@@ -1344,6 +1365,7 @@ struct glu_handle {
     std::vector<double> last_level_ms;
     // host-API staging
     double *d_a = nullptr, *d_v = nullptr, *d_x = nullptr;
+    double *d_ab = nullptr, *d_vb = nullptr;  // batched host-API staging
     cudaStream_t stream = nullptr;
 };
 
@@ -1532,7 +1554,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x};
+                    h->bar, h->ifail, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -1657,9 +1679,13 @@ extern "C" int64_t glu_scatter_device(glu_handle *h, const double *a_vals, doubl
 }
 
 static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream_t s,
-                             unsigned long long *fail = nullptr) {
+                             unsigned long long *fail = nullptr, int nb = 1) {
     if (!fail) fail = h->fail;
-    GLU_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s));
+    if (nb > 1 && h->tail_t0 < h->n) {
+        glu::set_error("batched launch needs a plan without a dense tail");
+        return GLU_EINVAL;
+    }
+    GLU_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long) * nb, s));
     GLU_CUDA(cudaMemsetAsync(h->sync, 0, h->sync_words * sizeof(unsigned), s));
     FactorParams P;
     P.v = v;
@@ -1678,6 +1704,8 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.express_R = (i32)std::min<i64>(h->express_R, h->grid - 1);
     P.n_levels = (i32)h->n_levels;
     P.n_div = (i32)h->tail_t0;
+    P.nb = nb;
+    P.set_stride = h->nnz;
     P.thresh = thresh;
     P.fail = fail;
     const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
@@ -1798,6 +1826,8 @@ static int64_t ensure_staging(glu_handle *h);
 // batch-major (set b at v + b * nnz); every set is factored in stream order
 // by the same resident plan, each with its own failure slot, and the
 // statuses are read back once for the whole batch.
+constexpr int kMaxBatchPerLaunch = 8;
+
 static int64_t ensure_batch(glu_handle *h, int64_t batch) {
     if (batch <= h->fail_batch_cap) return GLU_OK;
     if (h->fail_batch) cudaFree(h->fail_batch);
@@ -1830,8 +1860,15 @@ extern "C" int64_t glu_factor_batch_device(glu_handle *h, int64_t batch, double 
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = ensure_batch(h, std::max<int64_t>(batch, 1));
     if (rc != GLU_OK) return rc;
-    for (int64_t b = 0; b < batch; b++)
-        if ((rc = launch_factor(h, v + b * h->nnz, thresh, s, h->fail_batch + b)) != GLU_OK) return rc;
+    if (h->tail_t0 < h->n) {  // plan with a dense tail: one launch pair per set
+        for (int64_t b = 0; b < batch; b++)
+            if ((rc = launch_factor(h, v + b * h->nnz, thresh, s, h->fail_batch + b)) != GLU_OK) return rc;
+    } else {  // sets share each item's static loads, dependency wait and release
+        for (int64_t b0 = 0; b0 < batch; b0 += kMaxBatchPerLaunch) {
+            const int nb = (int)std::min<int64_t>(kMaxBatchPerLaunch, batch - b0);
+            if ((rc = launch_factor(h, v + b0 * h->nnz, thresh, s, h->fail_batch + b0, nb)) != GLU_OK) return rc;
+        }
+    }
     return batch_status(h, batch, fail_cols, s);
 }
 
@@ -1846,12 +1883,23 @@ extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const dou
     if (rc != GLU_OK) return rc;
     if ((rc = ensure_batch(h, std::max<int64_t>(batch, 1))) != GLU_OK) return rc;
     cudaStream_t s = h->stream;
-    // one set in flight on the device staging buffers; copies are stream-ordered
-    for (int64_t b = 0; b < batch; b++) {
-        GLU_CUDA(cudaMemcpyAsync(h->d_a, a_vals + b * h->nz, sizeof(double) * h->nz, cudaMemcpyHostToDevice, s));
-        if ((rc = glu_scatter_device(h, h->d_a, h->d_v, s)) != GLU_OK) return rc;
-        if ((rc = launch_factor(h, h->d_v, thresh, s, h->fail_batch + b)) != GLU_OK) return rc;
-        GLU_CUDA(cudaMemcpyAsync(lu_out + b * h->nnz, h->d_v, sizeof(double) * h->nnz, cudaMemcpyDeviceToHost, s));
+    const bool batched = h->tail_t0 >= h->n;  // tail-less plan: sets share a launch
+    const int chunk = batched ? kMaxBatchPerLaunch : 1;
+    if (batched && !h->d_vb) {
+        GLU_CUDA(cudaMalloc((void **)&h->d_vb, sizeof(double) * h->nnz * chunk));
+        GLU_CUDA(cudaMalloc((void **)&h->d_ab, sizeof(double) * std::max<i64>(h->nz, 1) * chunk));
+    }
+    double *dv = batched ? h->d_vb : h->d_v, *da = batched ? h->d_ab : h->d_a;
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int nb = (int)std::min<int64_t>(chunk, batch - b0);
+        GLU_CUDA(cudaMemcpyAsync(da, a_vals + b0 * h->nz, sizeof(double) * h->nz * nb,
+                                 cudaMemcpyHostToDevice, s));
+        for (int k = 0; k < nb; k++)
+            if ((rc = glu_scatter_device(h, da + (size_t)k * h->nz, dv + (size_t)k * h->nnz, s)) != GLU_OK)
+                return rc;
+        if ((rc = launch_factor(h, dv, thresh, s, h->fail_batch + b0, nb)) != GLU_OK) return rc;
+        GLU_CUDA(cudaMemcpyAsync(lu_out + b0 * h->nnz, dv, sizeof(double) * h->nnz * nb,
+                                 cudaMemcpyDeviceToHost, s));
     }
     return batch_status(h, batch, fail_cols, s);
 }

@@ -302,14 +302,17 @@ def _digest(a: np.ndarray) -> bytes:
     return hashlib.sha1(np.ascontiguousarray(a, dtype=np.int64).tobytes()).digest()
 
 
-def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int) -> Factorizer:
-    """Cached Factorizer for (fp, schedule, contract); dropped with fp."""
-    key = (id(fp), contract, _digest(level_of))
+def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int,
+                   tail: bool = True) -> Factorizer:
+    """Cached Factorizer for (fp, schedule, contract); dropped with fp.
+    tail=False builds the plan without the dense cluster tail, which lets a
+    launch factor several value sets at once (batch refactorization)."""
+    key = (id(fp), contract, _digest(level_of), tail)
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
         if hit is not None and hit[0]() is fp:
             return hit[1]
-        fz = Factorizer(fp, level_of, contract)
+        fz = Factorizer(fp, level_of, contract, tail_max=None if tail else 0)
 
         def _drop(_ref, key=key):
             with _CACHE_LOCK:
@@ -461,7 +464,7 @@ def refactorize_batch(lu: LuFactors, a_pattern: CscMatrix, values: np.ndarray,
         raise ValueError("values must be [batch, nz(A)]")
     level_of = schedule.level_of if schedule is not None else _relaxed_levels(lu.pattern)
     contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
-    fz = get_factorizer(lu.pattern, level_of, contract)
+    fz = get_factorizer(lu.pattern, level_of, contract, tail=False)
     with fz._lock:
         fz.set_input(a_pattern.col_ptr, a_pattern.row_idx)
         fz.set_option(2, 1 if schedule is None else 0)

@@ -195,19 +195,38 @@ def test_refactorize_batch_bitwise_per_set(det):
     assert fails[2] >= 0
 
 
-def test_batch_device_matches_single_calls():
+@pytest.mark.parametrize("tail", [True, False])
+def test_batch_device_matches_single_calls(tail):
     import torch
 
     a, fp, s, plans, vals = _cfg1_batch()
-    fz = glu.get_factorizer(fp, s.level_of, 1)
+    fz = glu.get_factorizer(fp, s.level_of, 1, tail=tail)
     fz.set_input(a.col_ptr, a.row_idx)
     dev = torch.device("cuda")
     v = torch.empty((len(vals), fp.nnz), dtype=torch.float64, device=dev)
     for b in range(len(vals)):
         fz.scatter_device(torch.from_numpy(vals[b]).to(dev), v[b])
     fails = fz.factor_batch_device(v, 1e-14)
+    ref = glu.get_factorizer(fp, s.level_of, 1)
+    ref.set_input(a.col_ptr, a.row_idx)
     for b in range(len(vals)):
-        single, rc = fz.factor_host(vals[b], 1e-14)
+        single, rc = ref.factor_host(vals[b], 1e-14)
         assert int(fails[b]) == rc
         if rc == -1:
             assert np.array_equal(v[b].cpu().numpy(), single)
+
+
+def test_cfg2_batched_launch_bitwise():
+    """Eight value sets in one tail-less launch == eight single factorizations."""
+    import torch
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make("cfg2")
+    fp, s, plans = _analyze(a, glu.B200_RESOURCE)
+    vals = np.stack([synthetic.perturb_values(a, 2000 + b) for b in range(8)])
+    out, fails = glu.refactorize_batch(glu.LuFactors(fp, np.zeros(fp.nnz)), a, vals, s,
+                                       glu.FactorOptions(deterministic=False))
+    assert np.all(fails == -1)
+    for b in (0, 5, 7):
+        assert np.array_equal(out[b], _oracle_values(glu.CscMatrix(a.n, a.col_ptr, a.row_idx, vals[b]),
+                                                     fp, s, False))
