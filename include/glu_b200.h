@@ -105,7 +105,7 @@ int64_t glu_find_hazards(int64_t n, const int64_t *col_ptr, const int64_t *row_i
    numeric.py:295-315).  contract: GLU_CONTRACT_A or GLU_CONTRACT_B.
    max_item_macs caps the MACs one push item carries (0 = adaptive per
    phase, 32..128); deep_min is the MAC count from which a target becomes
-   its own register-chained item (0 = default 8).  tail_max: the trailing
+   its own register-chained item (0 = default 32).  tail_max: the trailing
    columns that are each alone in the last phases (a near-dense separator
    block) go to the thread-block-cluster tail kernel, up to tail_max of them
    (0 = no tail; glu_tail_capacity() gives the device's limit).  Returns

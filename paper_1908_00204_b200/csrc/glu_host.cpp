@@ -541,7 +541,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         set_error("pattern has >= 2^31 entries; slot indices are int32 on the device");
         return GLU_EINVAL;
     }
-    const i64 D = deep_min > 0 ? deep_min : 8;
+    const i64 D = deep_min > 0 ? deep_min : 32;  // measured on cfg2: 8 -> 6.69 ms, 32 -> 6.58 ms
     i64 n_levels = 0;
     for (i64 j = 0; j < n; j++) n_levels = std::max(n_levels, level_of[j] + 1);
     const i64 t0 = find_tail(n, level_of, n_levels, tail_max);

@@ -14,6 +14,10 @@ timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_$
 cat gpurun_out/bench_${TAG}.json | cut -c1-400
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_${TAG}.json 2>&1; echo "ref rc=$?"
 cut -c1-300 gpurun_out/bench_ref_${TAG}.json
+timeout 600 python bench.py --batch 8 --steps 5 --warmup 3 > gpurun_out/bench_batch8_${TAG}.json 2> gpurun_out/bench_batch8_${TAG}.err; echo "batch rc=$?"
+cut -c1-300 gpurun_out/bench_batch8_${TAG}.json
+timeout 900 python bench.py --config cfg3 --steps 10 --warmup 3 > gpurun_out/bench_cfg3_${TAG}.json 2> gpurun_out/bench_cfg3_${TAG}.err; echo "cfg3 rc=$?"
+cut -c1-300 gpurun_out/bench_cfg3_${TAG}.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${TAG}.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "launch rc=$?"
