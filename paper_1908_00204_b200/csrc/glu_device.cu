@@ -132,6 +132,7 @@ struct FactorParams {
     unsigned *done;            // per phase: completed items (stride 8 words)
     unsigned *col_done;        // per column: completed items into it
     const i32 *col_total;      // per column: items into it
+    const glu::ColDep *cdeps;  // per item: destination columns + earlier-phase counts
     int *err;                  // watchdog flag
     unsigned long long *level_ns;  // optional per-phase completion timestamps
     unsigned long long *trace;     // optional per-item timestamps (diagnostics)
@@ -240,6 +241,7 @@ __device__ __forceinline__ bool wait_phase(const FactorParams &P, int w, int lan
 // queue in shared memory and are released together when the warp leaves the
 // phase (or the queue is full) -- never later than the phase counter, so the
 // dependency order and the deadlock-freedom argument are unchanged.
+constexpr int kMaxCols = 4;  // destination columns per item (glu_host.cpp kMaxItemCols)
 struct WarpQ {
     int col[32];
 };
@@ -263,18 +265,20 @@ __device__ __forceinline__ void flush_items(const FactorParams &P, WarpQ *q, int
     __syncwarp();
 }
 
-__device__ __forceinline__ void finish_item(const FactorParams &P, WarpQ *q, int &nq, int col,
-                                            bool crit, int lvl, unsigned ran, bool phase_end,
-                                            int lane) {
+__device__ __forceinline__ void finish_item(const FactorParams &P, WarpQ *q, int &nq, int mycol,
+                                            int ncol, bool crit, int lvl, unsigned ran,
+                                            bool phase_end, int lane) {
+    // lanes < ncol hold the item's destination columns in mycol
     if (crit) {
+        const int cc = __shfl_sync(0xffffffffu, mycol, (lane / kColRep) & 31);
         __syncwarp();
         fence_acq_rel_gpu();
-        if (lane < kColRep) red_add_relaxed(P.col_done + (size_t)col * kColRep + lane, 1);
+        if (lane < ncol * kColRep) red_add_relaxed(P.col_done + (size_t)cc * kColRep + (lane % kColRep), 1);
     } else {
-        if (lane == 0) q->col[nq] = col;
-        ++nq;
+        if (lane < ncol) q->col[nq + lane] = mycol;
+        nq += ncol;
     }
-    if (phase_end || nq == 32) flush_items(P, q, nq, lvl, ran, phase_end, lane);
+    if (phase_end || nq + kMaxCols > 32) flush_items(P, q, nq, lvl, ran, phase_end, lane);
 }
 
 // Fine-grained wait of a push item in phase lvl: its source columns complete
@@ -291,24 +295,33 @@ __device__ __forceinline__ void finish_item(const FactorParams &P, WarpQ *q, int
 // enough: the values are read .cg from L2 after the wait, and the producer
 // fenced its stores before counting.
 __device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool has_src, int j,
-                                          unsigned jneed, int k, unsigned kneed, int lvl,
-                                          CtaSync *cs, int rep) {
+                                          unsigned jneed, bool has_own, int k, unsigned kneed,
+                                          int lvl, CtaSync *cs, int rep) {
     const int w = threadIdx.x >> 5;
     volatile int *vready = cs->ready;
     volatile unsigned *vk = &cs->known;
-    // distinct requests: the own column (lane 0) and every distinct source column
+    // distinct requests: the own columns (lanes < ncol, distinct by
+    // construction) and every distinct source column
     const unsigned same = __match_any_sync(0xffffffffu, has_src ? j : -1 - lane);
     const bool src_lead = has_src && (__ffs(same) - 1) == lane;
-    const bool post_k = lane == 0;
+    const unsigned om = __ballot_sync(0xffffffffu, has_own);
     const unsigned pm = __ballot_sync(0xffffffffu, src_lead);
-    const int nsrc = __popc(pm);
+    const int nown = __popc(om), nsrc = __popc(pm);
     unsigned long long t0 = 0;
-    if (nsrc + 1 <= kReq) {
-        const int slot = src_lead ? 1 + __popc(pm & ((1u << lane) - 1u)) : -1;
-        if (post_k) { cs->req_col[w * kReq] = k; cs->req_need[w * kReq] = kneed; }
-        if (slot > 0) { cs->req_col[w * kReq + slot] = j; cs->req_need[w * kReq + slot] = jneed; }
+    if (nown + nsrc <= kReq) {
+        if (has_own) {
+            const int slot = __popc(om & ((1u << lane) - 1u));
+            cs->req_col[w * kReq + slot] = k;
+            cs->req_need[w * kReq + slot] = kneed;
+        }
+        if (src_lead) {
+            const int slot = nown + __popc(pm & ((1u << lane) - 1u));
+            cs->req_col[w * kReq + slot] = j;
+            cs->req_need[w * kReq + slot] = jneed;
+        }
         if (lane == 0)
-            for (int x = nsrc + 1; x < kReq; ++x) cs->req_col[w * kReq + x] = -1;
+            for (int x = nown + nsrc; x < kReq; ++x) cs->req_col[w * kReq + x] = -1;
+        __syncwarp();
         if (lane == 0) { cs->ready[w] = 0; __threadfence_block(); cs->pending[w] = 1; }
         __syncwarp();
         // only the service round clears a posted request (no other exit), so a
@@ -362,18 +375,18 @@ __device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool 
         __syncwarp();
         return true;
     }
-    // many distinct sources (wide phases): poll directly
+    // many distinct requests (wide phases): poll directly
     for (int spin = 0;; ++spin) {
         __nanosleep(P.poll_ns);
         if (*vk >= (unsigned)lvl) break;
         unsigned rem = 0;
         if (has_src) {
-            const unsigned c = ld_relaxed(P.col_done + (size_t)j * kColRep + rep);
-            rem = c >= jneed ? 0u : jneed - c;
+            const unsigned cc = ld_relaxed(P.col_done + (size_t)j * kColRep + rep);
+            rem = cc >= jneed ? 0u : jneed - cc;
         }
-        if (lane == 0) {
-            const unsigned c = ld_relaxed(P.col_done + (size_t)k * kColRep + rep);
-            rem = max(rem, c >= kneed ? 0u : kneed - c);
+        if (has_own) {
+            const unsigned cc = ld_relaxed(P.col_done + (size_t)k * kColRep + rep);
+            rem = max(rem, cc >= kneed ? 0u : kneed - cc);
         }
         const unsigned mx = __reduce_max_sync(0xffffffffu, rem);
         if (mx == 0) break;
@@ -438,18 +451,27 @@ __device__ __forceinline__ void stamp(unsigned long long *rec, int k, int lane) 
 
 __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, int4 c, int lane,
                                          CtaSync *cs, double *sg, unsigned long long *rec, int4 na,
-                                         int4 nb, int4 nc) {
+                                         int4 nb, int4 nc, int *mycol) {
     const i64 moff = (i64)(unsigned)a.x | ((i64)a.y << 32);
     const i64 toff = (i64)(unsigned)a.z | ((i64)a.w << 32);
     const int base = b.x, c0 = b.y, nch = b.z, ntgt = b.w, macs = c.x;
     const int lvl = c.y >> 2;
     const bool check = *(volatile unsigned *)&cs->known < (unsigned)lvl;
     const int rep = (blockIdx.x + (threadIdx.x >> 5)) % kColRep;
-    unsigned krem = 0, jrem = 0;
-    if (check && lane == 0) {  // first poll of the own-column dependency, in flight early
-        const unsigned x = ld_relaxed(P.col_done + (size_t)c.z * kColRep + rep);
-        krem = x >= (unsigned)c.w ? 0u : (unsigned)c.w - x;
+    // own columns: lanes < ncol hold (column, earlier-phase items into it)
+    const int ncol = c.w;
+    int kcol = -1;
+    unsigned kneed = 0, krem = 0, jrem = 0;
+    if (lane < ncol) {
+        const int2 cd = __ldg(reinterpret_cast<const int2 *>(P.cdeps) + c.z + lane);
+        kcol = cd.x;
+        kneed = (unsigned)cd.y;
+        if (check) {  // first poll of the own-column dependency, in flight early
+            const unsigned x = ld_relaxed(P.col_done + (size_t)kcol * kColRep + rep);
+            krem = x >= kneed ? 0u : kneed - x;
+        }
     }
+    *mycol = kcol;
     int4 ch = make_int4(0, 0, 0, 0);
     if (lane < nch) ch = ldp(reinterpret_cast<const int4 *>(P.chunks) + c0 + lane);
     const int cnt = ch.w & 0x7fffffff;
@@ -487,7 +509,7 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
     }
     stamp(rec, 3, lane);
     if (__reduce_max_sync(0xffffffffu, max(krem, jrem)) != 0 &&
-        !wait_cols(P, lane, lane < nch, ch.y, jneed, c.z, (unsigned)c.w, lvl, cs, rep))
+        !wait_cols(P, lane, lane < nch, ch.y, jneed, lane < ncol, kcol, kneed, lvl, cs, rep))
         return false;
     stamp(rec, 4, lane);
     prefetch_item(P, na, nb, nc, lane);
@@ -770,11 +792,18 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
                 rec[2] = globaltimer();
             }
         }
-        const bool ok = (c.y & 1) ? run_deep(P, a, b, c, lane, &cs, wait_l, ring, sg, na, nb, nc, rec)
-                                  : run_push(P, a, b, c, lane, &cs, sg, rec, na, nb, nc);
+        int mycol = -1;  // lanes < ncol: the item's destination columns
+        bool ok;
+        if (c.y & 1) {
+            if (lane == 0) mycol = __ldg(reinterpret_cast<const int2 *>(P.cdeps) + c.z).x;
+            ok = run_deep(P, a, b, c, lane, &cs, wait_l, ring, sg, na, nb, nc, rec);
+        } else {
+            ok = run_push(P, a, b, c, lane, &cs, sg, rec, na, nb, nc, &mycol);
+        }
         if (!ok) return;
         ++ran;
-        finish_item(P, wq, nq, c.z, (c.y >> 1) & 1, lvl, ran, (nc.y >> 2) != lvl, lane);
+        finish_item(P, wq, nq, mycol, (c.y & 1) ? 1 : c.w, (c.y >> 1) & 1, lvl, ran,
+                    (nc.y >> 2) != lvl, lane);
         if (rec && lane == 0 && !(c.y & 1)) rec[7] = globaltimer() | (1ull << 63);
         a = na; b = nb; c = nc;
     }
@@ -1316,6 +1345,7 @@ struct glu_handle {
     // plan
     i32 *level_need = nullptr;  // per phase: item count
     i32 *col_total = nullptr;   // per column: items into it
+    glu::ColDep *cdeps = nullptr;
     i64 tail_t0 = 0;            // dense cluster tail: columns [tail_t0, n)
     i64 n_express = 0, express_R = 0;
     TailShape tail;
@@ -1481,6 +1511,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         UP(h->level_need, need);
         h->sync_words = (size_t)std::max<i64>(pv.n_levels, 1) * 8 + kLineWords + (size_t)std::max<i64>(n, 1) * kColRep;
         UP(h->col_total, std::vector<i32>(pv.col_total, pv.col_total + n));
+        if ((rc = upload_raw(h, &h->cdeps, pv.cdeps, pv.n_cdeps)) != GLU_OK) return fail(rc);
         h->tail_t0 = pv.tail_t0;
         h->n_express = pv.n_express;
         h->express_R = pv.express_R;
@@ -1540,7 +1571,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
 
 extern "C" void glu_destroy(glu_handle *h) {
     if (!h) return;
-    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->sync, h->tail_g, h->fail_batch, h->items,
+    void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
                     h->bar, h->ifail, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
@@ -1701,6 +1732,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.done = h->sync;
     P.col_done = h->sync + nl8 + kLineWords;
     P.col_total = h->col_total;
+    P.cdeps = h->cdeps;
     P.err = (int *)(h->sync + nl8);
     P.level_ns = h->time_levels ? h->level_ns : nullptr;
     P.fail_by_column = h->fail_by_column ? 1 : 0;

@@ -373,9 +373,15 @@ struct RawChunk {
     i32 m, d, p0, cnt;
 };
 
+constexpr int kMaxItemCols = 4;  // destination columns one merged push item may cover
+constexpr i64 kMaxSpanSlots = 65535;  // u16 target offsets of a merged item
+constexpr i64 kMergeCols = 64;        // merge window (columns) of the plan workers
+
 struct LocalItem {
     i32 lvl;
-    i32 k;
+    i32 k;      // first destination column
+    i32 ncols;  // destination columns (1..kMaxItemCols)
+    i32 cols[kMaxItemCols];
     i32 kind;
     i64 base;    // kPush: slot the target offsets are relative to; kDeep: target slot
     i64 macs;
@@ -426,6 +432,7 @@ struct PushEmitter {
         if (pos_scratch.size() == 1) {  // one target: ordered chain
             LocalItem it{};
             it.lvl = lvl; it.k = k; it.kind = glu::kDeep;
+            it.ncols = 1; it.cols[0] = k;
             it.base = cb + pos_scratch[0];
             it.macs = macs;
             it.c0 = (i64)o.deep.size();
@@ -447,31 +454,88 @@ struct PushEmitter {
         emit(right);
     }
 
+    // A finished segment (one column, one phase) joins the phase's pending
+    // merged item when the merged item stays within the item limits; small
+    // segments of neighbouring columns thus share one warp task (the wide
+    // phases otherwise shatter into ~10-MAC items).
+    struct Pending {
+        std::vector<glu::Chunk> pieces;
+        std::vector<i64> slots;  // absolute target slot of every entry, in MAC order
+        i32 cols[kMaxItemCols];
+        i32 ncols = 0;
+        i64 macs = 0, ntgt = 0, lo = 0, hi = -1;
+        bool crit_dummy = false;
+    };
+    std::vector<Pending> pend;      // per phase
+    std::vector<i32> pend_phases;   // phases with a pending item
+    std::vector<i64> slot_scratch;
+    bool merge = true;
+
     void make_item(const std::vector<glu::Chunk> &pieces, i64 macs) {
-        pos_scratch.clear();
+        slot_scratch.clear();
         for (auto &c : pieces)
-            for (i32 t = 0; t < c.meta; t++) pos_scratch.push_back(pos_of(c.p0 + t));
-        std::sort(pos_scratch.begin(), pos_scratch.end());
-        pos_scratch.erase(std::unique(pos_scratch.begin(), pos_scratch.end()), pos_scratch.end());
-        const i32 lo = pos_scratch[0];
+            for (i32 t = 0; t < c.meta; t++) slot_scratch.push_back(cb + pos_of(c.p0 + t));
+        std::vector<i64> uniq(slot_scratch);
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        const i64 ntgt = (i64)uniq.size(), lo = uniq.front(), hi = uniq.back();
+        if ((i64)pend.size() <= lvl) pend.resize(lvl + 1);
+        Pending &P = pend[lvl];
+        if (P.macs > 0) {
+            const bool same_col = P.cols[P.ncols - 1] == k;
+            const bool fits = merge && P.macs + macs <= T && P.ntgt + ntgt <= glu::kMaxItemMacs &&
+                              (i64)(P.pieces.size() + pieces.size()) <= glu::kMaxItemChunks &&
+                              (same_col || P.ncols < kMaxItemCols) &&
+                              std::max(P.hi, hi) - std::min(P.lo, lo) <= kMaxSpanSlots;
+            if (!fits) flush_phase(lvl);
+        }
+        if (P.macs == 0) {
+            P.pieces.clear();
+            P.slots.clear();
+            P.ncols = 0;
+            P.ntgt = 0;
+            P.lo = lo;
+            P.hi = hi;
+            pend_phases.push_back(lvl);
+        }
+        if (P.ncols == 0 || P.cols[P.ncols - 1] != k) P.cols[P.ncols++] = k;
+        P.pieces.insert(P.pieces.end(), pieces.begin(), pieces.end());
+        P.slots.insert(P.slots.end(), slot_scratch.begin(), slot_scratch.end());
+        P.macs += macs;
+        P.ntgt += ntgt;
+        P.lo = std::min(P.lo, lo);
+        P.hi = std::max(P.hi, hi);
+    }
+
+    void flush_phase(i32 l) {
+        Pending &P = pend[l];
+        if (P.macs == 0) return;
+        std::vector<i64> uniq(P.slots);
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        const i64 lo = uniq.front();
         LocalItem it{};
-        it.lvl = lvl; it.k = k; it.kind = glu::kPush;
-        it.base = cb + lo;
-        it.macs = macs;
+        it.lvl = l;
+        it.k = P.cols[0];
+        it.ncols = P.ncols;
+        for (int x = 0; x < P.ncols; x++) it.cols[x] = P.cols[x];
+        it.kind = glu::kPush;
+        it.base = lo;
+        it.macs = P.macs;
         it.t0 = (i64)o.tgt16.size();
-        for (i32 q : pos_scratch) o.tgt16.push_back((uint16_t)(q - lo));
+        for (i64 q : uniq) o.tgt16.push_back((uint16_t)(q - lo));
         it.t1 = (i64)o.tgt16.size();
         it.m0 = (i64)o.map8.size();
         it.c0 = (i64)o.chunks.size();
-        stamp.assign(pos_scratch.size(), -1);
+        stamp.assign(uniq.size(), -1);
         i32 ep = 0;
         bool first = true;
-        for (auto c : pieces) {
+        size_t e = 0;
+        for (auto c : P.pieces) {
             bool clash = false;
             const size_t mstart = o.map8.size();
-            for (i32 t = 0; t < c.meta; t++) {
-                const i32 u = (i32)(std::lower_bound(pos_scratch.begin(), pos_scratch.end(),
-                                                     pos_of(c.p0 + t)) - pos_scratch.begin());
+            for (i32 t = 0; t < c.meta; t++, e++) {
+                const i32 u = (i32)(std::lower_bound(uniq.begin(), uniq.end(), P.slots[e]) - uniq.begin());
                 o.map8.push_back((uint8_t)u);
                 clash = clash || stamp[u] == ep;
             }
@@ -483,6 +547,12 @@ struct PushEmitter {
         }
         it.c1 = (i64)o.chunks.size();
         o.items.push_back(it);
+        P.macs = 0;
+    }
+
+    void flush_all() {
+        for (i32 l : pend_phases) flush_phase(l);
+        pend_phases.clear();
     }
 };
 
@@ -497,6 +567,7 @@ struct glu_plan {
     std::vector<uint8_t> map8;
     std::vector<uint16_t> tgt16;
     std::vector<i32> col_total;
+    std::vector<glu::ColDep> cdeps;  // per item: destination columns and their earlier-phase counts
     i64 tail_t0 = 0, tail_macs = 0;
     i64 n_express = 0, express_R = 0;  // express queue: items [0, n_express) on the first express_R SMs
     i64 max_item_macs = 0;
@@ -582,12 +653,14 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         std::vector<std::vector<glu::Chunk>> seg_chunks;
         std::vector<std::vector<glu::DeepRef>> deep_lists;
         std::vector<i64> deep_pos;
-        PushEmitter em{o, row_idx, posmap, 0, 0, 0, 0, {}, {}};
+        PushEmitter em{o, row_idx, posmap, 0, 0, 0, 0, {}, {}, {}, {}, {}, true};
+        if (const char *e = std::getenv("GLU_MERGE")) em.merge = std::atoi(e) != 0;
         while (true) {
             i64 k0 = next.fetch_add(block);
             if (k0 >= n) break;
             i64 k1 = std::min<i64>(n, k0 + block);
             for (i64 k = k0; k < k1; k++) {
+                if (k > k0 && (k - k0) % kMergeCols == 0) em.flush_all();
                 i64 cb = col_ptr[k], ce = col_ptr[k + 1], len = ce - cb;
                 raw.clear();
                 bool any = false;
@@ -722,6 +795,8 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                         LocalItem it{};
                         it.lvl = lvl;
                         it.k = (i32)k;
+                        it.ncols = 1;
+                        it.cols[0] = (i32)k;
                         it.kind = glu::kDeep;
                         it.base = cb + deep_pos[x];
                         it.macs = (i64)deep_lists[x].size();
@@ -741,6 +816,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
                 }
                 for (i64 t = 0; t < len; t++) posmap[row_idx[cb + t]] = -1;
             }
+            em.flush_all();
         }
     };
     std::vector<std::thread> th;
@@ -761,7 +837,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     // descending (the longest items go first in the static warp round-robin;
     // a deep item's serial chain costs ~8x a push item's MAC), then column,
     // then base.
-    struct Ref { i32 lvl; i32 crit; i32 tid; i64 idx; i64 cost; i32 need; };
+    struct Ref { i32 lvl; i32 crit; i32 tid; i64 idx; i64 cost; i32 need[kMaxItemCols]; };
     std::vector<Ref> refs;
     size_t total_items = 0, total_map = 0, total_tgt = 0, total_chunks = 0, total_deep = 0;
     for (auto &o : outs) {
@@ -779,9 +855,10 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     for (int t = 0; t < nt; t++)
         for (i64 i = 0; i < (i64)outs[t].items.size(); i++) {
             const LocalItem &x = outs[t].items[i];
-            // critical: the destination is a source column of the next phase
-            const i32 crit = level_of[x.k] == x.lvl + 1 ? 1 : 0;
-            refs.push_back({x.lvl, crit, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs, 0});
+            // critical: a destination is a source column of the next phase
+            i32 crit = 0;
+            for (int c = 0; c < x.ncols; c++) crit |= level_of[x.cols[c]] == x.lvl + 1 ? 1 : 0;
+            refs.push_back({x.lvl, crit, t, i, x.kind == glu::kDeep ? 8 * x.macs : x.macs, {0, 0, 0, 0}});
         }
     // inside a phase: deep chains first (the longest serial work), then the
     // items the next phase waits for, then by cost
@@ -801,13 +878,16 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
     std::vector<i32> cnt_k(n, 0), pend_k(n, 0), last_k(n, -1);
     for (auto &r : refs) {
         const LocalItem &x = outs[r.tid].items[r.idx];
-        if (last_k[x.k] != x.lvl) {
-            cnt_k[x.k] += pend_k[x.k];
-            pend_k[x.k] = 0;
-            last_k[x.k] = x.lvl;
+        for (int c = 0; c < x.ncols; c++) {
+            const i32 k = x.cols[c];
+            if (last_k[k] != x.lvl) {
+                cnt_k[k] += pend_k[k];
+                pend_k[k] = 0;
+                last_k[k] = x.lvl;
+            }
+            r.need[c] = cnt_k[k];
+            pend_k[k]++;
         }
-        r.need = cnt_k[x.k];
-        pend_k[x.k]++;
     }
     // Express queue: in thin phases, the items into columns that are sources
     // within the next K phases (the critical chain and the items one or two
@@ -852,8 +932,9 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
         const LocalItem &x = o.items[r.idx];
         plan->level_item_ptr[x.lvl + 1]++;
         glu::Item it{};
-        it.col = x.k;
-        it.need = r.need;
+        it.col = (i32)plan->cdeps.size();  // its (column, need) list
+        it.need = x.ncols;
+        for (int c = 0; c < x.ncols; c++) plan->cdeps.push_back({x.cols[c], r.need[c]});
         it.base = (i32)x.base;
         it.macs = (i32)x.macs;
         // phase in the upper bits (dataflow waits); bit 1: critical (signal at once)
@@ -967,6 +1048,8 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.col_total = p->col_total.data();
     v.tail_t0 = p->tail_t0;
     v.n_express = p->n_express;
+    v.cdeps = p->cdeps.data();
+    v.n_cdeps = (i64)p->cdeps.size();
     v.express_R = p->express_R;
     return v;
 }

@@ -32,8 +32,14 @@ struct alignas(16) Item {
     int32_t ntgt;     // kPush: distinct targets (<= kMaxItemMacs)
     int32_t macs;     // MACs carried
     int32_t kind;     // ItemKind | critical << 1 | phase << 2
-    int32_t col;      // destination column k
-    int32_t need;     // items into column k in earlier phases (dataflow dependency)
+    int32_t col;      // first entry of its ColDep list (destination columns)
+    int32_t need;     // number of destination columns (1..4)
+};
+
+// A destination column of an item and the number of items into that column
+// in earlier phases (the item's dataflow dependency on its own targets).
+struct ColDep {
+    int32_t col, need;
 };
 static_assert(sizeof(Item) == 48, "Item layout");
 
@@ -72,6 +78,8 @@ struct glu_plan_view {
     const int32_t *col_total;  // per column: items into it (all phases)
     int64_t tail_t0;           // columns >= tail_t0: dense cluster tail (n: none)
     int64_t n_express;         // items [0, n_express): express queue
+    const ColDep *cdeps;
+    int64_t n_cdeps;
     int64_t express_R;         // SMs reserved for the express queue
 };
 
