@@ -1385,6 +1385,9 @@ struct glu_handle {
     // host-API staging
     double *d_a = nullptr, *d_v = nullptr, *d_x = nullptr;
     double *d_ab = nullptr, *d_vb = nullptr;  // batched host-API staging
+    cudaEvent_t ev_main = nullptr, ev_copy = nullptr;  // host API: overlap the D2H copy with the tail
+    cudaStream_t stream2 = nullptr;
+    i64 col_ptr_h_t0 = 0;  // first slot of the dense tail
     cudaStream_t stream = nullptr;
 };
 
@@ -1513,6 +1516,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         UP(h->col_total, std::vector<i32>(pv.col_total, pv.col_total + n));
         if ((rc = upload_raw(h, &h->cdeps, pv.cdeps, pv.n_cdeps)) != GLU_OK) return fail(rc);
         h->tail_t0 = pv.tail_t0;
+        h->col_ptr_h_t0 = col_ptr[pv.tail_t0];
         h->n_express = pv.n_express;
         h->express_R = pv.express_R;
         const i64 m = n - pv.tail_t0;
@@ -1578,6 +1582,9 @@ extern "C" void glu_destroy(glu_handle *h) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->stream2) cudaStreamDestroy(h->stream2);
+    if (h->ev_main) cudaEventDestroy(h->ev_main);
+    if (h->ev_copy) cudaEventDestroy(h->ev_copy);
     for (cudaEvent_t e : h->kev) cudaEventDestroy(e);
     delete h;
 }
@@ -1759,6 +1766,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     GLU_CUDA(cudaLaunchCooperativeKernel((const void *)factor_kernel, dim3(h->grid), dim3(kThreads),
                                          args, kFactorDynSmem, s));
     if (ke) GLU_CUDA(cudaEventRecord(ke[1], s));
+    if (h->ev_main) GLU_CUDA(cudaEventRecord(h->ev_main, s));  // columns < tail_t0 final
     if (h->tail_t0 < h->n) {
         TailParams T;
         T.v = v;
@@ -1997,8 +2005,26 @@ extern "C" int64_t glu_factor_host(glu_handle *h, const double *a_vals, double *
     cudaStream_t s = h->stream;
     GLU_CUDA(cudaMemcpyAsync(h->d_a, a_vals, sizeof(double) * h->nz, cudaMemcpyHostToDevice, s));
     if ((rc = glu_scatter_device(h, h->d_a, h->d_v, s)) != GLU_OK) return rc;
+    const bool split = h->tail_t0 < h->n && h->tail_t0 > 0;
+    if (split && !h->ev_main) {
+        GLU_CUDA(cudaEventCreateWithFlags(&h->ev_main, cudaEventDisableTiming));
+        GLU_CUDA(cudaEventCreateWithFlags(&h->ev_copy, cudaEventDisableTiming));
+        GLU_CUDA(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+    }
     if ((rc = launch_factor(h, h->d_v, thresh, s)) != GLU_OK) return rc;
-    GLU_CUDA(cudaMemcpyAsync(lu_out, h->d_v, sizeof(double) * h->nnz, cudaMemcpyDeviceToHost, s));
+    if (split) {
+        // the columns below the dense tail are final when the main kernel
+        // ends: copy them out while the cluster tail kernel runs
+        const i64 head = h->col_ptr_h_t0;
+        GLU_CUDA(cudaStreamWaitEvent(h->stream2, h->ev_main, 0));
+        GLU_CUDA(cudaMemcpyAsync(lu_out, h->d_v, sizeof(double) * head, cudaMemcpyDeviceToHost, h->stream2));
+        GLU_CUDA(cudaEventRecord(h->ev_copy, h->stream2));
+        GLU_CUDA(cudaMemcpyAsync(lu_out + head, h->d_v + head, sizeof(double) * (h->nnz - head),
+                                 cudaMemcpyDeviceToHost, s));
+        GLU_CUDA(cudaStreamWaitEvent(s, h->ev_copy, 0));
+    } else {
+        GLU_CUDA(cudaMemcpyAsync(lu_out, h->d_v, sizeof(double) * h->nnz, cudaMemcpyDeviceToHost, s));
+    }
     return read_fail(h, s);
 }
 
