@@ -206,6 +206,11 @@ int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const double *a_vals
 int64_t glu_solve_device(glu_handle *h, const double *lu, double *x, void *stream);
 int64_t glu_lower_solve_device(glu_handle *h, const double *lu, double *x, void *stream);
 int64_t glu_upper_solve_device(glu_handle *h, const double *lu, double *x, void *stream);
+/* Multi-RHS solves (device): x holds nrhs right-hand sides (column r at
+   x + r * ldx, ldx >= n), overwritten by the solutions; part 0 = L then U,
+   1 = L only, 2 = U only.  Each column is bitwise the single-RHS result. */
+int64_t glu_solve_multi_device(glu_handle *h, const double *lu, double *x, int64_t nrhs,
+                               int64_t ldx, int32_t part, void *stream);
 
 /* End-to-end host-buffer calls (the reference-facing plugin boundary):
    H2D of A values, device scatter, factor, D2H of LU. */

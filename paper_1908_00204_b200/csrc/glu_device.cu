@@ -1275,39 +1275,69 @@ struct SolveParams {
     i32 n_levels;
     unsigned int *bar;
     i32 upper;
+    i32 nrhs;      // right-hand sides, x + r * ldx
+    long long ldx;
 };
 
 __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveParams S) {
-    const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    constexpr int kSB = 4;  // product buffers in flight per warp
+    __shared__ __align__(16) double sbuf[kWarps][kSB][32];
+    __shared__ unsigned sbits[kWarps][kSB];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kWarps + w;
     const int nw = gridDim.x * kWarps;
     unsigned int target = 0;
     for (int l = 0; l < S.n_levels; ++l) {
         const int r0 = __ldg(S.lvl_ptr + l), r1 = __ldg(S.lvl_ptr + l + 1);
-        for (int ri = r0 + gw; ri < r1; ri += nw) {
+        const int cnt_l = r1 - r0;
+        // (row, right-hand side) pairs of the level over the warps
+        for (int idx = gw; idx < cnt_l * S.nrhs; idx += nw) {
+            const int ri = r0 + idx % cnt_l;
+            double *X = S.x + (size_t)(idx / cnt_l) * S.ldx;
             const int i = __ldg(S.rows + ri);
             const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
-            double acc = ldv(S.x + i);
+            double acc = ldv(X + i);
             const int ne = e1 - e0;
-            for (int base = 0; base < ne; base += 32) {
+            // lanes form 32 products at a time (independent roundings) into a
+            // shared buffer; lane 0 runs the ordered subtraction chain from
+            // it while the lanes load and form the next 32
+            auto form = [&](int base, int buf) {
                 // upper: entries are stored ascending; consume them descending
                 const int e = S.upper ? (e1 - 1 - base - lane) : (e0 + base + lane);
-                const int cnt = min(32, ne - base);
                 double prod = 0.0;
                 bool use = false;
-                if (lane < cnt) {
-                    const double xj = ldv(S.x + __ldg(S.ent_col + e));
+                if (base + lane < ne) {
+                    const double xj = ldv(X + __ldg(S.ent_col + e));
                     prod = __dmul_rn(ldv(S.v + __ldg(S.ent_slot + e)), xj);
                     use = S.upper ? true : (xj != 0.0);
                 }
-                const unsigned umask = __ballot_sync(0xffffffffu, use);
-                for (int s = 0; s < cnt; ++s) {
-                    const double p = __shfl_sync(0xffffffffu, prod, s);
-                    if (umask & (1u << s)) acc = __dsub_rn(acc, p);
+                sbuf[w][buf][lane] = prod;
+                const unsigned um = __ballot_sync(0xffffffffu, use);
+                if (lane == 0) sbits[w][buf] = um;
+            };
+            for (int c = 0; c < kSB - 1; ++c)
+                if (32 * c < ne) form(32 * c, c);
+            for (int base = 0; base < ne; base += 32) {
+                const int buf = (base >> 5) % kSB;
+                __syncwarp();
+                const int ahead = base + 32 * (kSB - 1);
+                if (ahead < ne) form(ahead, (ahead >> 5) % kSB);
+                if (lane == 0) {
+                    const unsigned um = sbits[w][buf];
+                    const double2 *pb = reinterpret_cast<const double2 *>(sbuf[w][buf]);
+#pragma unroll
+                    for (int s2 = 0; s2 < 16; ++s2) {
+                        const double2 x = pb[s2];
+                        const double a1 = __dsub_rn(acc, x.x);
+                        acc = ((um >> (2 * s2)) & 1u) ? a1 : acc;
+                        const double a2 = __dsub_rn(acc, x.y);
+                        acc = ((um >> (2 * s2 + 1)) & 1u) ? a2 : acc;
+                    }
                 }
+                __syncwarp();
             }
-            if (S.upper) acc = __ddiv_rn(acc, ldv(S.v + __ldg(S.diag_pos + i)));
-            if (lane == 0) stv(S.x + i, acc);
+            if (S.upper && lane == 0) acc = __ddiv_rn(acc, ldv(S.v + __ldg(S.diag_pos + i)));
+            if (lane == 0) stv(X + i, acc);
         }
         target += gridDim.x;
         grid_barrier(S.bar, target);
@@ -1933,7 +1963,8 @@ extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const dou
     return batch_status(h, batch, fail_cols, s);
 }
 
-static int64_t launch_solve(glu_handle *h, const double *lu, double *x, bool upper, cudaStream_t s) {
+static int64_t launch_solve(glu_handle *h, const double *lu, double *x, bool upper, cudaStream_t s,
+                            int nrhs = 1, i64 ldx = 0) {
     SolveParams S;
     S.v = lu;
     S.x = x;
@@ -1946,6 +1977,8 @@ static int64_t launch_solve(glu_handle *h, const double *lu, double *x, bool upp
     S.diag_pos = h->diag_pos;
     S.n_levels = (i32)(upper ? h->u_levels : h->l_levels);
     S.bar = h->bar;
+    S.nrhs = nrhs;
+    S.ldx = ldx > 0 ? ldx : h->n;
     GLU_CUDA(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int), s));
     void *args[] = {&S};
     GLU_CUDA(cudaLaunchCooperativeKernel((const void *)solve_kernel, dim3(h->grid), dim3(kThreads),
@@ -1995,6 +2028,26 @@ static int64_t ensure_staging(glu_handle *h) {
     if (!h->d_v) GLU_CUDA(cudaMalloc((void **)&h->d_v, sizeof(double) * std::max<i64>(h->nnz, 1)));
     if (!h->d_a) GLU_CUDA(cudaMalloc((void **)&h->d_a, sizeof(double) * std::max<i64>(h->nz, 1)));
     if (!h->d_x) GLU_CUDA(cudaMalloc((void **)&h->d_x, sizeof(double) * std::max<i64>(h->n, 1)));
+    return GLU_OK;
+}
+
+// Multi-RHS solves: x holds nrhs right-hand sides, column r at
+// x + r * ldx; part 0 = L then U, 1 = L only, 2 = U only.  Every level
+// spreads its (row, right-hand side) pairs over the warps; the per-element
+// order is the reference's, so every column is bitwise the single solve.
+extern "C" int64_t glu_solve_multi_device(glu_handle *h, const double *lu, double *x, int64_t nrhs,
+                                          int64_t ldx, int32_t part, void *stream) {
+    if (nrhs < 0 || (nrhs > 0 && ldx < h->n) || part < 0 || part > 2) {
+        glu::set_error("bad multi-RHS solve arguments");
+        return GLU_EINVAL;
+    }
+    if (nrhs == 0) return GLU_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    i64 rc;
+    if (part != 1 && (rc = check_zero_pivot(h, lu, s)) != GLU_OK) return rc;
+    if (part != 2 && (rc = launch_solve(h, lu, x, false, s, (int)nrhs, ldx)) != GLU_OK) return rc;
+    if (part != 1 && (rc = launch_solve(h, lu, x, true, s, (int)nrhs, ldx)) != GLU_OK) return rc;
+    GLU_CUDA(cudaStreamSynchronize(s));
     return GLU_OK;
 }
 

@@ -508,6 +508,32 @@ def _solve(lu: LuFactors, b: np.ndarray, part: str) -> np.ndarray:
     return x
 
 
+def solve_many(lu: LuFactors, b: np.ndarray) -> np.ndarray:
+    """Solve A X = B for the columns of B ([n, k]) in one pair of level-
+    scheduled launches; column j of the result is bitwise
+    solve(lu, B[:, j])."""
+    import torch
+
+    bb = np.asarray(b, dtype=np.float64)
+    if bb.ndim != 2 or bb.shape[0] != lu.n:
+        raise ValueError("right-hand sides must be [n, k]")
+    if lu.values.dtype != np.float64:
+        raise TypeError(f"the B200 path solves fp64 factors; got {lu.values.dtype}")
+    fz = get_factorizer(lu.pattern, _relaxed_levels(lu.pattern), _lib.CONTRACT_A)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    with fz._lock:
+        lu_d = torch.from_numpy(_lib.f64(lu.values)).to(dev)
+        x_d = torch.from_numpy(np.ascontiguousarray(bb.T)).to(dev)  # [k, n]: column j at j * n
+        s = torch.cuda.current_stream()
+        rc = _lib.check(_lib.lib.glu_solve_multi_device(fz.handle, _dptr(lu_d), _dptr(x_d), bb.shape[1],
+                                                        lu.n, 0, ctypes.c_void_p(s.cuda_stream)),
+                        "glu_solve_multi_device")
+        out = x_d.cpu().numpy().T.copy()
+    if rc >= 0:
+        raise PivotError(rc)
+    return out
+
+
 def lower_solve(lu: LuFactors, b: np.ndarray) -> np.ndarray:
     """L y = b, implicit unit diagonal (levlu/numeric.py:354-361)."""
     return _solve(lu, b, "lower")

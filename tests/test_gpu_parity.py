@@ -230,3 +230,16 @@ def test_cfg2_batched_launch_bitwise():
     for b in (0, 5, 7):
         assert np.array_equal(out[b], _oracle_values(glu.CscMatrix(a.n, a.col_ptr, a.row_idx, vals[b]),
                                                      fp, s, False))
+
+
+def test_solve_many_matches_single_solves():
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a)
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
+    B = np.random.default_rng(7).standard_normal((a.n, 5))
+    B[:, 3] = 0.0
+    X = glu.solve_many(lu, B)
+    for j in range(B.shape[1]):
+        assert np.array_equal(X[:, j], glu.solve(lu, B[:, j]))

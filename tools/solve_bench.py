@@ -1,0 +1,44 @@
+"""Triangular-solve timing (level-scheduled solve_kernel), cfg2: one and
+several right-hand sides, device-resident factors."""
+import sys, json, pathlib, ctypes
+import numpy as np
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import torch
+import paper_1908_00204_b200 as glu
+from paper_1908_00204_b200 import synthetic, _lib
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+a = synthetic.make(cfg)
+fp = glu.symbolic_fillin(a.pattern)
+s = glu.levelize(glu.detect_relaxed(fp))
+fz = glu.get_factorizer(fp, s.level_of, 0)
+fz.set_input(a.col_ptr, a.row_idx)
+lu, rc = fz.factor_host(a.values, 1e-14)
+assert rc == -1
+dev = torch.device("cuda", 0)
+lu_d = torch.from_numpy(lu).to(dev)
+st = torch.cuda.current_stream()
+out = {"config": cfg, "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
+       "usolve_levels": fz.handle_info["usolve_levels"]}
+for k in (1, 8, 32):
+    x = torch.randn((k, a.n), dtype=torch.float64, device=dev)
+    for _ in range(2):
+        _lib.lib.glu_solve_multi_device(fz.handle, glu.numeric._dptr(lu_d), glu.numeric._dptr(x), k, a.n, 0,
+                                        ctypes.c_void_p(st.cuda_stream))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    reps = 5
+    for _ in range(reps):
+        _lib.lib.glu_solve_multi_device(fz.handle, glu.numeric._dptr(lu_d), glu.numeric._dptr(x), k, a.n, 0,
+                                        ctypes.c_void_p(st.cuda_stream))
+    e1.record(st)
+    torch.cuda.synchronize()
+    out[f"nrhs{k}_ms"] = e0.elapsed_time(e1) / reps
+# residual of one solve through the public API
+b = np.random.default_rng(0).standard_normal(a.n)
+xs = glu.solve(glu.LuFactors(fp, lu), b)
+import scipy.sparse as sp
+A = sp.csc_matrix((a.values, a.row_idx, a.col_ptr), shape=(a.n, a.n))
+out["residual"] = float(np.linalg.norm(A @ xs - b) / np.linalg.norm(b))
+print(json.dumps(out))
