@@ -449,6 +449,7 @@ __device__ __forceinline__ void stamp(unsigned long long *rec, int k, int lane) 
     if (rec && lane == 0) rec[k] = globaltimer();
 }
 
+template <int KR, int NS>
 __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, int4 c, int lane,
                                          CtaSync *cs, double *sg, unsigned long long *rec, int4 na,
                                          int4 nb, int4 nc, int *mycol) {
@@ -496,9 +497,9 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
             jrem = x >= jneed ? 0u : jneed - x;
         }
     }
-    int u[kR], ci[kR], to[kR];
+    int u[KR], ci[KR], to[KR];
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
+    for (int r = 0; r < KR; ++r) {
         u[r] = -1;
         to[r] = -1;
         if (r < nr) {
@@ -513,59 +514,70 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
         return false;
     stamp(rec, 4, lane);
     prefetch_item(P, na, nb, nc, lane);
-    // value phase, once per value set of the launch (batch: the static part,
-    // the dependency wait and the release are shared by all sets)
-    for (int bs = 0; bs < P.nb; ++bs) {
-    double *V = P.v + (size_t)bs * P.set_stride;
-    // one round of independent loads
-    double piv = 1.0, mult = 0.0;
-    if (lane < nch) {
-        piv = ldv(V + dslot);
-        mult = ldv(V + ch.x);
-    }
-    double t[kR], l[kR];
+    // value phase: NS value sets per round of loads (batch launches share
+    // the static part, the dependency wait and the release across all sets)
+    int ep[KR];
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
-        if (to[r] >= 0) t[r] = ldv(V + base + to[r]);
-        if (r < nr) {
-            const int cp0 = __shfl_sync(0xffffffffu, ch.z, ci[r]);
-            const int cest = __shfl_sync(0xffffffffu, est, ci[r]);
-            if (u[r] >= 0) l[r] = ldv(V + cp0 + (32 * r + lane - cest));
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < kR; ++r)
-        if (to[r] >= 0) sg[32 * r + lane] = t[r];
-    int ep[kR];
-#pragma unroll
-    for (int r = 0; r < kR; ++r) {
-        if (r < nr) {
-            const double pv = __shfl_sync(0xffffffffu, piv, ci[r]);
-            const double mu = __shfl_sync(0xffffffffu, mult, ci[r]);
-            ep[r] = __shfl_sync(0xffffffffu, myep, ci[r]);
-            if (u[r] >= 0) l[r] = __dmul_rn(__ddiv_rn(l[r], pv), mu);  // the product
-        }
-    }
-    __syncwarp();
-    if (bs == 0) stamp(rec, 5, lane);
+    for (int r = 0; r < KR; ++r) ep[r] = __shfl_sync(0xffffffffu, myep, r < nr ? ci[r] : 0);
     const int nep = __popc(epm);
-    if (nep == 1) {
+    for (int bs0 = 0; bs0 < P.nb; bs0 += NS) {
+        double piv[NS], mult[NS], t[NS][KR], l[NS][KR];
 #pragma unroll
-        for (int r = 0; r < kR; ++r)
-            if (u[r] >= 0) sg[u[r]] = __dsub_rn(sg[u[r]], l[r]);
-    } else {
-        for (int e = 0; e < nep; ++e) {
+        for (int ns = 0; ns < NS; ++ns) {
+            piv[ns] = 1.0;
+            mult[ns] = 0.0;
+            if (bs0 + ns >= P.nb) continue;
+            const double *V = P.v + (size_t)(bs0 + ns) * P.set_stride;
+            if (lane < nch) {
+                piv[ns] = ldv(V + dslot);
+                mult[ns] = ldv(V + ch.x);
+            }
 #pragma unroll
-            for (int r = 0; r < kR; ++r)
-                if (u[r] >= 0 && ep[r] == e) sg[u[r]] = __dsub_rn(sg[u[r]], l[r]);
-            __syncwarp();
+            for (int r = 0; r < KR; ++r) {
+                if (to[r] >= 0) t[ns][r] = ldv(V + base + to[r]);
+                if (r < nr) {
+                    const int cp0 = __shfl_sync(0xffffffffu, ch.z, ci[r]);
+                    const int cest = __shfl_sync(0xffffffffu, est, ci[r]);
+                    if (u[r] >= 0) l[ns][r] = ldv(V + cp0 + (32 * r + lane - cest));
+                }
+            }
         }
-    }
-    __syncwarp();
 #pragma unroll
-    for (int r = 0; r < kR; ++r)
-        if (to[r] >= 0) stv(V + base + to[r], sg[32 * r + lane]);
-    __syncwarp();
+        for (int ns = 0; ns < NS; ++ns) {
+            if (bs0 + ns >= P.nb) continue;
+            double *sgn = sg + ns * (KR * 32);
+            double *V = P.v + (size_t)(bs0 + ns) * P.set_stride;
+#pragma unroll
+            for (int r = 0; r < KR; ++r)
+                if (to[r] >= 0) sgn[32 * r + lane] = t[ns][r];
+#pragma unroll
+            for (int r = 0; r < KR; ++r) {
+                if (r < nr) {
+                    const double pv = __shfl_sync(0xffffffffu, piv[ns], ci[r]);
+                    const double mu = __shfl_sync(0xffffffffu, mult[ns], ci[r]);
+                    if (u[r] >= 0) l[ns][r] = __dmul_rn(__ddiv_rn(l[ns][r], pv), mu);  // the product
+                }
+            }
+            __syncwarp();
+            if (bs0 + ns == 0) stamp(rec, 5, lane);
+            if (nep == 1) {
+#pragma unroll
+                for (int r = 0; r < KR; ++r)
+                    if (u[r] >= 0) sgn[u[r]] = __dsub_rn(sgn[u[r]], l[ns][r]);
+            } else {
+                for (int e = 0; e < nep; ++e) {
+#pragma unroll
+                    for (int r = 0; r < KR; ++r)
+                        if (u[r] >= 0 && ep[r] == e) sgn[u[r]] = __dsub_rn(sgn[u[r]], l[ns][r]);
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < KR; ++r)
+                if (to[r] >= 0) stv(V + base + to[r], sgn[32 * r + lane]);
+        }
+        __syncwarp();
     }
     __syncwarp();
     stamp(rec, 6, lane);
@@ -718,6 +730,7 @@ __device__ __forceinline__ void divide_column(const FactorParams &Pin, int j, in
     for (int p = d + 1 + lane; p < hi; p += 32) stv(P.v + p, __ddiv_rn(ldv(P.v + p), piv));
 }
 
+template <int KR, int NS>
 __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     const int lane = threadIdx.x & 31;
     // consecutive items go to consecutive SMs (a thin phase spreads over the chip)
@@ -798,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
             if (lane == 0) mycol = __ldg(reinterpret_cast<const int2 *>(P.cdeps) + c.z).x;
             ok = run_deep(P, a, b, c, lane, &cs, wait_l, ring, sg, na, nb, nc, rec);
         } else {
-            ok = run_push(P, a, b, c, lane, &cs, sg, rec, na, nb, nc, &mycol);
+            ok = run_push<KR, NS>(P, a, b, c, lane, &cs, sg, rec, na, nb, nc, &mycol);
         }
         if (!ok) return;
         ++ran;
@@ -1378,6 +1391,7 @@ struct glu_handle {
     glu::ColDep *cdeps = nullptr;
     i64 tail_t0 = 0;            // dense cluster tail: columns [tail_t0, n)
     i64 n_express = 0, express_R = 0;
+    i64 max_push_macs = 0;  // largest push item of the plan (kernel variant)
     TailShape tail;
     double *tail_g = nullptr;
     unsigned long long *fail_batch = nullptr;
@@ -1548,6 +1562,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         h->tail_t0 = pv.tail_t0;
         h->col_ptr_h_t0 = col_ptr[pv.tail_t0];
         h->n_express = pv.n_express;
+        h->max_push_macs = pv.max_push_macs;
         h->express_R = pv.express_R;
         const i64 m = n - pv.tail_t0;
         if (m > 0) {
@@ -1596,8 +1611,10 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         cudaMalloc((void **)&h->ifail, sizeof(int)) != cudaSuccess) {
         glu::set_error("cudaMalloc(scratch)"); return fail(GLU_ECUDA);
     }
-    h->grid = std::min(coop_grid((const void *)factor_kernel, h->sm_count, kFactorDynSmem),
-                       coop_grid((const void *)solve_kernel, h->sm_count));
+    h->grid = std::min({coop_grid((const void *)factor_kernel<4, 1>, h->sm_count, kFactorDynSmem),
+                        coop_grid((const void *)factor_kernel<2, 2>, h->sm_count, kFactorDynSmem),
+                        coop_grid((const void *)factor_kernel<2, 1>, h->sm_count, kFactorDynSmem),
+                        coop_grid((const void *)solve_kernel, h->sm_count)});
     if (h->grid <= 0) { glu::set_error("persistent kernel cannot be co-resident"); return fail(GLU_ECUDA); }
     *out = h;
     return GLU_OK;
@@ -1793,8 +1810,12 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         h->kev_next++;
         GLU_CUDA(cudaEventRecord(ke[0], s));
     }
-    GLU_CUDA(cudaLaunchCooperativeKernel((const void *)factor_kernel, dim3(h->grid), dim3(kThreads),
-                                         args, kFactorDynSmem, s));
+    // plans with <= 64-MAC items (batch plans) run the 2-entries-per-lane
+    // variant, which loads two value sets per round in batched launches
+    const void *kfn = h->max_push_macs <= 64 ? (nb > 1 ? (const void *)factor_kernel<2, 2>
+                                                        : (const void *)factor_kernel<2, 1>)
+                                             : (const void *)factor_kernel<4, 1>;
+    GLU_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(h->grid), dim3(kThreads), args, kFactorDynSmem, s));
     if (ke) GLU_CUDA(cudaEventRecord(ke[1], s));
     if (h->ev_main) GLU_CUDA(cudaEventRecord(h->ev_main, s));  // columns < tail_t0 final
     if (h->tail_t0 < h->n) {

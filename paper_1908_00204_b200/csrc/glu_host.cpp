@@ -571,6 +571,7 @@ struct glu_plan {
     i64 tail_t0 = 0, tail_macs = 0;
     i64 n_express = 0, express_R = 0;  // express queue: items [0, n_express) on the first express_R SMs
     i64 max_item_macs = 0;
+    i64 max_push_macs = 0;
     i64 max_chunks = 0;
     i64 deferred = 0;
     i64 n_deep_items = 0;
@@ -959,6 +960,7 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
             }
             it.nch = (i32)(x.c1 - x.c0);
             plan->max_chunks = std::max<i64>(plan->max_chunks, x.c1 - x.c0);
+            plan->max_push_macs = std::max<i64>(plan->max_push_macs, x.macs);
         }
         plan->max_item_macs = std::max<i64>(plan->max_item_macs, x.macs);
         plan->items.push_back(it);
@@ -1049,6 +1051,7 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.tail_t0 = p->tail_t0;
     v.n_express = p->n_express;
     v.cdeps = p->cdeps.data();
+    v.max_push_macs = p->max_push_macs;
     v.n_cdeps = (i64)p->cdeps.size();
     v.express_R = p->express_R;
     return v;

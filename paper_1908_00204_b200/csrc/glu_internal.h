@@ -80,6 +80,7 @@ struct glu_plan_view {
     int64_t n_express;         // items [0, n_express): express queue
     const ColDep *cdeps;
     int64_t n_cdeps;
+    int64_t max_push_macs;     // largest push item (selects the kernel variant)
     int64_t express_R;         // SMs reserved for the express queue
 };
 

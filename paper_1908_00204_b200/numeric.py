@@ -312,7 +312,10 @@ def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int,
         hit = _CACHE.get(key)
         if hit is not None and hit[0]() is fp:
             return hit[1]
-        fz = Factorizer(fp, level_of, contract, tail_max=None if tail else 0)
+        # batch plans: no dense tail, 64-MAC items (the kernel variant that
+        # loads two value sets per round)
+        fz = Factorizer(fp, level_of, contract, tail_max=None if tail else 0,
+                        max_item_macs=0 if tail else 64)
 
         def _drop(_ref, key=key):
             with _CACHE_LOCK:
