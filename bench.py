@@ -60,6 +60,25 @@ def parse():
     return p.parse_args()
 
 
+def init_dist(world, local):
+    """One process per GPU over NCCL.  GLU_DIST_BACKEND=gloo (test only) lets
+    several ranks share one GPU to exercise the multi-rank code path."""
+    import torch
+
+    ndev = max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = os.environ.get("GLU_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -282,12 +301,7 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     import paper_1908_00204_b200 as glu
 
     a = load_config(args.config)
@@ -327,7 +341,7 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with Clocks(dev.index) as clk:
         for i in range(args.steps):
             flush.zero_()  # L2 flush outside the timed events
             step(i, evs[i])
@@ -461,12 +475,7 @@ def run_batch(args):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     import paper_1908_00204_b200 as glu
     from paper_1908_00204_b200 import batch as glu_batch
 
@@ -493,7 +502,7 @@ def run_batch(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(dev.index) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             fails = step()  # status read per step (synchronizes: part of the API)
