@@ -42,6 +42,7 @@ CONFIG_DESC = {
     "cfg2": "synthetic rajat-style circuit n=100,000 + 4 dense power/ground hubs (10%), "
             "SuperLU MMD order",
     "cfg3": "synthetic ASIC_680k-like n=680,000 (1-D local +-40, 6 hubs x 1%), SuperLU MMD order",
+    "g400": "G3-family 5-point grid 400x400 (n=160,000), geometric nested dissection",
 }
 
 

@@ -231,6 +231,8 @@ CONFIGS = {
     "cfg2": lambda: circuit_like(100_000, hubs=4, hub_frac=0.10, seed=0),
     "cfg3": lambda: asic_like(680_000, seed=0),
     "cfg4": lambda: grid5(1258, seed=0),
+    # G3-family data point at a size whose plan fits (cfg4's does not yet)
+    "g400": lambda: grid5(400, seed=0),
 }
 
 
