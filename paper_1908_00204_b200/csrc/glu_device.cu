@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1249,9 +1250,11 @@ TailShape pick_tail(int m, int *cap_out) {
         };
         while (cap + 1 <= 2 * kTailThreads && fits(cap + 1, 4)) ++cap;
         if (cap_out && cap > *cap_out) *cap_out = cap;
+        int bmax = 16;  // widest panel that fits (GLU_TAIL_B caps it: tuning)
+        if (const char *e = std::getenv("GLU_TAIL_B")) bmax = std::max(4, std::min(16, std::atoi(e)));
         if (m > 0)
             for (int b : {16, 8, 4})
-                if (fits(m, b)) return tail_shape(m, C, b);
+                if (b <= bmax && fits(m, b)) return tail_shape(m, C, b);
     }
     return best;
 }
