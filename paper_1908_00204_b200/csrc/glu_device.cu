@@ -1005,10 +1005,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
 #pragma unroll
                 for (int kk = k + 1; kk < kTailB; ++kk) {
                     const double u = ur[kk];
-                    const double ta = __dsub_rn(ra[kk], __dmul_rn(la, u));
-                    const double tb = __dsub_rn(rb[kk], __dmul_rn(lb, u));
-                    ra[kk] = ((ma >> kk) & 1u) ? ta : ra[kk];
-                    rb[kk] = ((mb >> kk) & 1u) ? tb : rb[kk];
+                    ra[kk] = __dsub_rn(ra[kk], ((ma >> kk) & 1u) ? __dmul_rn(la, u) : 0.0);
+                    rb[kk] = __dsub_rn(rb[kk], ((mb >> kk) & 1u) ? __dmul_rn(lb, u) : 0.0);
                 }
             }
         }
@@ -1082,10 +1080,9 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
                 double t0 = c0[ia], t1 = c1[ia];
 #pragma unroll
                 for (int k = 0; k < kTailB; ++k) {
-                    const double r0 = __dsub_rn(t0, __dmul_rn(la[k], c0[s0 + k]));
-                    const double r1 = __dsub_rn(t1, __dmul_rn(la[k], c1[s0 + k]));
-                    t0 = ((a0 >> k) & 1u) ? r0 : t0;
-                    t1 = ((a1 >> k) & 1u) ? r1 : t1;
+                    // absent MACs contribute +0.0 (an exact no-op): no select in the chain
+                    t0 = __dsub_rn(t0, ((a0 >> k) & 1u) ? __dmul_rn(la[k], c0[s0 + k]) : 0.0);
+                    t1 = __dsub_rn(t1, ((a1 >> k) & 1u) ? __dmul_rn(la[k], c1[s0 + k]) : 0.0);
                 }
                 c0[ia] = t0;
                 c1[ia] = t1;
@@ -1094,10 +1091,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
                 double t0 = c0[ib], t1 = c1[ib];
 #pragma unroll
                 for (int k = 0; k < kTailB; ++k) {
-                    const double r0 = __dsub_rn(t0, __dmul_rn(lb[k], c0[s0 + k]));
-                    const double r1 = __dsub_rn(t1, __dmul_rn(lb[k], c1[s0 + k]));
-                    t0 = ((b0 >> k) & 1u) ? r0 : t0;
-                    t1 = ((b1 >> k) & 1u) ? r1 : t1;
+                    t0 = __dsub_rn(t0, ((b0 >> k) & 1u) ? __dmul_rn(lb[k], c0[s0 + k]) : 0.0);
+                    t1 = __dsub_rn(t1, ((b1 >> k) & 1u) ? __dmul_rn(lb[k], c1[s0 + k]) : 0.0);
                 }
                 c0[ib] = t0;
                 c1[ib] = t1;
@@ -1110,19 +1105,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
             if (ua) {
                 double t = cq[ia];
 #pragma unroll
-                for (int k = 0; k < kTailB; ++k) {
-                    const double r = __dsub_rn(t, __dmul_rn(la[k], cq[s0 + k]));
-                    t = ((ua >> k) & 1u) ? r : t;
-                }
+                for (int k = 0; k < kTailB; ++k)
+                    t = __dsub_rn(t, ((ua >> k) & 1u) ? __dmul_rn(la[k], cq[s0 + k]) : 0.0);
                 cq[ia] = t;
             }
             if (ubb) {
                 double t = cq[ib];
 #pragma unroll
-                for (int k = 0; k < kTailB; ++k) {
-                    const double r = __dsub_rn(t, __dmul_rn(lb[k], cq[s0 + k]));
-                    t = ((ubb >> k) & 1u) ? r : t;
-                }
+                for (int k = 0; k < kTailB; ++k)
+                    t = __dsub_rn(t, ((ubb >> k) & 1u) ? __dmul_rn(lb[k], cq[s0 + k]) : 0.0);
                 cq[ib] = t;
             }
         }
@@ -1295,10 +1286,17 @@ struct SolveParams {
     long long ldx;
 };
 
+constexpr int kSolveRing = 4;  // entry-index chunks in flight per warp (cp.async)
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pred) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = pred ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveParams S) {
-    constexpr int kSB = 4;  // product buffers in flight per warp
-    __shared__ __align__(16) double sbuf[kWarps][kSB][32];
-    __shared__ unsigned sbits[kWarps][kSB];
+    __shared__ __align__(16) double pbuf[kWarps][32];
+    __shared__ int icol[kWarps][kSolveRing][32], islot[kWarps][kSolveRing][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarps + w;
     const int nw = gridDim.x * kWarps;
@@ -1313,45 +1311,69 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveParams S) {
             const int i = __ldg(S.rows + ri);
             const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
             double acc = ldv(X + i);
-            const int ne = e1 - e0;
-            // lanes form 32 products at a time (independent roundings) into a
-            // shared buffer; lane 0 runs the ordered subtraction chain from
-            // it while the lanes load and form the next 32
-            auto form = [&](int base, int buf) {
-                // upper: entries are stored ascending; consume them descending
-                const int e = S.upper ? (e1 - 1 - base - lane) : (e0 + base + lane);
-                double prod = 0.0;
-                bool use = false;
-                if (base + lane < ne) {
-                    const double xj = ldv(X + __ldg(S.ent_col + e));
-                    prod = __dmul_rn(ldv(S.v + __ldg(S.ent_slot + e)), xj);
-                    use = S.upper ? true : (xj != 0.0);
-                }
-                sbuf[w][buf][lane] = prod;
-                const unsigned um = __ballot_sync(0xffffffffu, use);
-                if (lane == 0) sbits[w][buf] = um;
+            const int ne = e1 - e0, ng = (ne + 31) >> 5;
+            // Pipeline per row: entry indices stream into a shared ring
+            // kSolveRing chunks ahead (cp.async), the x / L-or-U value loads of
+            // chunk g+1 are in flight while lanes form the products of chunk g
+            // (independent roundings) and lane 0 runs the ordered chain --
+            // ascending column for L (skipping zero x, _kernels.py:176-183),
+            // descending for U (_kernels.py:186-197) -- from shared memory.
+            auto ent = [&](int k) { return S.upper ? (e1 - 1 - k) : (e0 + k); };
+            auto issue_idx = [&](int g) {
+                const int k = 32 * g + lane;
+                const int e = ent(min(k, ne - 1));
+                cp_async4(&icol[w][g % kSolveRing][lane], S.ent_col + e, k < ne);
+                cp_async4(&islot[w][g % kSolveRing][lane], S.ent_slot + e, k < ne);
+                cp_async_commit();
             };
-            for (int c = 0; c < kSB - 1; ++c)
-                if (32 * c < ne) form(32 * c, c);
-            for (int base = 0; base < ne; base += 32) {
-                const int buf = (base >> 5) % kSB;
-                __syncwarp();
-                const int ahead = base + 32 * (kSB - 1);
-                if (ahead < ne) form(ahead, (ahead >> 5) % kSB);
-                if (lane == 0) {
-                    const unsigned um = sbits[w][buf];
-                    const double2 *pb = reinterpret_cast<const double2 *>(sbuf[w][buf]);
 #pragma unroll
-                    for (int s2 = 0; s2 < 16; ++s2) {
-                        const double2 x = pb[s2];
-                        const double a1 = __dsub_rn(acc, x.x);
-                        acc = ((um >> (2 * s2)) & 1u) ? a1 : acc;
-                        const double a2 = __dsub_rn(acc, x.y);
-                        acc = ((um >> (2 * s2 + 1)) & 1u) ? a2 : acc;
+            for (int g = 0; g < kSolveRing; ++g) issue_idx(g);
+            double xa = 0.0, va = 0.0;  // operands of the chunk being consumed next
+            cp_async_wait<kSolveRing - 1>();
+            __syncwarp();
+            if (lane < ne) {
+                xa = ldv(X + icol[w][0][lane]);
+                va = ldv(S.v + islot[w][0][lane]);
+            }
+            for (int g = 0; g < ng; ++g) {
+                // operands of chunk g+1 (its indices landed: at most kSolveRing-2
+                // newer groups pending)
+                double xb = 0.0, vb = 0.0;
+                cp_async_wait<kSolveRing - 2>();
+                __syncwarp();
+                if (32 * (g + 1) + lane < ne) {
+                    xb = ldv(X + icol[w][(g + 1) % kSolveRing][lane]);
+                    vb = ldv(S.v + islot[w][(g + 1) % kSolveRing][lane]);
+                }
+                __syncwarp();
+                issue_idx(g + kSolveRing);  // refill the slot of chunk g
+                const bool live = 32 * g + lane < ne;
+                const bool use = live && (S.upper ? true : (xa != 0.0));
+                // a skipped entry contributes +0.0: subtracting +0.0 is an exact
+                // no-op in IEEE round-to-nearest (also for -0, inf and NaN), so
+                // the chain is pure subtractions with no select in its path
+                pbuf[w][lane] = use ? __dmul_rn(va, xa) : 0.0;
+                __syncwarp();
+                if (lane == 0) {
+                    const double2 *pb = reinterpret_cast<const double2 *>(pbuf[w]);
+                    const int cnt = min(32, ne - 32 * g);
+                    if (cnt == 32) {
+#pragma unroll
+                        for (int s2 = 0; s2 < 16; ++s2) {
+                            const double2 x = pb[s2];
+                            acc = __dsub_rn(acc, x.x);
+                            acc = __dsub_rn(acc, x.y);
+                        }
+                    } else {
+                        for (int s1 = 0; s1 < cnt; ++s1) acc = __dsub_rn(acc, pbuf[w][s1]);
                     }
                 }
                 __syncwarp();
+                xa = xb;
+                va = vb;
             }
+            cp_async_wait<0>();
+            __syncwarp();
             if (S.upper && lane == 0) acc = __ddiv_rn(acc, ldv(S.v + __ldg(S.diag_pos + i)));
             if (lane == 0) stv(X + i, acc);
         }
