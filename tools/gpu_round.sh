@@ -18,6 +18,7 @@ timeout 600 python bench.py --batch 8 --steps 5 --warmup 3 > gpurun_out/bench_ba
 cut -c1-300 gpurun_out/bench_batch8_${TAG}.json
 timeout 900 python bench.py --config cfg3 --steps 10 --warmup 3 > gpurun_out/bench_cfg3_${TAG}.json 2> gpurun_out/bench_cfg3_${TAG}.err; echo "cfg3 rc=$?"
 cut -c1-300 gpurun_out/bench_cfg3_${TAG}.json
+timeout 300 python tools/solve_bench.py cfg2 > gpurun_out/solve_${TAG}.json 2>&1; echo "solve rc=$?"; cut -c1-300 gpurun_out/solve_${TAG}.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${TAG}.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "launch rc=$?"
