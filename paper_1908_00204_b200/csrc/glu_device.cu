@@ -1382,6 +1382,165 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveParams S) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Dataflow triangular solves (default): no grid barrier.  Every unknown of
+// the solve's OUTPUT vector holds a signalling-NaN sentinel until its row is
+// done; IEEE arithmetic never produces a signalling NaN, so one relaxed
+// 8-byte load both observes "ready" and fetches the value -- no flags, no
+// fences.  Rows are taken in level order from a ticket counter, so a row
+// waits only on rows with smaller tickets, all held by running warps
+// (cooperative launch): deadlock-free.  A long row streams its chain chunk
+// by chunk as its inputs arrive instead of waiting for its level.
+//
+// Buffers: the L pass reads b from X, writes y to Y (all-sentinel on entry)
+// and leaves X all-sentinel; the U pass reads y from Y, restores Y to the
+// sentinel and writes x to X.  Between calls Y is all-sentinel.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kSent = 0x7FF4DEAD5EB17A11ull;  // signalling NaN
+constexpr unsigned long long kQuietBit = 1ull << 51;
+
+struct SolveDfParams {
+    const double *v;
+    const double *in;     // L: b (X), U: y (Y)
+    double *out;          // L: y (Y), U: x (X)
+    double *reset;        // L: X (set to sentinel), U: Y (restored to sentinel)
+    long long ld_in, ld_out, ld_reset;
+    const i32 *rows;      // level-sorted
+    const i32 *ent_ptr, *ent_col, *ent_slot;
+    const i32 *diag_pos;
+    i32 n;
+    i32 upper;
+    i32 nrhs;
+    unsigned int *ticket;
+    unsigned int *err;
+};
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(double *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) {
+    __shared__ __align__(16) double pbuf[kWarps][32];
+    __shared__ int icol[kWarps][kSolveRing][32], islot[kWarps][kSolveRing][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned total = (unsigned)S.n * (unsigned)S.nrhs;
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(S.ticket, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    while (t < total) {
+        unsigned tn = 0;  // next ticket, in flight while this row runs
+        if (lane == 0) tn = atomicAdd(S.ticket, 1u);
+        const int ri = (int)(t / (unsigned)S.nrhs), r = (int)(t % (unsigned)S.nrhs);
+        const int i = __ldg(S.rows + ri);
+        const double *Xin = S.out + (size_t)r * S.ld_out;  // rows read by this row (ready-or-sentinel)
+        const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
+        double acc = ldv(S.in + (size_t)r * S.ld_in + i);
+        const int ne = e1 - e0, ng = (ne + 31) >> 5;
+        auto ent = [&](int k) { return S.upper ? (e1 - 1 - k) : (e0 + k); };
+        auto issue_idx = [&](int g) {
+            const int k = 32 * g + lane;
+            const int e = ent(min(k, ne - 1));
+            cp_async4(&icol[w][g % kSolveRing][lane], S.ent_col + e, k < ne);
+            cp_async4(&islot[w][g % kSolveRing][lane], S.ent_slot + e, k < ne);
+            cp_async_commit();
+        };
+        if (ne > 0) {
+#pragma unroll
+            for (int g = 0; g < kSolveRing; ++g) issue_idx(g);
+            unsigned long long xa = 0;
+            double va = 0.0;
+            cp_async_wait<kSolveRing - 1>();
+            __syncwarp();
+            if (lane < ne) {
+                xa = ld_relaxed_u64(Xin + icol[w][0][lane]);
+                va = ldv(S.v + islot[w][0][lane]);
+            }
+            for (int g = 0; g < ng; ++g) {
+                unsigned long long xb = 0;
+                double vb = 0.0;
+                cp_async_wait<kSolveRing - 2>();
+                __syncwarp();
+                const bool live = 32 * g + lane < ne;
+                // chunk g's inputs: re-poll the lanes whose row is not done yet
+                if (__any_sync(0xffffffffu, live && xa == kSent)) {
+                    const unsigned long long t0 = globaltimer();
+                    const int c = icol[w][g % kSolveRing][lane];
+                    while (true) {
+                        const bool pend = live && xa == kSent;
+                        if (!__any_sync(0xffffffffu, pend)) break;
+                        if (pend) xa = ld_relaxed_u64(Xin + c);
+                        if (globaltimer() - t0 > kWatchdogNs) {
+                            if (lane == 0) atomicExch(S.err, 1u);
+                            return;
+                        }
+                    }
+                }
+                if (32 * (g + 1) + lane < ne) {
+                    xb = ld_relaxed_u64(Xin + icol[w][(g + 1) % kSolveRing][lane]);
+                    vb = ldv(S.v + islot[w][(g + 1) % kSolveRing][lane]);
+                }
+                __syncwarp();
+                issue_idx(g + kSolveRing);
+                const double x = __longlong_as_double((long long)xa);
+                const bool use = live && (S.upper ? true : (x != 0.0));
+                pbuf[w][lane] = use ? __dmul_rn(va, x) : 0.0;
+                __syncwarp();
+                if (lane == 0) {
+                    const double2 *pb = reinterpret_cast<const double2 *>(pbuf[w]);
+                    const int cnt = min(32, ne - 32 * g);
+                    if (cnt == 32) {
+#pragma unroll
+                        for (int s2 = 0; s2 < 16; ++s2) {
+                            const double2 p2 = pb[s2];
+                            acc = __dsub_rn(acc, p2.x);
+                            acc = __dsub_rn(acc, p2.y);
+                        }
+                    } else {
+                        for (int s1 = 0; s1 < cnt; ++s1) acc = __dsub_rn(acc, pbuf[w][s1]);
+                    }
+                }
+                __syncwarp();
+                xa = xb;
+                va = vb;
+            }
+            cp_async_wait<0>();
+            __syncwarp();
+        }
+        if (lane == 0) {
+            if (S.upper) acc = __ddiv_rn(acc, ldv(S.v + __ldg(S.diag_pos + i)));
+            unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
+            if (bits == kSent) bits |= kQuietBit;  // only an untouched input can carry it
+            st_relaxed_u64(S.out + (size_t)r * S.ld_out + i, bits);
+            st_relaxed_u64(S.reset + (size_t)r * S.ld_reset + i, kSent);
+        }
+        t = __shfl_sync(0xffffffffu, tn, 0);
+    }
+}
+
+// dst[r][i] = src[r][i]; src[r][i] = sentinel (moves a vector into or out of
+// the sentinel-managed buffers for the L-only / U-only entry points)
+__global__ void solve_move_kernel(double *src, long long ld_src, double *dst, long long ld_dst,
+                                  i32 n, i32 nrhs) {
+    const long long total = (long long)n * nrhs;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (long long)gridDim.x * blockDim.x) {
+        const long long r = k / n, i = k % n;
+        dst[r * ld_dst + i] = src[r * ld_src + i];
+        src[r * ld_src + i] = __longlong_as_double((long long)kSent);
+    }
+}
+
+__global__ void fill_sentinel_kernel(double *p, long long m) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (long long)gridDim.x * blockDim.x)
+        p[k] = __longlong_as_double((long long)kSent);
+}
+
 __global__ void zero_pivot_kernel(const double *v, const i32 *diag_pos, i32 n, int *fail) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
         if (v[diag_pos[j]] == 0.0) atomicMax(fail, j);
@@ -1442,6 +1601,11 @@ struct glu_handle {
     unsigned long long *fail = nullptr;
     unsigned int *bar = nullptr;
     int *ifail = nullptr;
+    // dataflow solves: sentinel-managed y buffer, [ticket, err] words
+    double *solve_y = nullptr;
+    i64 solve_y_cap = 0;
+    unsigned *sctl = nullptr;
+    int solve_mode = 0;  // 0 dataflow, 1 level-synchronous (grid barrier per level)
     unsigned long long *level_ns = nullptr;
     std::vector<i64> level_item_ptr_h;
     unsigned long long *trace = nullptr;
@@ -1633,13 +1797,15 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
 #undef UP
     if (cudaMalloc((void **)&h->fail, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc((void **)&h->bar, sizeof(unsigned int)) != cudaSuccess ||
-        cudaMalloc((void **)&h->ifail, sizeof(int)) != cudaSuccess) {
+        cudaMalloc((void **)&h->ifail, sizeof(int)) != cudaSuccess ||
+        cudaMalloc((void **)&h->sctl, 2 * sizeof(unsigned)) != cudaSuccess) {
         glu::set_error("cudaMalloc(scratch)"); return fail(GLU_ECUDA);
     }
     h->grid = std::min({coop_grid((const void *)factor_kernel<4, 1>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)factor_kernel<2, 2>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)factor_kernel<2, 1>, h->sm_count, kFactorDynSmem),
-                        coop_grid((const void *)solve_kernel, h->sm_count)});
+                        coop_grid((const void *)solve_kernel, h->sm_count),
+                        coop_grid((const void *)solve_df_kernel, h->sm_count)});
     if (h->grid <= 0) { glu::set_error("persistent kernel cannot be co-resident"); return fail(GLU_ECUDA); }
     *out = h;
     return GLU_OK;
@@ -1650,7 +1816,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->solve_y, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -1703,6 +1869,9 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             for (auto &e : h->kev) GLU_CUDA(cudaEventCreate(&e));
             return GLU_OK;
         }
+        case 9:  // solves: 0 dataflow (default), 1 level-synchronous
+            h->solve_mode = value != 0 ? 1 : 0;
+            return GLU_OK;
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
             return GLU_OK;
@@ -2009,8 +2178,8 @@ extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const dou
     return batch_status(h, batch, fail_cols, s);
 }
 
-static int64_t launch_solve(glu_handle *h, const double *lu, double *x, bool upper, cudaStream_t s,
-                            int nrhs = 1, i64 ldx = 0) {
+static int64_t launch_solve_level(glu_handle *h, const double *lu, double *x, bool upper,
+                                  cudaStream_t s, int nrhs, i64 ldx) {
     SolveParams S;
     S.v = lu;
     S.x = x;
@@ -2024,11 +2193,91 @@ static int64_t launch_solve(glu_handle *h, const double *lu, double *x, bool upp
     S.n_levels = (i32)(upper ? h->u_levels : h->l_levels);
     S.bar = h->bar;
     S.nrhs = nrhs;
-    S.ldx = ldx > 0 ? ldx : h->n;
+    S.ldx = ldx;
     GLU_CUDA(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int), s));
     void *args[] = {&S};
     GLU_CUDA(cudaLaunchCooperativeKernel((const void *)solve_kernel, dim3(h->grid), dim3(kThreads),
                                          args, 0, s));
+    return GLU_OK;
+}
+
+// y scratch of the dataflow solves, all-sentinel between calls
+static int64_t ensure_solve_y(glu_handle *h, int nrhs, cudaStream_t s) {
+    const i64 need = std::max<i64>(h->n, 1) * nrhs;
+    if (need <= h->solve_y_cap) return GLU_OK;
+    GLU_CUDA(cudaStreamSynchronize(s));
+    if (h->solve_y) cudaFree(h->solve_y);
+    h->solve_y = nullptr;
+    h->solve_y_cap = 0;
+    GLU_CUDA(cudaMalloc((void **)&h->solve_y, sizeof(double) * need));
+    fill_sentinel_kernel<<<h->sm_count * 4, 256, 0, s>>>(h->solve_y, need);
+    GLU_CUDA(cudaGetLastError());
+    h->solve_y_cap = need;
+    return GLU_OK;
+}
+
+static int64_t launch_solve_df(glu_handle *h, const double *lu, double *x, bool upper,
+                               cudaStream_t s, int nrhs, i64 ldx) {
+    SolveDfParams S;
+    S.v = lu;
+    S.upper = upper ? 1 : 0;
+    if (upper) {
+        S.in = h->solve_y; S.ld_in = h->n;
+        S.out = x; S.ld_out = ldx;
+        S.reset = h->solve_y; S.ld_reset = h->n;
+    } else {
+        S.in = x; S.ld_in = ldx;
+        S.out = h->solve_y; S.ld_out = h->n;
+        S.reset = x; S.ld_reset = ldx;
+    }
+    S.rows = upper ? h->u_rows : h->l_rows;
+    S.ent_ptr = upper ? h->u_ptr : h->l_ptr;
+    S.ent_col = upper ? h->u_col : h->l_col;
+    S.ent_slot = upper ? h->u_slot : h->l_slot;
+    S.diag_pos = h->diag_pos;
+    S.n = (i32)h->n;
+    S.nrhs = nrhs;
+    S.ticket = h->sctl;
+    S.err = h->sctl + 1;
+    GLU_CUDA(cudaMemsetAsync(h->sctl, 0, sizeof(unsigned), s));
+    void *args[] = {&S};
+    GLU_CUDA(cudaLaunchCooperativeKernel((const void *)solve_df_kernel, dim3(h->grid), dim3(kThreads),
+                                         args, 0, s));
+    return GLU_OK;
+}
+
+// part 0 = L then U, 1 = L only, 2 = U only; x holds nrhs vectors at stride ldx.
+static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, cudaStream_t s,
+                          int nrhs = 1, i64 ldx = 0) {
+    if (ldx <= 0) ldx = h->n;
+    i64 rc;
+    if (h->solve_mode == 1 || h->n == 0) {
+        if (part != 2 && (rc = launch_solve_level(h, lu, x, false, s, nrhs, ldx)) != GLU_OK) return rc;
+        if (part != 1 && (rc = launch_solve_level(h, lu, x, true, s, nrhs, ldx)) != GLU_OK) return rc;
+        return GLU_OK;
+    }
+    if ((rc = ensure_solve_y(h, nrhs, s)) != GLU_OK) return rc;
+    GLU_CUDA(cudaMemsetAsync(h->sctl + 1, 0, sizeof(unsigned), s));
+    const int mg = h->sm_count * 4;
+    if (part == 2) {  // x (= y) into the y buffer, x to sentinel
+        solve_move_kernel<<<mg, 256, 0, s>>>(x, ldx, h->solve_y, h->n, (i32)h->n, nrhs);
+        GLU_CUDA(cudaGetLastError());
+    }
+    if (part != 2 && (rc = launch_solve_df(h, lu, x, false, s, nrhs, ldx)) != GLU_OK) return rc;
+    if (part != 1 && (rc = launch_solve_df(h, lu, x, true, s, nrhs, ldx)) != GLU_OK) return rc;
+    if (part == 1) {  // y back into x, the y buffer to sentinel
+        solve_move_kernel<<<mg, 256, 0, s>>>(h->solve_y, h->n, x, ldx, (i32)h->n, nrhs);
+        GLU_CUDA(cudaGetLastError());
+    }
+    unsigned err = 0;
+    GLU_CUDA(cudaMemcpyAsync(&err, h->sctl + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    GLU_CUDA(cudaStreamSynchronize(s));
+    if (err) {
+        fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_y, h->solve_y_cap);
+        cudaStreamSynchronize(s);
+        glu::set_error("triangular solve: dependency wait exceeded the watchdog");
+        return GLU_ECUDA;
+    }
     return GLU_OK;
 }
 
@@ -2044,7 +2293,7 @@ static int64_t check_zero_pivot(glu_handle *h, const double *lu, cudaStream_t s)
 
 extern "C" int64_t glu_lower_solve_device(glu_handle *h, const double *lu, double *x, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    i64 rc = launch_solve(h, lu, x, false, s);
+    i64 rc = run_solves(h, lu, x, 1, s);
     if (rc != GLU_OK) return rc;
     GLU_CUDA(cudaStreamSynchronize(s));
     return GLU_OK;
@@ -2054,7 +2303,7 @@ extern "C" int64_t glu_upper_solve_device(glu_handle *h, const double *lu, doubl
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = check_zero_pivot(h, lu, s);
     if (rc != GLU_OK) return rc;
-    rc = launch_solve(h, lu, x, true, s);
+    rc = run_solves(h, lu, x, 2, s);
     if (rc != GLU_OK) return rc;
     GLU_CUDA(cudaStreamSynchronize(s));
     return GLU_OK;
@@ -2064,8 +2313,7 @@ extern "C" int64_t glu_solve_device(glu_handle *h, const double *lu, double *x, 
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = check_zero_pivot(h, lu, s);
     if (rc != GLU_OK) return rc;
-    if ((rc = launch_solve(h, lu, x, false, s)) != GLU_OK) return rc;
-    if ((rc = launch_solve(h, lu, x, true, s)) != GLU_OK) return rc;
+    if ((rc = run_solves(h, lu, x, 0, s)) != GLU_OK) return rc;
     GLU_CUDA(cudaStreamSynchronize(s));
     return GLU_OK;
 }
@@ -2091,8 +2339,7 @@ extern "C" int64_t glu_solve_multi_device(glu_handle *h, const double *lu, doubl
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc;
     if (part != 1 && (rc = check_zero_pivot(h, lu, s)) != GLU_OK) return rc;
-    if (part != 2 && (rc = launch_solve(h, lu, x, false, s, (int)nrhs, ldx)) != GLU_OK) return rc;
-    if (part != 1 && (rc = launch_solve(h, lu, x, true, s, (int)nrhs, ldx)) != GLU_OK) return rc;
+    if ((rc = run_solves(h, lu, x, (int)part, s, (int)nrhs, ldx)) != GLU_OK) return rc;
     GLU_CUDA(cudaStreamSynchronize(s));
     return GLU_OK;
 }

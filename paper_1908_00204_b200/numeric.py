@@ -512,8 +512,8 @@ def _solve(lu: LuFactors, b: np.ndarray, part: str) -> np.ndarray:
 
 
 def solve_many(lu: LuFactors, b: np.ndarray) -> np.ndarray:
-    """Solve A X = B for the columns of B ([n, k]) in one pair of level-
-    scheduled launches; column j of the result is bitwise
+    """Solve A X = B for the columns of B ([n, k]) in one pair of dataflow
+    launches; column j of the result is bitwise
     solve(lu, B[:, j])."""
     import torch
 

@@ -243,3 +243,56 @@ def test_solve_many_matches_single_solves():
     X = glu.solve_many(lu, B)
     for j in range(B.shape[1]):
         assert np.array_equal(X[:, j], glu.solve(lu, B[:, j]))
+
+
+def _solve_factorizer(lu):
+    return glu.get_factorizer(lu.pattern, glu.numeric._relaxed_levels(lu.pattern), 0)
+
+
+@pytest.mark.parametrize("mode", [0, 1])  # 0 dataflow (default), 1 level-synchronous
+def test_solve_modes_interleaved_bitwise(mode):
+    """Both solve kernels, every entry point, interleaved in an order that
+    exercises the dataflow solve's sentinel buffer hand-over (L-only leaves
+    it via a move, U-only enters it via one)."""
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a)
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
+    fz = _solve_factorizer(lu)
+    fz.set_option(9, mode)
+    try:
+        pat = orc.Pattern.from_fp(fp)
+        rng = np.random.default_rng(11)
+        for step in range(3):
+            b = rng.standard_normal(a.n)
+            b[rng.integers(0, a.n, 50)] = 0.0
+            yr = orc.lower_solve(pat, lu.values, b)
+            xr, bad = orc.upper_solve(pat, lu.values, yr)
+            assert bad == -1
+            assert np.array_equal(glu.lower_solve(lu, b), yr), step
+            assert np.array_equal(glu.solve(lu, b), xr), step
+            assert np.array_equal(glu.upper_solve(lu, yr), xr), step
+            B = np.stack([b, -b, np.zeros(a.n)], axis=1)
+            X = glu.solve_many(lu, B)
+            assert np.array_equal(X[:, 0], xr) and np.array_equal(X[:, 1], glu.solve(lu, -b))
+            assert not X[:, 2].any()
+    finally:
+        fz.set_option(9, 0)
+
+
+def test_solve_rhs_carrying_the_sentinel_pattern():
+    """The dataflow solve marks unfinished unknowns with one signalling-NaN
+    bit pattern; an input carrying exactly that pattern must neither hang nor
+    poison the next solve (it comes back quieted, still a NaN)."""
+    a = glu.to_csc(glu.Triplets(3, 3, [0, 1, 2, 1], [0, 1, 2, 0], [2.0, 4.0, 8.0, 1.0]))
+    fp = glu.symbolic_fillin(a.pattern)
+    s = glu.levelize(glu.detect_relaxed(fp))
+    plans = glu.plan_schedule(s, glu.level_stats(fp, s), a.n, glu.ResourceModel())
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
+    b = np.array([0.0, 1.0, 1.0])
+    b.view(np.uint64)[0] = np.uint64(0x7FF4DEAD5EB17A11)
+    y = glu.lower_solve(lu, b)
+    assert np.isnan(y[0]) and np.isnan(y[1]) and y[2] == 1.0
+    x = glu.solve(lu, np.array([2.0, 5.0, 8.0]))
+    assert np.array_equal(x, [1.0, 1.0, 1.0])

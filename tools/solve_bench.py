@@ -1,6 +1,6 @@
 """Triangular-solve timing (level-scheduled solve_kernel), cfg2: one and
 several right-hand sides, device-resident factors."""
-import sys, json, pathlib, ctypes
+import sys, os, json, pathlib, ctypes
 import numpy as np
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
@@ -14,12 +14,14 @@ fp = glu.symbolic_fillin(a.pattern)
 s = glu.levelize(glu.detect_relaxed(fp))
 fz = glu.get_factorizer(fp, s.level_of, 0)
 fz.set_input(a.col_ptr, a.row_idx)
+mode = int(os.environ.get("GLU_SOLVE_MODE", "0"))  # 0 dataflow, 1 level-synchronous
+fz.set_option(9, mode)
 lu, rc = fz.factor_host(a.values, 1e-14)
 assert rc == -1
 dev = torch.device("cuda", 0)
 lu_d = torch.from_numpy(lu).to(dev)
 st = torch.cuda.current_stream()
-out = {"config": cfg, "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
+out = {"config": cfg, "solve_mode": ["dataflow", "level-synchronous"][mode], "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
        "usolve_levels": fz.handle_info["usolve_levels"]}
 for k in (1, 8, 32):
     x = torch.randn((k, a.n), dtype=torch.float64, device=dev)
