@@ -1411,6 +1411,8 @@ struct SolveDfParams {
     i32 n;
     i32 upper;
     i32 nrhs;
+    i32 tblock;           // tasks per ticket grab; 0 = static round-robin over the warps
+    i32 in_il, reset_il;  // multi-RHS kernel: in / reset interleaved (out always is)
     unsigned int *ticket;
     unsigned int *err;
 };
@@ -1429,12 +1431,20 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
     __shared__ int icol[kWarps][kSolveRing][32], islot[kWarps][kSolveRing][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned total = (unsigned)S.n * (unsigned)S.nrhs;
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(S.ticket, 1u);
-    t = __shfl_sync(0xffffffffu, t, 0);
+    const unsigned nw = gridDim.x * kWarps;
+    const unsigned tb = S.tblock > 0 ? (unsigned)S.tblock : 1u;
+    // tasks [t, t_end): a block of tb tickets (dynamic) or one task (static)
+    unsigned t = 0, t_end = 0;
+    if (S.tblock > 0) {
+        if (lane == 0) t = atomicAdd(S.ticket, tb);
+        t = __shfl_sync(0xffffffffu, t, 0);
+    } else {
+        t = blockIdx.x * kWarps + w;
+    }
+    t_end = t + tb;
     while (t < total) {
-        unsigned tn = 0;  // next ticket, in flight while this row runs
-        if (lane == 0) tn = atomicAdd(S.ticket, 1u);
+        unsigned tn = 0;  // next block of tickets, in flight while this block runs
+        if (S.tblock > 0 && t + 1 == t_end && lane == 0) tn = atomicAdd(S.ticket, tb);
         const int ri = (int)(t / (unsigned)S.nrhs), r = (int)(t % (unsigned)S.nrhs);
         const int i = __ldg(S.rows + ri);
         const double *Xin = S.out + (size_t)r * S.ld_out;  // rows read by this row (ready-or-sentinel)
@@ -1474,9 +1484,9 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
                         const bool pend = live && xa == kSent;
                         if (!__any_sync(0xffffffffu, pend)) break;
                         if (pend) xa = ld_relaxed_u64(Xin + c);
-                        if (globaltimer() - t0 > kWatchdogNs) {
+                        if (__shfl_sync(0xffffffffu, globaltimer() - t0 > kWatchdogNs, 0)) {
                             if (lane == 0) atomicExch(S.err, 1u);
-                            return;
+                            return;  // warp-uniform
                         }
                     }
                 }
@@ -1518,7 +1528,196 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
             st_relaxed_u64(S.out + (size_t)r * S.ld_out + i, bits);
             st_relaxed_u64(S.reset + (size_t)r * S.ld_reset + i, kSent);
         }
-        t = __shfl_sync(0xffffffffu, tn, 0);
+        if (S.tblock == 0) {
+            t += nw;
+        } else if (++t == t_end) {
+            t = __shfl_sync(0xffffffffu, tn, 0);
+            t_end = t + tb;
+        }
+    }
+}
+
+// Several right-hand sides, on interleaved vectors (group g of 32
+// right-hand sides, row c, lane l at ((g * n + c) * 32 + l)).  The host
+// builds a level-ordered task list per k: a short row is ONE task per group
+// of 32 right-hand sides -- lane l owns right-hand side 32g + l and runs its
+// own chain, the row's indices and values are loaded once per chunk and
+// shared through shared memory; a long row (more than kSolveLongRow entries,
+// where that chain's per-chunk load latency would sit on the critical path)
+// is one task PER right-hand side in the single-RHS form (lanes over
+// entries, operands one chunk ahead).  Either way every column keeps the
+// reference's per-element order: bitwise the single solve.
+constexpr int kSolveLongRow = 96;
+
+struct SolveTask {
+    i32 row;
+    i32 sub;  // >= 0: one right-hand side (long row); < 0: group -sub-1 (short row)
+};
+
+__global__ void __launch_bounds__(kThreads, 1) solve_dfm_kernel(SolveDfParams S, const SolveTask *tasks,
+                                                                unsigned n_tasks) {
+    __shared__ __align__(16) double vbuf[kWarps][32];
+    __shared__ int icol[kWarps][kSolveRing][32], islot[kWarps][kSolveRing][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned nw = gridDim.x * kWarps;
+    unsigned t = 0;
+    if (S.tblock > 0) {
+        if (lane == 0) t = atomicAdd(S.ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+    } else {
+        t = blockIdx.x * kWarps + w;
+    }
+    while (t < n_tasks) {
+        unsigned tn = 0;
+        if (S.tblock > 0 && lane == 0) tn = atomicAdd(S.ticket, 1u);
+        const SolveTask tk = tasks[t];
+        const int i = tk.row;
+        const bool per_rhs = tk.sub >= 0;
+        const int grp = per_rhs ? (tk.sub >> 5) : (-tk.sub - 1);
+        // this thread's right-hand side: the task's one (long row) or lane's (short row)
+        const int r = per_rhs ? tk.sub : grp * 32 + lane;
+        const int rl = r & 31;  // its lane within the interleaved group
+        const bool active = r < S.nrhs;
+        const double *Xg = S.out + (size_t)grp * S.n * 32 + rl;  // row c at Xg[c * 32]
+        const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
+        const size_t own = ((size_t)grp * S.n + i) * 32 + rl;
+        double acc = 0.0;
+        if (active && (!per_rhs || lane == 0))
+            acc = ldv(S.in_il ? S.in + own : S.in + (size_t)r * S.ld_in + i);
+        const int ne = e1 - e0, ng = (ne + 31) >> 5;
+        auto ent = [&](int k) { return S.upper ? (e1 - 1 - k) : (e0 + k); };
+        auto issue_idx = [&](int g) {
+            const int k = 32 * g + lane;
+            const int e = ent(min(k, ne - 1));
+            cp_async4(&icol[w][g % kSolveRing][lane], S.ent_col + e, k < ne);
+            cp_async4(&islot[w][g % kSolveRing][lane], S.ent_slot + e, k < ne);
+            cp_async_commit();
+        };
+        bool dead = false;
+        if (ne > 0) {
+#pragma unroll
+            for (int g = 0; g < kSolveRing; ++g) issue_idx(g);
+            if (per_rhs) {
+                // lanes over entries, operands one chunk ahead, lane 0 chains
+                unsigned long long xa = 0;
+                double va = 0.0;
+                cp_async_wait<kSolveRing - 1>();
+                __syncwarp();
+                if (lane < ne) {
+                    xa = ld_relaxed_u64(Xg + (size_t)icol[w][0][lane] * 32);
+                    va = ldv(S.v + islot[w][0][lane]);
+                }
+                for (int g = 0; g < ng && !dead; ++g) {
+                    unsigned long long xb = 0;
+                    double vb = 0.0;
+                    cp_async_wait<kSolveRing - 2>();
+                    __syncwarp();
+                    const bool live = 32 * g + lane < ne;
+                    if (__any_sync(0xffffffffu, live && xa == kSent)) {
+                        const unsigned long long t0 = globaltimer();
+                        const int c = icol[w][g % kSolveRing][lane];
+                        while (true) {
+                            const bool pend = live && xa == kSent;
+                            if (!__any_sync(0xffffffffu, pend)) break;
+                            if (pend) xa = ld_relaxed_u64(Xg + (size_t)c * 32);
+                            if (__shfl_sync(0xffffffffu, globaltimer() - t0 > kWatchdogNs, 0)) {
+                                dead = true;
+                                break;
+                            }
+                        }
+                    }
+                    if (32 * (g + 1) + lane < ne) {
+                        xb = ld_relaxed_u64(Xg + (size_t)icol[w][(g + 1) % kSolveRing][lane] * 32);
+                        vb = ldv(S.v + islot[w][(g + 1) % kSolveRing][lane]);
+                    }
+                    __syncwarp();
+                    issue_idx(g + kSolveRing);
+                    const double x = __longlong_as_double((long long)xa);
+                    const bool use = live && (S.upper ? true : (x != 0.0));
+                    vbuf[w][lane] = use ? __dmul_rn(va, x) : 0.0;
+                    __syncwarp();
+                    if (lane == 0) {
+                        const double2 *pb = reinterpret_cast<const double2 *>(vbuf[w]);
+                        const int cnt = min(32, ne - 32 * g);
+                        if (cnt == 32) {
+#pragma unroll
+                            for (int s2 = 0; s2 < 16; ++s2) {
+                                const double2 p2 = pb[s2];
+                                acc = __dsub_rn(acc, p2.x);
+                                acc = __dsub_rn(acc, p2.y);
+                            }
+                        } else {
+                            for (int s1 = 0; s1 < cnt; ++s1) acc = __dsub_rn(acc, vbuf[w][s1]);
+                        }
+                    }
+                    __syncwarp();
+                    xa = xb;
+                    va = vb;
+                }
+            } else {
+                // lanes over right-hand sides
+                for (int g = 0; g < ng && !dead; ++g) {
+                    cp_async_wait<kSolveRing - 1>();
+                    __syncwarp();
+                    const int sl = g % kSolveRing;
+                    const int cnt = min(32, ne - 32 * g);
+                    vbuf[w][lane] = lane < cnt ? ldv(S.v + islot[w][sl][lane]) : 0.0;
+                    unsigned long long xs[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        xs[e] = (active && e < cnt) ? ld_relaxed_u64(Xg + (size_t)icol[w][sl][e] * 32)
+                                                    : 0ull;
+                    __syncwarp();
+                    bool pend = false;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) pend |= xs[e] == kSent;
+                    if (__any_sync(0xffffffffu, pend)) {  // some inputs not done yet
+                        const unsigned long long t0 = globaltimer();
+                        while (true) {
+                            pend = false;
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (xs[e] == kSent) {
+                                    xs[e] = ld_relaxed_u64(Xg + (size_t)icol[w][sl][e] * 32);
+                                    pend = true;
+                                }
+                            if (!__any_sync(0xffffffffu, pend)) break;
+                            if (__shfl_sync(0xffffffffu, globaltimer() - t0 > kWatchdogNs, 0)) {
+                                dead = true;
+                                break;
+                            }
+                        }
+                    }
+                    // products first (independent), then the ordered chain
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const double x = __longlong_as_double((long long)xs[e]);
+                        const bool use = e < cnt && (S.upper ? true : (x != 0.0));
+                        xs[e] = (unsigned long long)__double_as_longlong(use ? __dmul_rn(vbuf[w][e], x) : 0.0);
+                    }
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) acc = __dsub_rn(acc, __longlong_as_double((long long)xs[e]));
+                    __syncwarp();
+                    issue_idx(g + kSolveRing);  // refill the slot of chunk g
+                }
+            }
+            cp_async_wait<0>();
+            __syncwarp();
+        }
+        if (dead) {  // warp-uniform
+            if (lane == 0) atomicExch(S.err, 1u);
+            return;
+        }
+        if (active && (!per_rhs || lane == 0)) {
+            if (S.upper) acc = __ddiv_rn(acc, ldv(S.v + __ldg(S.diag_pos + i)));
+            unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
+            if (bits == kSent) bits |= kQuietBit;
+            st_relaxed_u64(S.out + own, bits);
+            if (S.reset)
+                st_relaxed_u64(S.reset_il ? S.reset + own : S.reset + (size_t)r * S.ld_reset + i, kSent);
+        }
+        if (S.tblock == 0) t += nw;
+        else t = __shfl_sync(0xffffffffu, tn, 0);
     }
 }
 
@@ -1532,6 +1731,25 @@ __global__ void solve_move_kernel(double *src, long long ld_src, double *dst, lo
         const long long r = k / n, i = k % n;
         dst[r * ld_dst + i] = src[r * ld_src + i];
         src[r * ld_src + i] = __longlong_as_double((long long)kSent);
+    }
+}
+
+// the same between the caller's layout (vector r at base + r * ld) and the
+// interleaved one of the multi-RHS kernel
+__device__ __forceinline__ double *vec_at(double *base, long long ld, int il, i32 n, long long r,
+                                          long long i) {
+    return il ? base + ((r >> 5) * n + i) * 32 + (r & 31) : base + r * ld + i;
+}
+
+__global__ void solve_xmove_kernel(double *src, long long ld_src, int il_src, double *dst,
+                                   long long ld_dst, int il_dst, i32 n, i32 nrhs) {
+    const long long total = (long long)n * nrhs;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (long long)gridDim.x * blockDim.x) {
+        const long long i = k / nrhs, r = k % nrhs;
+        double *ps = vec_at(src, ld_src, il_src, n, r, i);
+        *vec_at(dst, ld_dst, il_dst, n, r, i) = *ps;
+        *ps = __longlong_as_double((long long)kSent);
     }
 }
 
@@ -1606,6 +1824,16 @@ struct glu_handle {
     i64 solve_y_cap = 0;
     unsigned *sctl = nullptr;
     int solve_mode = 0;  // 0 dataflow, 1 level-synchronous (grid barrier per level)
+    int solve_tblock = 1;  // dataflow solve: tickets per grab (0 = static round-robin)
+    bool solve_multi = true;  // k > 1: lanes over right-hand sides (solve_dfm_kernel)
+    double *solve_yi = nullptr, *solve_zi = nullptr;  // interleaved y / x, sentinel between calls
+    i64 solve_il_cap = 0;
+    // multi-RHS task lists (level order; built per k)
+    std::vector<i32> l_rows_h, u_rows_h, l_ptr_h, u_ptr_h;
+    SolveTask *tasks_l = nullptr, *tasks_u = nullptr;
+    unsigned n_tasks_l = 0, n_tasks_u = 0;
+    int tasks_k = 0;
+    int solve_long_row = kSolveLongRow;
     unsigned long long *level_ns = nullptr;
     std::vector<i64> level_item_ptr_h;
     unsigned long long *trace = nullptr;
@@ -1794,6 +2022,8 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     solve_levels(n, up_, uc, true, ulp, urows, h->u_levels);
     UP(h->l_ptr, lp); UP(h->l_col, lc); UP(h->l_slot, ls); UP(h->l_lvl_ptr, llp); UP(h->l_rows, lrows);
     UP(h->u_ptr, up_); UP(h->u_col, uc); UP(h->u_slot, us); UP(h->u_lvl_ptr, ulp); UP(h->u_rows, urows);
+    h->l_rows_h = std::move(lrows); h->u_rows_h = std::move(urows);
+    h->l_ptr_h = std::move(lp); h->u_ptr_h = std::move(up_);
 #undef UP
     if (cudaMalloc((void **)&h->fail, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc((void **)&h->bar, sizeof(unsigned int)) != cudaSuccess ||
@@ -1805,7 +2035,8 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
                         coop_grid((const void *)factor_kernel<2, 2>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)factor_kernel<2, 1>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)solve_kernel, h->sm_count),
-                        coop_grid((const void *)solve_df_kernel, h->sm_count)});
+                        coop_grid((const void *)solve_df_kernel, h->sm_count),
+                        coop_grid((const void *)solve_dfm_kernel, h->sm_count)});
     if (h->grid <= 0) { glu::set_error("persistent kernel cannot be co-resident"); return fail(GLU_ECUDA); }
     *out = h;
     return GLU_OK;
@@ -1816,7 +2047,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->solve_y, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -1871,6 +2102,16 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
         }
         case 9:  // solves: 0 dataflow (default), 1 level-synchronous
             h->solve_mode = value != 0 ? 1 : 0;
+            return GLU_OK;
+        case 11:  // tuning: k > 1 right-hand sides, 1 lanes over right-hand sides, 0 one warp each
+            h->solve_multi = value != 0;
+            return GLU_OK;
+        case 12:  // tuning: k > 1 solves, rows longer than this run one task per right-hand side
+            h->solve_long_row = (int)std::max<int64_t>(0, std::min<int64_t>(value, 1 << 30));
+            h->tasks_k = 0;  // rebuild the task lists
+            return GLU_OK;
+        case 10:  // tuning: dataflow-solve tasks per ticket grab (0 = static round-robin)
+            h->solve_tblock = (int)std::max<int64_t>(0, std::min<int64_t>(value, 64));
             return GLU_OK;
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
@@ -2216,11 +2457,102 @@ static int64_t ensure_solve_y(glu_handle *h, int nrhs, cudaStream_t s) {
     return GLU_OK;
 }
 
+static int64_t ensure_solve_il(glu_handle *h, int nrhs, cudaStream_t s) {
+    const i64 need = std::max<i64>(h->n, 1) * (i64)((nrhs + 31) / 32) * 32;
+    if (need <= h->solve_il_cap) return GLU_OK;
+    GLU_CUDA(cudaStreamSynchronize(s));
+    for (double **p : {&h->solve_yi, &h->solve_zi}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    h->solve_il_cap = 0;
+    GLU_CUDA(cudaMalloc((void **)&h->solve_yi, sizeof(double) * need));
+    GLU_CUDA(cudaMalloc((void **)&h->solve_zi, sizeof(double) * need));
+    fill_sentinel_kernel<<<h->sm_count * 4, 256, 0, s>>>(h->solve_yi, need);
+    fill_sentinel_kernel<<<h->sm_count * 4, 256, 0, s>>>(h->solve_zi, need);
+    GLU_CUDA(cudaGetLastError());
+    h->solve_il_cap = need;
+    return GLU_OK;
+}
+
+static int64_t ensure_solve_tasks(glu_handle *h, int nrhs, cudaStream_t s) {
+    if (h->tasks_k == nrhs) return GLU_OK;
+    GLU_CUDA(cudaStreamSynchronize(s));
+    for (SolveTask **p : {&h->tasks_l, &h->tasks_u}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    h->tasks_k = 0;
+    const int groups = (nrhs + 31) / 32;
+    auto build = [&](const std::vector<i32> &rows, const std::vector<i32> &ptr, SolveTask **dst,
+                     unsigned *cnt) -> int64_t {
+        std::vector<SolveTask> t;
+        t.reserve(rows.size() * groups);
+        for (i32 i : rows) {
+            if (ptr[i + 1] - ptr[i] > h->solve_long_row)
+                for (int r = 0; r < nrhs; r++) t.push_back({i, r});
+            else
+                for (int g = 0; g < groups; g++) t.push_back({i, -(g + 1)});
+        }
+        if (t.size() >= (size_t)UINT32_MAX) {
+            glu::set_error("too many solve tasks");
+            return GLU_EINVAL;
+        }
+        *cnt = (unsigned)t.size();
+        GLU_CUDA(upload(dst, t));
+        return GLU_OK;
+    };
+    i64 rc;
+    if ((rc = build(h->l_rows_h, h->l_ptr_h, &h->tasks_l, &h->n_tasks_l)) != GLU_OK) return rc;
+    if ((rc = build(h->u_rows_h, h->u_ptr_h, &h->tasks_u, &h->n_tasks_u)) != GLU_OK) return rc;
+    h->tasks_k = nrhs;
+    return GLU_OK;
+}
+
+static void solve_params_common(glu_handle *h, SolveDfParams &S, const double *lu, bool upper, int nrhs) {
+    S.v = lu;
+    S.upper = upper ? 1 : 0;
+    S.rows = upper ? h->u_rows : h->l_rows;
+    S.ent_ptr = upper ? h->u_ptr : h->l_ptr;
+    S.ent_col = upper ? h->u_col : h->l_col;
+    S.ent_slot = upper ? h->u_slot : h->l_slot;
+    S.diag_pos = h->diag_pos;
+    S.n = (i32)h->n;
+    S.nrhs = nrhs;
+    S.tblock = h->solve_tblock;
+    S.ticket = h->sctl;
+    S.err = h->sctl + 1;
+    S.in_il = S.reset_il = 0;
+}
+
+// multi-RHS pass on the interleaved buffers: L reads x (caller layout) into
+// yi; U reads yi (restoring it) into zi
+static int64_t launch_solve_dfm(glu_handle *h, const double *lu, double *x, bool upper,
+                                cudaStream_t s, int nrhs, i64 ldx) {
+    SolveDfParams S;
+    solve_params_common(h, S, lu, upper, nrhs);
+    if (upper) {
+        S.in = h->solve_yi; S.in_il = 1; S.ld_in = 0;
+        S.out = h->solve_zi; S.ld_out = 0;
+        S.reset = h->solve_yi; S.reset_il = 1; S.ld_reset = 0;
+    } else {
+        S.in = x; S.ld_in = ldx;
+        S.out = h->solve_yi; S.ld_out = 0;
+        S.reset = nullptr; S.ld_reset = 0;
+    }
+    const SolveTask *tasks = upper ? h->tasks_u : h->tasks_l;
+    unsigned n_tasks = upper ? h->n_tasks_u : h->n_tasks_l;
+    GLU_CUDA(cudaMemsetAsync(h->sctl, 0, sizeof(unsigned), s));
+    void *args[] = {&S, &tasks, &n_tasks};
+    GLU_CUDA(cudaLaunchCooperativeKernel((const void *)solve_dfm_kernel, dim3(h->grid), dim3(kThreads),
+                                         args, 0, s));
+    return GLU_OK;
+}
+
 static int64_t launch_solve_df(glu_handle *h, const double *lu, double *x, bool upper,
                                cudaStream_t s, int nrhs, i64 ldx) {
     SolveDfParams S;
-    S.v = lu;
-    S.upper = upper ? 1 : 0;
+    solve_params_common(h, S, lu, upper, nrhs);
     if (upper) {
         S.in = h->solve_y; S.ld_in = h->n;
         S.out = x; S.ld_out = ldx;
@@ -2230,15 +2562,6 @@ static int64_t launch_solve_df(glu_handle *h, const double *lu, double *x, bool 
         S.out = h->solve_y; S.ld_out = h->n;
         S.reset = x; S.ld_reset = ldx;
     }
-    S.rows = upper ? h->u_rows : h->l_rows;
-    S.ent_ptr = upper ? h->u_ptr : h->l_ptr;
-    S.ent_col = upper ? h->u_col : h->l_col;
-    S.ent_slot = upper ? h->u_slot : h->l_slot;
-    S.diag_pos = h->diag_pos;
-    S.n = (i32)h->n;
-    S.nrhs = nrhs;
-    S.ticket = h->sctl;
-    S.err = h->sctl + 1;
     GLU_CUDA(cudaMemsetAsync(h->sctl, 0, sizeof(unsigned), s));
     void *args[] = {&S};
     GLU_CUDA(cudaLaunchCooperativeKernel((const void *)solve_df_kernel, dim3(h->grid), dim3(kThreads),
@@ -2256,9 +2579,23 @@ static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, 
         if (part != 1 && (rc = launch_solve_level(h, lu, x, true, s, nrhs, ldx)) != GLU_OK) return rc;
         return GLU_OK;
     }
-    if ((rc = ensure_solve_y(h, nrhs, s)) != GLU_OK) return rc;
-    GLU_CUDA(cudaMemsetAsync(h->sctl + 1, 0, sizeof(unsigned), s));
     const int mg = h->sm_count * 4;
+    GLU_CUDA(cudaMemsetAsync(h->sctl + 1, 0, sizeof(unsigned), s));
+    if (nrhs > 1 && h->solve_multi) {
+        if ((rc = ensure_solve_il(h, nrhs, s)) != GLU_OK) return rc;
+        if ((rc = ensure_solve_tasks(h, nrhs, s)) != GLU_OK) return rc;
+        const i32 n32 = (i32)h->n;
+        if (part == 2) {  // y (caller layout) -> yi
+            solve_xmove_kernel<<<mg, 256, 0, s>>>(x, ldx, 0, h->solve_yi, 0, 1, n32, nrhs);
+            GLU_CUDA(cudaGetLastError());
+        }
+        if (part != 2 && (rc = launch_solve_dfm(h, lu, x, false, s, nrhs, ldx)) != GLU_OK) return rc;
+        if (part != 1 && (rc = launch_solve_dfm(h, lu, x, true, s, nrhs, ldx)) != GLU_OK) return rc;
+        double *res = part == 1 ? h->solve_yi : h->solve_zi;  // result -> x, buffer -> sentinel
+        solve_xmove_kernel<<<mg, 256, 0, s>>>(res, 0, 1, x, ldx, 0, n32, nrhs);
+        GLU_CUDA(cudaGetLastError());
+    } else {
+    if ((rc = ensure_solve_y(h, nrhs, s)) != GLU_OK) return rc;
     if (part == 2) {  // x (= y) into the y buffer, x to sentinel
         solve_move_kernel<<<mg, 256, 0, s>>>(x, ldx, h->solve_y, h->n, (i32)h->n, nrhs);
         GLU_CUDA(cudaGetLastError());
@@ -2269,11 +2606,14 @@ static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, 
         solve_move_kernel<<<mg, 256, 0, s>>>(h->solve_y, h->n, x, ldx, (i32)h->n, nrhs);
         GLU_CUDA(cudaGetLastError());
     }
+    }
     unsigned err = 0;
     GLU_CUDA(cudaMemcpyAsync(&err, h->sctl + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     GLU_CUDA(cudaStreamSynchronize(s));
     if (err) {
-        fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_y, h->solve_y_cap);
+        if (h->solve_y) fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_y, h->solve_y_cap);
+        if (h->solve_yi) fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_yi, h->solve_il_cap);
+        if (h->solve_zi) fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_zi, h->solve_il_cap);
         cudaStreamSynchronize(s);
         glu::set_error("triangular solve: dependency wait exceeded the watchdog");
         return GLU_ECUDA;

@@ -296,3 +296,42 @@ def test_solve_rhs_carrying_the_sentinel_pattern():
     assert np.isnan(y[0]) and np.isnan(y[1]) and y[2] == 1.0
     x = glu.solve(lu, np.array([2.0, 5.0, 8.0]))
     assert np.array_equal(x, [1.0, 1.0, 1.0])
+
+
+@pytest.mark.parametrize("multi", [1, 0])  # 1: lanes over right-hand sides, 0: one warp each
+def test_solve_multi_parts_and_groups(multi):
+    """k > 32 right-hand sides (two lane groups, a ragged last one) through
+    glu_solve_multi_device for L then U, L only and U only, each column
+    bitwise the oracle's single solve."""
+    import ctypes
+
+    import torch
+    from paper_1908_00204_b200 import _lib, synthetic
+
+    a = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a)
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
+    fz = _solve_factorizer(lu)
+    fz.set_option(11, multi)
+    pat = orc.Pattern.from_fp(fp)
+    k, ld = 41, a.n + 7
+    B = np.random.default_rng(5).standard_normal((k, a.n))
+    B[3] = 0.0
+    Y = np.stack([orc.lower_solve(pat, lu.values, b) for b in B])
+    X = np.stack([orc.upper_solve(pat, lu.values, y)[0] for y in Y])
+    dev = torch.device("cuda", 0)
+    lu_d = torch.from_numpy(lu.values).to(dev)
+    try:
+        for part, src, want in ((0, B, X), (1, B, Y), (2, Y, X), (0, B, X)):
+            buf = torch.full((k, ld), 7.0, dtype=torch.float64, device=dev)
+            buf[:, : a.n] = torch.from_numpy(src).to(dev)
+            st = torch.cuda.current_stream()
+            rc = _lib.lib.glu_solve_multi_device(fz.handle, glu.numeric._dptr(lu_d),
+                                                 glu.numeric._dptr(buf), k, ld, part,
+                                                 ctypes.c_void_p(st.cuda_stream))
+            assert rc == -1, _lib.lib.glu_last_error()
+            out = buf.cpu().numpy()
+            assert np.array_equal(out[:, : a.n], want), part
+            assert (out[:, a.n:] == 7.0).all()  # padding untouched
+    finally:
+        fz.set_option(11, 1)

@@ -16,12 +16,20 @@ fz = glu.get_factorizer(fp, s.level_of, 0)
 fz.set_input(a.col_ptr, a.row_idx)
 mode = int(os.environ.get("GLU_SOLVE_MODE", "0"))  # 0 dataflow, 1 level-synchronous
 fz.set_option(9, mode)
+tblock = int(os.environ.get("GLU_SOLVE_TBLOCK", "-1"))
+if tblock >= 0:
+    fz.set_option(10, tblock)
+multi = int(os.environ.get("GLU_SOLVE_MULTI", "1"))
+fz.set_option(11, multi)
+long_row = int(os.environ.get("GLU_SOLVE_LONG", "-1"))
+if long_row >= 0:
+    fz.set_option(12, long_row)
 lu, rc = fz.factor_host(a.values, 1e-14)
 assert rc == -1
 dev = torch.device("cuda", 0)
 lu_d = torch.from_numpy(lu).to(dev)
 st = torch.cuda.current_stream()
-out = {"config": cfg, "solve_mode": ["dataflow", "level-synchronous"][mode], "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
+out = {"config": cfg, "solve_mode": ["dataflow", "level-synchronous"][mode], "tblock": tblock, "multi": multi, "long_row": long_row, "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
        "usolve_levels": fz.handle_info["usolve_levels"]}
 for k in (1, 8, 32):
     x = torch.randn((k, a.n), dtype=torch.float64, device=dev)
