@@ -43,6 +43,8 @@ CONFIG_DESC = {
             "SuperLU MMD order",
     "cfg3": "synthetic ASIC_680k-like n=680,000 (1-D local +-40, 6 hubs x 1%), SuperLU MMD order",
     "g400": "G3-family 5-point grid 400x400 (n=160,000), geometric nested dissection",
+    "g600": "G3-family 5-point grid 600x600 (n=360,000), geometric nested dissection",
+    "g800": "G3-family 5-point grid 800x800 (n=640,000), geometric nested dissection",
 }
 
 

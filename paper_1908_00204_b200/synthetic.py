@@ -233,6 +233,8 @@ CONFIGS = {
     "cfg4": lambda: grid5(1258, seed=0),
     # G3-family data point at a size whose plan fits (cfg4's does not yet)
     "g400": lambda: grid5(400, seed=0),
+    "g600": lambda: grid5(600, seed=0),
+    "g800": lambda: grid5(800, seed=0),
 }
 
 
