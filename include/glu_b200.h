@@ -155,6 +155,12 @@ int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value);
    t_stored, 0} (%globaltimer ns) in the next factorization; read them
    with glu_trace_read (returns the record count). */
 int64_t glu_trace_read(glu_handle *h, int64_t *out, int64_t max_records);
+/* Diagnostics: glu_set_option(h, 13, 1) records %globaltimer stamps of the
+   dense-tail kernel: out[0], [1], [2], [4] = CTA 0 start, columns loaded,
+   panels done, columns stored and divided; then per panel p (8 + 6p ..): its owner observed
+   panel p-1, applied it, finished the column sweep of p, wrote p back, published p.  Returns the word count
+   copied (0 when off). */
+int64_t glu_tail_trace_read(glu_handle *h, int64_t *out, int64_t max_words);
 /* Diagnostics: glu_set_option(h, 8, n) records CUDA events (on the launch
    stream) around the factor kernel and the dense-tail kernel of the next n
    factorizations; after a synchronize, glu_kernel_times writes

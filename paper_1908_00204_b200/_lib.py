@@ -49,6 +49,7 @@ SIGNATURES = {
     "glu_tail_capacity": (_i64, []),
     "glu_plan_info": (None, [_p, _p]),
     "glu_trace_read": (_i64, [_p, _p, _i64]),
+    "glu_tail_trace_read": (_i64, [_p, _p, _i64]),
     "glu_kernel_times": (_i64, [_p, _p, _i64]),
     "glu_plan_export": (None, [_p, _p, _p, _p, _p, _p, _p]),
     "glu_plan_free": (None, [_p]),

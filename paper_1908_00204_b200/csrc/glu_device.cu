@@ -864,6 +864,9 @@ struct TailParams {
     double thresh;
     unsigned long long *fail;
     i32 fail_by_column;
+    // diagnostics (option 13): [0..7] CTA 0 phase stamps, then per panel
+    // {observed p-1, applied p-1 to it, column sweep done, written back, published} by its owner
+    unsigned long long *trace;
 };
 
 __device__ __forceinline__ bool mbit(const unsigned long long *mk, int i) {
@@ -928,6 +931,10 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     }
     __syncthreads();
     auto qglob = [&](int x) { return qtab[x]; };
+    auto stamp_t = [&](int k) {
+        if (T.trace && tid == 0) T.trace[k] = globaltimer();
+    };
+    if (c == 0) stamp_t(0);
     int nvalid = ncol;  // owned columns that exist (the last panel may be short)
     while (nvalid > 0 && qtab[nvalid - 1] >= M) --nvalid;
     for (int x = 0; x < ncol; ++x) {
@@ -950,6 +957,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         }
     }
     __syncthreads();
+    if (c == 0) stamp_t(1);
     const int ia = tid, ib = tid + nt;  // this thread's rows (m <= 2 * nt)
 
     // Owner: factor panel pp in place (its columns already hold every update
@@ -1010,6 +1018,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
                 }
             }
         }
+        stamp_t(8 + 6 * pp + 2);
 #pragma unroll
         for (int k = 0; k < kTailB; ++k) {
             if (k < bp) {
@@ -1143,8 +1152,11 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     };
     const int qmax = nvalid > 0 ? qtab[nvalid - 1] : -1;  // no panel beyond it concerns this CTA
     if (T.np > 0 && c == 0) {
+        stamp_t(8 + 1);  // panel 0: observed = applied
         factor_panel(0);
+        stamp_t(8 + 3);
         publish(0);
+        stamp_t(8 + 4);
     }
     for (int p = 0; p < T.np; ++p) {
         if (p * B > qmax) break;  // no owned column beyond this panel
@@ -1152,10 +1164,14 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         const int pn = p + 1;
         const bool own_next = pn < T.np && (pn % C) == c;
         if (own_next) {  // lookahead: the next panel first
+            stamp_t(8 + 6 * pn);
             const int xn = xloc(pn * B);
             apply_panel(p, xn, min(xn + B, ncol));
+            stamp_t(8 + 6 * pn + 1);
             factor_panel(pn);
+            stamp_t(8 + 6 * pn + 3);
             publish(pn);
+            stamp_t(8 + 6 * pn + 4);
             const int xl = xn + B;
             apply_panel(p, 0, xn);
             apply_panel(p, xl, ncol);
@@ -1163,6 +1179,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
             apply_panel(p, 0, ncol);
         }
     }
+    if (c == 0) stamp_t(2);
     for (int x = 0; x < ncol; ++x) {
         const int q = qglob(x);
         if (q >= M) break;
@@ -1176,6 +1193,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     __syncthreads();
     for (int x = wid; x < ncol; x += nwarp)
         if (qglob(x) < M) divide_column_t(T, T.t0 + qglob(x), lane);
+    __syncthreads();
+    if (c == 0) stamp_t(4);
 }
 
 struct TailShape;
@@ -1834,6 +1853,7 @@ struct glu_handle {
     unsigned n_tasks_l = 0, n_tasks_u = 0;
     int tasks_k = 0;
     int solve_long_row = kSolveLongRow;
+    unsigned long long *tail_trace = nullptr;  // option 13
     unsigned long long *level_ns = nullptr;
     std::vector<i64> level_item_ptr_h;
     unsigned long long *trace = nullptr;
@@ -2047,7 +2067,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->tail_trace, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -2106,6 +2126,16 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
         case 11:  // tuning: k > 1 right-hand sides, 1 lanes over right-hand sides, 0 one warp each
             h->solve_multi = value != 0;
             return GLU_OK;
+        case 13: {  // diagnostics: tail-kernel timestamps (glu_tail_trace_read)
+            if (h->tail_trace) cudaFree(h->tail_trace);
+            h->tail_trace = nullptr;
+            if (value != 0 && h->tail.np > 0) {
+                const size_t words = 8 + 6 * (size_t)h->tail.np;
+                GLU_CUDA(cudaMalloc((void **)&h->tail_trace, sizeof(unsigned long long) * words));
+                GLU_CUDA(cudaMemset(h->tail_trace, 0, sizeof(unsigned long long) * words));
+            }
+            return GLU_OK;
+        }
         case 12:  // tuning: k > 1 solves, rows longer than this run one task per right-hand side
             h->solve_long_row = (int)std::max<int64_t>(0, std::min<int64_t>(value, 1 << 30));
             h->tasks_k = 0;  // rebuild the task lists
@@ -2132,6 +2162,14 @@ extern "C" int64_t glu_kernel_times(glu_handle *h, double *ms, int64_t max_launc
         ms[2 * k + 1] = b;
     }
     return m;
+}
+
+extern "C" int64_t glu_tail_trace_read(glu_handle *h, int64_t *out, int64_t max_words) {
+    if (!h->tail_trace) return 0;
+    const i64 words = std::min<i64>(max_words, 8 + 6 * (i64)h->tail.np);
+    GLU_CUDA(cudaDeviceSynchronize());
+    GLU_CUDA(cudaMemcpy(out, h->tail_trace, sizeof(int64_t) * words, cudaMemcpyDeviceToHost));
+    return words;
 }
 
 extern "C" int64_t glu_trace_read(glu_handle *h, int64_t *out, int64_t max_records) {
@@ -2274,6 +2312,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         T.thresh = thresh;
         T.fail = fail;
         T.fail_by_column = h->fail_by_column ? 1 : 0;
+        T.trace = h->tail_trace;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
