@@ -415,7 +415,6 @@ __device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool 
 // values, pivots and multipliers.  The targets are staged in shared memory,
 // the MACs applied there epoch by epoch (entries of one epoch hit distinct
 // targets; only epochs are ordered), and every target written back once.
-constexpr int kR = glu::kMaxItemMacs / 32;  // entries per lane
 
 // L2 prefetch of an item's static plan data (descriptor already loaded):
 // its chunk descriptors, u8 map and target list, or the first deep refs.
@@ -1072,12 +1071,6 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         __syncthreads();
         // (B) rows below the panel, target in a register across the b sources;
         // two columns at a time so each thread carries independent chains
-        auto colB = [&](int x, double *u, unsigned &ub_out) {
-            double *cq = cols + (size_t)x * T.mpad;
-            ub_out = mbits(mk + x * T.mw, s0, bp);
-#pragma unroll
-            for (int k = 0; k < kTailB; ++k) u[k] = k < bp ? cq[s0 + k] : 0.0;
-        };
         int x = xa;
         xb = min(xb, nvalid);
         while (x < xb && qglob(x) < s1) ++x;  // owned columns beyond the panel are contiguous
@@ -1126,7 +1119,6 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
                 cq[ib] = t;
             }
         }
-        (void)colB;
         __syncthreads();
     };
 
