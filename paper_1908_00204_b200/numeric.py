@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import os
 import threading
 import weakref
 from dataclasses import dataclass, field
@@ -164,6 +165,8 @@ class Factorizer:
         self._finalizer = weakref.finalize(self, _lib.lib.glu_destroy, h)
         self._input_key = None
         self._lock = threading.Lock()
+        if "GLU_POLL_NS" in os.environ:  # tuning: ns between dependency polls (option 6)
+            self.set_option(6, int(os.environ["GLU_POLL_NS"]))
         info = np.zeros(12, dtype=np.int64)
         _lib.lib.glu_handle_info(h, _lib.ptr(info))
         self.handle_info = dict(zip(("n", "nnz", "levels", "items", "chunks", "macs",
