@@ -335,3 +335,73 @@ def test_solve_multi_parts_and_groups(multi):
             assert (out[:, a.n:] == 7.0).all()  # padding untouched
     finally:
         fz.set_option(11, 1)
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "g200"])
+@pytest.mark.parametrize("det", [True, False])
+def test_full_size_bitwise_vs_oracle(cfg, det):
+    """cfg3 (the deep, stream-mode schedule: 680k columns, 912 levels) and a
+    G3-family grid (wide levels, deep hub items, the cluster dense tail) at
+    full size, both contracts, against the C restatement of the reference."""
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make(cfg) if cfg in synthetic.CONFIGS else synthetic.grid5(200, seed=0)
+    fp, s, plans = _analyze(a, glu.B200_RESOURCE)
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions(deterministic=det))
+    assert np.array_equal(lu.values, _oracle_values(a, fp, s, det))
+    b = np.random.default_rng(1).standard_normal(a.n)
+    pat = orc.Pattern.from_fp(fp)
+    xr, bad = orc.upper_solve(pat, lu.values, orc.lower_solve(pat, lu.values, b))
+    assert bad == -1 and np.array_equal(glu.solve(lu, b), xr)
+
+
+def test_one_by_one():
+    a = glu.to_csc(glu.Triplets(1, 1, [0], [0], [5.0]))
+    fp, s, plans = _analyze(a)
+    for det in (True, False):
+        lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions(deterministic=det))
+        assert lu.values.tolist() == [5.0]
+    assert glu.solve(lu, np.array([10.0])).tolist() == [2.0]
+    z = glu.to_csc(glu.Triplets(1, 1, [0], [0], [0.0]))
+    with pytest.raises(glu.PivotError) as e:
+        glu.factor_parallel(z, fp, s, plans, glu.FactorOptions())
+    assert e.value.column == 0
+
+
+@pytest.mark.parametrize("det", [True, False])
+def test_pivot_breakdown_inside_cfg1_matches_oracle(det):
+    """Shrink two diagonals of cfg1 (a low column in level 10, a high one in
+    level 0) and raise the relative pivot threshold so both break down: the
+    reported column is the oracle's for each path's order -- the earliest
+    level's lowest column for factor_parallel (1483 here), the lowest column
+    for the sequential paths (1414)."""
+    from paper_1908_00204_b200 import synthetic
+
+    a0 = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a0)
+    cols = np.repeat(np.arange(a0.n), np.diff(a0.col_ptr))
+    lv = np.asarray(s.level_of)
+    lo = int(np.nonzero(lv >= 10)[0].min())  # a low column in a late level
+    hi = int(np.nonzero(lv == 0)[0].max())   # a high column in level 0
+    assert lo < hi
+    vals = a0.values.copy()
+    for c in (lo, hi):
+        vals[(a0.row_idx == c) & (cols == c)] *= 0.01
+    a = glu.CscMatrix(a0.n, a0.col_ptr, a0.row_idx, vals)
+    th = 0.5
+    pat = orc.Pattern.from_fp(fp)
+    lp = np.concatenate([[0], np.cumsum([len(c) for c in s.levels])])
+    v, _ = orc.scatter(pat, a.col_ptr, a.row_idx, a.values)
+    want = orc.factor_parallel(pat, v, lp, np.concatenate(s.levels),
+                               np.ones(len(s.levels), dtype=np.int64), det, th)
+    v, _ = orc.scatter(pat, a.col_ptr, a.row_idx, a.values)
+    want_seq = orc.factor_left_looking(pat, v, th)
+    assert want == hi and want_seq == lo  # the orders differ on this input
+    with pytest.raises(glu.PivotError) as e:
+        glu.factor_parallel(a, fp, s, plans,
+                            glu.FactorOptions(deterministic=det, zero_pivot_threshold=th))
+    assert e.value.column == want
+    for fn in (glu.factor_left_looking, glu.factor_right_looking_seq):
+        with pytest.raises(glu.PivotError) as e:
+            fn(a, fp, glu.FactorOptions(zero_pivot_threshold=th))
+        assert e.value.column == want_seq
