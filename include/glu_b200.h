@@ -217,6 +217,15 @@ int64_t glu_upper_solve_device(glu_handle *h, const double *lu, double *x, void 
    1 = L only, 2 = U only.  Each column is bitwise the single-RHS result. */
 int64_t glu_solve_multi_device(glu_handle *h, const double *lu, double *x, int64_t nrhs,
                                int64_t ldx, int32_t part, void *stream);
+/* Batch solves: nb systems on this pattern, each with its OWN factors (set b
+   at lu + b * lu_stride, e.g. the output of glu_factor_batch_device) and one
+   right-hand side (x + b * ldx, overwritten with the solution); one pair of
+   dataflow launches.  status[nb] (host) gets -1 per set, or the column whose
+   diagonal is exactly zero (the PivotError upper_solve raises, numeric.py:
+   364-373); such a set's x is unspecified.  Each solved set is bitwise
+   glu_solve_device on its factors. */
+int64_t glu_solve_batch_device(glu_handle *h, const double *lu, int64_t lu_stride, double *x,
+                               int64_t nb, int64_t ldx, int64_t *status, void *stream);
 
 /* End-to-end host-buffer calls (the reference-facing plugin boundary):
    H2D of A values, device scatter, factor, D2H of LU. */

@@ -69,6 +69,7 @@ SIGNATURES = {
     "glu_lower_solve_device": (_i64, [_p, _p, _p, _p]),
     "glu_upper_solve_device": (_i64, [_p, _p, _p, _p]),
     "glu_solve_multi_device": (_i64, [_p, _p, _p, _i64, _i64, _i32, _p]),
+    "glu_solve_batch_device": (_i64, [_p, _p, _i64, _p, _i64, _i64, _p, _p]),
     "glu_factor_host": (_i64, [_p, _p, _p, _dbl]),
     "glu_solve_host": (_i64, [_p, _p, _p, _p]),
 }

@@ -1412,6 +1412,7 @@ constexpr unsigned long long kQuietBit = 1ull << 51;
 
 struct SolveDfParams {
     const double *v;
+    long long v_stride;   // batch solves: right-hand side r uses factors v + r * v_stride
     const double *in;     // L: b (X), U: y (Y)
     double *out;          // L: y (Y), U: x (X)
     double *reset;        // L: X (set to sentinel), U: Y (restored to sentinel)
@@ -1459,6 +1460,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
         const int ri = (int)(t / (unsigned)S.nrhs), r = (int)(t % (unsigned)S.nrhs);
         const int i = __ldg(S.rows + ri);
         const double *Xin = S.out + (size_t)r * S.ld_out;  // rows read by this row (ready-or-sentinel)
+        const double *V = S.v + (size_t)r * S.v_stride;    // this task's factors
         const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
         double acc = ldv(S.in + (size_t)r * S.ld_in + i);
         const int ne = e1 - e0, ng = (ne + 31) >> 5;
@@ -1479,7 +1481,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
             __syncwarp();
             if (lane < ne) {
                 xa = ld_relaxed_u64(Xin + icol[w][0][lane]);
-                va = ldv(S.v + islot[w][0][lane]);
+                va = ldv(V + islot[w][0][lane]);
             }
             for (int g = 0; g < ng; ++g) {
                 unsigned long long xb = 0;
@@ -1503,7 +1505,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
                 }
                 if (32 * (g + 1) + lane < ne) {
                     xb = ld_relaxed_u64(Xin + icol[w][(g + 1) % kSolveRing][lane]);
-                    vb = ldv(S.v + islot[w][(g + 1) % kSolveRing][lane]);
+                    vb = ldv(V + islot[w][(g + 1) % kSolveRing][lane]);
                 }
                 __syncwarp();
                 issue_idx(g + kSolveRing);
@@ -1533,7 +1535,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
             __syncwarp();
         }
         if (lane == 0) {
-            if (S.upper) acc = __ddiv_rn(acc, ldv(S.v + __ldg(S.diag_pos + i)));
+            if (S.upper) acc = __ddiv_rn(acc, ldv(V + __ldg(S.diag_pos + i)));
             unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
             if (bits == kSent) bits |= kQuietBit;  // only an untouched input can carry it
             st_relaxed_u64(S.out + (size_t)r * S.ld_out + i, bits);
@@ -1768,6 +1770,18 @@ __global__ void fill_sentinel_kernel(double *p, long long m) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (long long)gridDim.x * blockDim.x)
         p[k] = __longlong_as_double((long long)kSent);
+}
+
+// per set: the largest column with an exactly zero diagonal (the column the
+// reference's reverse sweep stops at, _kernels.py:186-197), or -1
+__global__ void zero_pivot_batch_kernel(const double *v, long long stride, const i32 *diag_pos, i32 n,
+                                        int nb, int *fail) {
+    const long long total = (long long)n * nb;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(k / n), j = (int)(k % n);
+        if (v[(size_t)b * stride + diag_pos[j]] == 0.0) atomicMax(fail + b, j);
+    }
 }
 
 __global__ void zero_pivot_kernel(const double *v, const i32 *diag_pos, i32 n, int *fail) {
@@ -2542,6 +2556,7 @@ static int64_t ensure_solve_tasks(glu_handle *h, int nrhs, cudaStream_t s) {
 
 static void solve_params_common(glu_handle *h, SolveDfParams &S, const double *lu, bool upper, int nrhs) {
     S.v = lu;
+    S.v_stride = 0;
     S.upper = upper ? 1 : 0;
     S.rows = upper ? h->u_rows : h->l_rows;
     S.ent_ptr = upper ? h->u_ptr : h->l_ptr;
@@ -2581,9 +2596,10 @@ static int64_t launch_solve_dfm(glu_handle *h, const double *lu, double *x, bool
 }
 
 static int64_t launch_solve_df(glu_handle *h, const double *lu, double *x, bool upper,
-                               cudaStream_t s, int nrhs, i64 ldx) {
+                               cudaStream_t s, int nrhs, i64 ldx, i64 v_stride = 0) {
     SolveDfParams S;
     solve_params_common(h, S, lu, upper, nrhs);
+    S.v_stride = v_stride;
     if (upper) {
         S.in = h->solve_y; S.ld_in = h->n;
         S.out = x; S.ld_out = ldx;
@@ -2602,9 +2618,13 @@ static int64_t launch_solve_df(glu_handle *h, const double *lu, double *x, bool 
 
 // part 0 = L then U, 1 = L only, 2 = U only; x holds nrhs vectors at stride ldx.
 static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, cudaStream_t s,
-                          int nrhs = 1, i64 ldx = 0) {
+                          int nrhs = 1, i64 ldx = 0, i64 v_stride = 0) {
     if (ldx <= 0) ldx = h->n;
     i64 rc;
+    if (v_stride != 0 && h->solve_mode == 1) {
+        glu::set_error("batch solves need the dataflow solve kernel (option 9 = 0)");
+        return GLU_EINVAL;
+    }
     if (h->solve_mode == 1 || h->n == 0) {
         if (part != 2 && (rc = launch_solve_level(h, lu, x, false, s, nrhs, ldx)) != GLU_OK) return rc;
         if (part != 1 && (rc = launch_solve_level(h, lu, x, true, s, nrhs, ldx)) != GLU_OK) return rc;
@@ -2612,7 +2632,7 @@ static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, 
     }
     const int mg = h->sm_count * 4;
     GLU_CUDA(cudaMemsetAsync(h->sctl + 1, 0, sizeof(unsigned), s));
-    if (nrhs > 1 && h->solve_multi) {
+    if (nrhs > 1 && h->solve_multi && v_stride == 0) {
         if ((rc = ensure_solve_il(h, nrhs, s)) != GLU_OK) return rc;
         if ((rc = ensure_solve_tasks(h, nrhs, s)) != GLU_OK) return rc;
         const i32 n32 = (i32)h->n;
@@ -2631,8 +2651,8 @@ static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, 
         solve_move_kernel<<<mg, 256, 0, s>>>(x, ldx, h->solve_y, h->n, (i32)h->n, nrhs);
         GLU_CUDA(cudaGetLastError());
     }
-    if (part != 2 && (rc = launch_solve_df(h, lu, x, false, s, nrhs, ldx)) != GLU_OK) return rc;
-    if (part != 1 && (rc = launch_solve_df(h, lu, x, true, s, nrhs, ldx)) != GLU_OK) return rc;
+    if (part != 2 && (rc = launch_solve_df(h, lu, x, false, s, nrhs, ldx, v_stride)) != GLU_OK) return rc;
+    if (part != 1 && (rc = launch_solve_df(h, lu, x, true, s, nrhs, ldx, v_stride)) != GLU_OK) return rc;
     if (part == 1) {  // y back into x, the y buffer to sentinel
         solve_move_kernel<<<mg, 256, 0, s>>>(h->solve_y, h->n, x, ldx, (i32)h->n, nrhs);
         GLU_CUDA(cudaGetLastError());
@@ -2712,6 +2732,34 @@ extern "C" int64_t glu_solve_multi_device(glu_handle *h, const double *lu, doubl
     if (part != 1 && (rc = check_zero_pivot(h, lu, s)) != GLU_OK) return rc;
     if ((rc = run_solves(h, lu, x, (int)part, s, (int)nrhs, ldx)) != GLU_OK) return rc;
     GLU_CUDA(cudaStreamSynchronize(s));
+    return GLU_OK;
+}
+
+// Batch solves: set b's factors at lu + b * lu_stride,
+// its right-hand side / solution at x + b * ldx; one pair of dataflow
+// launches for all sets.  status[b] = -1, or the zero-diagonal column the
+// reference's upper_solve raises for that set (its x is then unspecified).
+extern "C" int64_t glu_solve_batch_device(glu_handle *h, const double *lu, int64_t lu_stride, double *x,
+                                          int64_t nb, int64_t ldx, int64_t *status, void *stream) {
+    if (nb < 0 || (nb > 0 && (ldx < h->n || lu_stride < h->nnz))) {
+        glu::set_error("bad batch solve arguments");
+        return GLU_EINVAL;
+    }
+    if (nb == 0) return GLU_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int *dfail = nullptr;
+    GLU_CUDA(cudaMallocAsync((void **)&dfail, sizeof(int) * nb, s));
+    GLU_CUDA(cudaMemsetAsync(dfail, 0xff, sizeof(int) * nb, s));  // -1
+    zero_pivot_batch_kernel<<<h->sm_count * 4, 256, 0, s>>>(lu, lu_stride, h->diag_pos, (i32)h->n,
+                                                           (int)nb, dfail);
+    GLU_CUDA(cudaGetLastError());
+    i64 rc = run_solves(h, lu, x, 0, s, (int)nb, ldx, lu_stride);
+    std::vector<int> f((size_t)nb, -1);
+    cudaMemcpyAsync(f.data(), dfail, sizeof(int) * nb, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(dfail, s);
+    GLU_CUDA(cudaStreamSynchronize(s));
+    if (rc != GLU_OK) return rc;
+    for (i64 b = 0; b < nb; b++) status[b] = f[b];
     return GLU_OK;
 }
 

@@ -540,6 +540,40 @@ def solve_many(lu: LuFactors, b: np.ndarray) -> np.ndarray:
     return out
 
 
+def solve_batch(lu: LuFactors, lu_values: np.ndarray, b: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Solve B systems on lu's pattern, each with its own factors -- row b of
+    `lu_values` ([B, nnz], e.g. refactorize_batch's output) -- and its own
+    right-hand side (row b of `b`, [B, n]), in one pair of dataflow launches
+    (the solve after each Newton / transient
+    refactorization).  Returns (x [B, n], status [B]): status[b] is -1, or
+    the column whose diagonal is exactly zero (the PivotError upper_solve
+    raises, levlu/numeric.py:364-373), x[b] then being unspecified.  Every
+    solved row is bitwise solve(LuFactors(pattern, lu_values[b]), b[b])."""
+    import torch
+
+    vals = np.ascontiguousarray(lu_values, dtype=np.float64)
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    if vals.ndim != 2 or vals.shape[1] != lu.pattern.nnz:
+        raise ValueError("lu_values must be [batch, nnz]")
+    if bb.shape != (vals.shape[0], lu.n):
+        raise ValueError("right-hand sides must be [batch, n]")
+    nb = vals.shape[0]
+    status = np.full(nb, -1, dtype=np.int64)
+    if nb == 0:
+        return bb.copy(), status
+    fz = get_factorizer(lu.pattern, _relaxed_levels(lu.pattern), _lib.CONTRACT_A)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    with fz._lock:
+        lu_d = torch.from_numpy(vals).to(dev)
+        x_d = torch.from_numpy(bb.copy()).to(dev)
+        s = torch.cuda.current_stream()
+        _lib.check(_lib.lib.glu_solve_batch_device(fz.handle, _dptr(lu_d), lu.pattern.nnz, _dptr(x_d), nb,
+                                                   lu.n, _lib.ptr(status), ctypes.c_void_p(s.cuda_stream)),
+                   "glu_solve_batch_device")
+        out = x_d.cpu().numpy()
+    return out, status
+
+
 def lower_solve(lu: LuFactors, b: np.ndarray) -> np.ndarray:
     """L y = b, implicit unit diagonal (levlu/numeric.py:354-361)."""
     return _solve(lu, b, "lower")

@@ -405,3 +405,41 @@ def test_pivot_breakdown_inside_cfg1_matches_oracle(det):
         with pytest.raises(glu.PivotError) as e:
             fn(a, fp, glu.FactorOptions(zero_pivot_threshold=th))
         assert e.value.column == want_seq
+
+
+@pytest.mark.parametrize("check_refusal", [False, True])
+def test_solve_batch_per_set_bitwise(check_refusal):
+    """refactorize_batch -> solve_batch (the Newton-loop pair): every set's
+    solution is bitwise the oracle's solve with that set's factors; a set
+    with an exactly zero diagonal reports the column upper_solve raises."""
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a)
+    lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
+    nb = 6
+    vals = np.stack([synthetic.perturb_values(a, 100 + k) for k in range(nb)])
+    L, st = glu.refactorize_batch(lu, a, vals)
+    assert (st == -1).all()
+    L = L.copy()
+    bad_col = int(np.asarray(s.level_of).argmax())
+    L[4, fp.diag_pos[bad_col]] = 0.0  # set 4: a zero diagonal
+    B = np.random.default_rng(9).standard_normal((nb, a.n))
+    B[2] = 0.0
+    if check_refusal:  # the level-synchronous kernel has no per-set factors: refused
+        fz = glu.get_factorizer(lu.pattern, glu.numeric._relaxed_levels(lu.pattern), 0)
+        fz.set_option(9, 1)
+        try:
+            with pytest.raises(Exception):
+                glu.solve_batch(lu, L, B)
+        finally:
+            fz.set_option(9, 0)
+    X, status = glu.solve_batch(lu, L, B)
+    pat = orc.Pattern.from_fp(fp)
+    for k in range(nb):
+        y = orc.lower_solve(pat, L[k], B[k])
+        xr, bad = orc.upper_solve(pat, L[k], y)
+        assert status[k] == bad, k
+        if bad == -1:
+            assert np.array_equal(X[k], xr), k
+    assert status[4] >= 0 and (status[[0, 1, 2, 3, 5]] == -1).all()

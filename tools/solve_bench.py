@@ -45,6 +45,24 @@ for k in (1, 8, 32):
     e1.record(st)
     torch.cuda.synchronize()
     out[f"nrhs{k}_ms"] = e0.elapsed_time(e1) / reps
+# batch solves: nb sets, each its own factors (replicas here) and right-hand side
+for nbs in (8, 32):
+    L = lu_d.repeat(nbs, 1).reshape(nbs, -1).contiguous()
+    X = torch.randn((nbs, a.n), dtype=torch.float64, device=dev)
+    status = np.zeros(nbs, dtype=np.int64)
+    def run():
+        rc = _lib.lib.glu_solve_batch_device(fz.handle, glu.numeric._dptr(L), L.shape[1], glu.numeric._dptr(X),
+                                             nbs, a.n, _lib.ptr(status), ctypes.c_void_p(st.cuda_stream))
+        assert rc == -1, _lib.last_error()
+    for _ in range(2):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(5):
+        run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    out[f"batch{nbs}_ms"] = e0.elapsed_time(e1) / 5
 # residual of one solve through the public API
 b = np.random.default_rng(0).standard_normal(a.n)
 xs = glu.solve(glu.LuFactors(fp, lu), b)
