@@ -138,7 +138,7 @@ struct FactorParams {
     unsigned long long *level_ns;  // optional per-phase completion timestamps
     unsigned long long *trace;     // optional per-item timestamps (diagnostics)
     i32 trace_i0, trace_i1;        // traced item range
-    i32 prefetch;                  // L2-prefetch the next item's static plan data
+    i32 prefetch;                  // L2-prefetch the next item's static plan data when its phase < prefetch
     i32 poll_ns;                   // sleep between dependency polls
     i32 fail_by_column;            // 1: key = column only (sequential API semantics)
 };
@@ -419,7 +419,7 @@ __device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool 
 // L2 prefetch of an item's static plan data (descriptor already loaded):
 // its chunk descriptors, u8 map and target list, or the first deep refs.
 __device__ __forceinline__ void prefetch_item(const FactorParams &P, int4 a, int4 b, int4 c, int lane) {
-    if (c.y < 0 || !P.prefetch) return;
+    if (c.y < 0 || (c.y >> 2) >= P.prefetch) return;
     const char *p = nullptr;
     if (c.y & 1) {
         const i64 off = (i64)(unsigned)a.x | ((i64)a.y << 32);
@@ -1866,7 +1866,7 @@ struct glu_handle {
     i64 trace_l0 = 0, trace_nl = 0, trace_cap = 0;
     bool time_levels = false;
     bool fail_by_column = false;
-    bool prefetch = false;
+    int prefetch = 0;  // phases whose items get their plan data L2-prefetched (option 5)
     int poll_ns = 32;
     std::vector<double> last_level_ms;
     // host-API staging
@@ -2111,8 +2111,8 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             }
             return GLU_OK;
         }
-        case 5:  // tuning: L2 prefetch of the next item's plan data (default on)
-            h->prefetch = value != 0;
+        case 5:  // tuning: L2-prefetch the next item's plan data for items of phases < value (0 = off)
+            h->prefetch = (int)std::max<int64_t>(0, std::min<int64_t>(value, INT32_MAX));
             return GLU_OK;
         case 6:  // tuning: nanoseconds between dependency polls
             h->poll_ns = (int)std::max<int64_t>(0, std::min<int64_t>(value, 100000));
@@ -2271,7 +2271,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.fail_by_column = h->fail_by_column ? 1 : 0;
     P.trace = nullptr;
     P.trace_i0 = P.trace_i1 = 0;
-    P.prefetch = h->prefetch ? 1 : 0;
+    P.prefetch = h->prefetch;
     P.poll_ns = h->poll_ns;
     if (h->trace_nl > 0 && h->trace) {
         P.trace = h->trace;

@@ -167,6 +167,8 @@ class Factorizer:
         self._lock = threading.Lock()
         if "GLU_POLL_NS" in os.environ:  # tuning: ns between dependency polls (option 6)
             self.set_option(6, int(os.environ["GLU_POLL_NS"]))
+        if "GLU_PREFETCH_PHASES" in os.environ:  # tuning: L2-prefetch plan data of the first phases (option 5)
+            self.set_option(5, int(os.environ["GLU_PREFETCH_PHASES"]))
         info = np.zeros(12, dtype=np.int64)
         _lib.lib.glu_handle_info(h, _lib.ptr(info))
         self.handle_info = dict(zip(("n", "nnz", "levels", "items", "chunks", "macs",
