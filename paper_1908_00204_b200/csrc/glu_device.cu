@@ -971,6 +971,12 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         unsigned *grow = reinterpret_cast<unsigned *>(g + (size_t)B * T.mpad);
         double ra[kTailB], rb[kTailB];
         unsigned pa = 0, pb = 0;  // bit k: row ia / ib is in panel column s0+k
+        // warps whose rows all lie above the panel (or past M) have nothing
+        // to update in it: their chains would only subtract +0.0 (the sweep
+        // is FP64-bound on the owner SM, so they are skipped -- measured
+        // ~550 + 70 x (remaining columns) cycles per step with them)
+        const bool wa = __any_sync(0xffffffffu, ia < M && ia >= s0);
+        const bool wb = __any_sync(0xffffffffu, ib < M && ib >= s0);
 #pragma unroll
         for (int k = 0; k < kTailB; ++k) {
             ra[k] = 0.0;
@@ -1009,11 +1015,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
                 // branch-free: every product is formed, the subtraction is
                 // selected only where L(i,s) and U(s,q) are in the pattern
                 const unsigned ma = ba ? ub : 0u, mb = bb ? ub : 0u;
+                if (wa) {
 #pragma unroll
-                for (int kk = k + 1; kk < kTailB; ++kk) {
-                    const double u = ur[kk];
-                    ra[kk] = __dsub_rn(ra[kk], ((ma >> kk) & 1u) ? __dmul_rn(la, u) : 0.0);
-                    rb[kk] = __dsub_rn(rb[kk], ((mb >> kk) & 1u) ? __dmul_rn(lb, u) : 0.0);
+                    for (int kk = k + 1; kk < kTailB; ++kk)
+                        ra[kk] = __dsub_rn(ra[kk], ((ma >> kk) & 1u) ? __dmul_rn(la, ur[kk]) : 0.0);
+                }
+                if (wb) {
+#pragma unroll
+                    for (int kk = k + 1; kk < kTailB; ++kk)
+                        rb[kk] = __dsub_rn(rb[kk], ((mb >> kk) & 1u) ? __dmul_rn(lb, ur[kk]) : 0.0);
                 }
             }
         }
@@ -1022,8 +1032,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         for (int k = 0; k < kTailB; ++k) {
             if (k < bp) {
                 double *cq = cols + (size_t)(xb0 + k) * T.mpad;
-                if (ia < M) cq[ia] = ra[k];
-                if (ib < M) cq[ib] = rb[k];
+                if (wa && ia < M) cq[ia] = ra[k];
+                if (wb && ib < M) cq[ib] = rb[k];
             }
         }
         if (ia < M) __stcg(grow + ia, bra);

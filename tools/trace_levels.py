@@ -10,7 +10,7 @@ from paper_1908_00204_b200 import synthetic, _lib
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 contract = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-ranges = [(0, 2), (300, 4), (700, 4), (1200, 4)]
+ranges = [(0, 2), (10, 2), (300, 4), (690, 2)]
 a = synthetic.make(cfg)
 fp = glu.symbolic_fillin(a.pattern)
 s = glu.levelize(glu.detect_relaxed(fp))
@@ -42,6 +42,8 @@ for l0, nl in ranges:
     out[f"r{l0}"] = rec
     out[f"ends{l0}"] = ends
     fz.set_option(4, 0)
+    if not len(rec):
+        continue
     t0 = rec[:, 2].min()
     lv = rec[:, 0] >> 32
     for l in range(l0, l0 + nl):
