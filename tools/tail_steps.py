@@ -22,3 +22,5 @@ d = np.diff(C[:, :17], axis=1)  # cycles per step (k -> k+1), last = write-back 
 print("panels", npan)
 print("median cycles per step:", np.median(d[1:], axis=0).astype(int).tolist())
 print("panel totals (cycles):", (C[1:6, 16] - C[1:6, 0]).tolist())
+tot = C[:, 16] - C[:, 0]
+print("per-panel sweep cycles, every 4th panel:", tot[::4].tolist())
