@@ -1058,7 +1058,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         double la[kTailB], lb[kTailB];
         const unsigned bitsa = (ia >= s1 && ia < M) ? __ldcg(grow + ia) : 0u;
         const unsigned bitsb = (ib >= s1 && ib < M) ? __ldcg(grow + ib) : 0u;
-        const bool ra = ia < T.mpad, rb = ib < T.mpad;
+        // only rows below the panel use its L values (bitsa/bitsb are 0 above)
+        const bool ra = ia >= s1 && ia < M, rb = ib >= s1 && ib < M;
 #pragma unroll
         for (int k = 0; k < kTailB; ++k) {
             la[k] = (ra && k < bp) ? __ldcg(g + (size_t)k * T.mpad + ia) : 0.0;
