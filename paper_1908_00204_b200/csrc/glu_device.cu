@@ -863,6 +863,7 @@ struct TailParams {
     double thresh;
     unsigned long long *fail;
     i32 fail_by_column;
+    const unsigned long long *mk0;  // structure bitmasks of the tail columns (m x mw, host-built)
     // diagnostics (option 13): [0..7] CTA 0 phase stamps, then per panel
     // {observed p-1, applied p-1 to it, column sweep done, written back, published} by its owner
     unsigned long long *trace;
@@ -936,23 +937,23 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     if (c == 0) stamp_t(0);
     int nvalid = ncol;  // owned columns that exist (the last panel may be short)
     while (nvalid > 0 && qtab[nvalid - 1] >= M) --nvalid;
-    for (int x = 0; x < ncol; ++x) {
-        if (qglob(x) >= M) break;
-        for (int i = tid; i < T.mpad; i += nt) cols[(size_t)x * T.mpad + i] = 0.0;
-        for (int w = tid; w < T.mw; w += nt) mk[x * T.mw + w] = 0ull;
+    // load the owned columns: zero-fill, structure masks from the host-built
+    // table, then a warp per column with its entry loads batched
+    for (int e = tid; e < nvalid * T.mpad; e += nt) cols[e] = 0.0;
+    for (int e = tid; e < nvalid * T.mw; e += nt) {
+        const int x = e / T.mw;
+        mk[e] = __ldg(T.mk0 + (size_t)qglob(x) * T.mw + (e - x * T.mw));
     }
     __syncthreads();
-    for (int x = 0; x < ncol; ++x) {
-        const int q = qglob(x);
-        if (q >= M) break;
-        const int j = T.t0 + q;
+    for (int x = wid; x < nvalid; x += nwarp) {
+        const int j = T.t0 + qglob(x);
         const int lo = __ldg(T.col_ptr + j), hi = __ldg(T.col_ptr + j + 1);
-        for (int p = lo + tid; p < hi; p += nt) {
+        double *cq = cols + (size_t)x * T.mpad;
+#pragma unroll 4
+        for (int p = lo + lane; p < hi; p += 32) {
             const int r = __ldg(T.row_idx + p) - T.t0;
-            if (r >= 0) {
-                cols[(size_t)x * T.mpad + r] = ldv(T.v + p);
-                atomicOr(&mk[x * T.mw + (r >> 6)], 1ull << (r & 63));
-            }
+            const double val = ldv(T.v + p);
+            if (r >= 0) cq[r] = val;
         }
     }
     __syncthreads();
@@ -1832,6 +1833,7 @@ struct glu_handle {
     i64 max_push_macs = 0;  // largest push item of the plan (kernel variant)
     TailShape tail;
     double *tail_g = nullptr;
+    unsigned long long *tail_mk = nullptr;  // structure bitmasks of the tail columns
     unsigned long long *fail_batch = nullptr;
     i64 fail_batch_cap = 0;
     // optional per-launch kernel timing: a ring of event triples
@@ -2026,6 +2028,16 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
                                " columns exceeds this device's cluster capacity (glu_tail_capacity)");
                 return fail(GLU_EINVAL);
             }
+            {  // per tail column: rows of the block present in the pattern
+                const int mw = h->tail.mw;
+                std::vector<unsigned long long> mk((size_t)m * mw, 0ull);
+                for (i64 q = 0; q < m; q++)
+                    for (i64 p = col_ptr[pv.tail_t0 + q]; p < col_ptr[pv.tail_t0 + q + 1]; p++) {
+                        const i64 r = row_idx[p] - pv.tail_t0;
+                        if (r >= 0) mk[(size_t)q * mw + (r >> 6)] |= 1ull << (r & 63);
+                    }
+                UP(h->tail_mk, mk);
+            }
             const size_t gstride = (size_t)tail_gstride(h->tail);
             if (cudaMalloc((void **)&h->tail_g, (size_t)h->tail.np * gstride * sizeof(double) +
                                                     sizeof(unsigned) * (h->tail.np + 32)) != cudaSuccess) {
@@ -2084,7 +2096,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->tail_trace, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -2330,6 +2342,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         T.fail = fail;
         T.fail_by_column = h->fail_by_column ? 1 : 0;
         T.trace = h->tail_trace;
+        T.mk0 = h->tail_mk;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
