@@ -864,6 +864,8 @@ struct TailParams {
     unsigned long long *fail;
     i32 fail_by_column;
     const unsigned long long *mk0;  // structure bitmasks of the tail columns (m x mw, host-built)
+    const i32 *blk;     // per tail column: first slot inside the block (rows >= t0)
+    double *umax;       // per tail column: max |value| above the block (final before the tail)
     // diagnostics (option 13): [0..7] CTA 0 phase stamps, then per panel
     // {observed p-1, applied p-1 to it, column sweep done, written back, published} by its owner
     unsigned long long *trace;
@@ -880,31 +882,6 @@ __device__ __forceinline__ unsigned mbits(const unsigned long long *mk, int s, i
     return (unsigned)(x & ((1ull << len) - 1ull));
 }
 
-__device__ __forceinline__ void divide_column_t(const TailParams &T, int j, int lane) {
-    const int lo = __ldg(T.col_ptr + j), hi = __ldg(T.col_ptr + j + 1);
-    const int d = __ldg(T.diag_pos + j);
-    double cmax = 0.0;
-    for (int p = lo + lane; p < hi; p += 32) {
-        const double av = fabs(ldv(T.v + p));
-        if (av > cmax) cmax = av;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double x = __shfl_xor_sync(0xffffffffu, cmax, o);
-        if (x > cmax) cmax = x;
-    }
-    const double piv = ldv(T.v + d);
-    if (fabs(piv) <= __dmul_rn(T.thresh, cmax)) {
-        if (lane == 0) {
-            const unsigned long long key =
-                T.fail_by_column ? (unsigned long long)j
-                                 : (((unsigned long long)__ldg(T.level_of + j)) << 32) | (unsigned)j;
-            atomicMin(T.fail, key);
-        }
-        return;
-    }
-    for (int p = d + 1 + lane; p < hi; p += 32) stv(T.v + p, __ddiv_rn(ldv(T.v + p), piv));
-}
 
 __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     extern __shared__ __align__(16) double tsm[];
@@ -947,7 +924,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     __syncthreads();
     for (int x = wid; x < nvalid; x += nwarp) {
         const int j = T.t0 + qglob(x);
-        const int lo = __ldg(T.col_ptr + j), hi = __ldg(T.col_ptr + j + 1);
+        const int lo = __ldg(T.blk + qglob(x)), hi = __ldg(T.col_ptr + j + 1);  // block rows only
         double *cq = cols + (size_t)x * T.mpad;
 #pragma unroll 4
         for (int p = lo + lane; p < hi; p += 32) {
@@ -958,6 +935,43 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
     }
     __syncthreads();
     if (c == 0) stamp_t(1);
+    // Column maxima above the block (the U rows: final before this kernel),
+    // for the pivot test at the end.  Work units of <= 1024 entries are dealt
+    // over the warps (the power/ground hub columns hold ~34k each); the
+    // apply phase's tri[] array accumulates the bits of the non-negative
+    // maxima.  NaN never wins, as in the reference's `av > cmax`.
+    auto umax_pass = [&]() {
+        unsigned long long *acc = reinterpret_cast<unsigned long long *>(tri);
+        for (int x = tid; x < kTailMaxLocal; x += nt) acc[x] = 0ull;
+        __syncthreads();
+        int u = 0;
+        for (int x = 0; x < nvalid; ++x) {
+            const int j = T.t0 + qglob(x);
+            const int lo = __ldg(T.col_ptr + j), hb = __ldg(T.blk + qglob(x));
+            for (int p0 = lo; p0 < hb; p0 += 1024, ++u) {
+                if (u % nwarp != wid) continue;
+                const int p1 = min(p0 + 1024, hb);
+                double m = 0.0;
+#pragma unroll 8
+                for (int p = p0 + lane; p < p1; p += 32) {
+                    const double av = fabs(ldv(T.v + p));
+                    if (av > m) m = av;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double y = __shfl_xor_sync(0xffffffffu, m, o);
+                    if (y > m) m = y;
+                }
+                if (lane == 0 && m > 0.0) atomicMax(acc + x, (unsigned long long)__double_as_longlong(m));
+            }
+        }
+        __syncthreads();
+        for (int x = tid; x < nvalid; x += nt) T.umax[qglob(x)] = __longlong_as_double((long long)acc[x]);
+        __syncthreads();
+    };
+    // CTAs 0 and 1 own the first panels (needed before a pass of ~30 us
+    // would end): they run it at the end, where they have slack
+    if (c >= 2) umax_pass();
     const int ia = tid, ib = tid + nt;  // this thread's rows (m <= 2 * nt)
 
     // Owner: factor panel pp in place (its columns already hold every update
@@ -1184,19 +1198,40 @@ __global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
         }
     }
     if (c == 0) stamp_t(2);
-    for (int x = 0; x < ncol; ++x) {
-        const int q = qglob(x);
-        if (q >= M) break;
-        const int j = T.t0 + q;
-        const int lo = __ldg(T.col_ptr + j), hi = __ldg(T.col_ptr + j + 1);
-        for (int p = lo + tid; p < hi; p += nt) {
-            const int r = __ldg(T.row_idx + p) - T.t0;
-            if (r >= 0) stv(T.v + p, cols[(size_t)x * T.mpad + r]);
+    if (c < 2) umax_pass();
+    // store + pivot check + divide, a warp per column: the column maximum is
+    // the one above the block (umax) and the block's own (a scan of the
+    // column in shared memory: absent rows hold zeros), as divide_columns
+    // takes it over the whole column (_kernels.py:152-173)
+    for (int x = wid; x < nvalid; x += nwarp) {
+        const int q = qglob(x), j = T.t0 + q;
+        const int hb = __ldg(T.blk + q), hi = __ldg(T.col_ptr + j + 1);
+        const int d = __ldg(T.diag_pos + j);
+        const double *cq = cols + (size_t)x * T.mpad;
+        double cmax = __ldcg(T.umax + q);
+        for (int r = lane; r < M; r += 32) {
+            const double av = fabs(cq[r]);
+            if (av > cmax) cmax = av;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, cmax, o);
+            if (y > cmax) cmax = y;
+        }
+        const double piv = cq[q];
+        const bool bad = fabs(piv) <= __dmul_rn(T.thresh, cmax);
+        if (bad && lane == 0) {
+            const unsigned long long key =
+                T.fail_by_column ? (unsigned long long)j
+                                 : (((unsigned long long)__ldg(T.level_of + j)) << 32) | (unsigned)j;
+            atomicMin(T.fail, key);
+        }
+#pragma unroll 4
+        for (int p = hb + lane; p < hi; p += 32) {
+            const double val = cq[__ldg(T.row_idx + p) - T.t0];
+            stv(T.v + p, (!bad && p > d) ? __ddiv_rn(val, piv) : val);
         }
     }
-    __syncthreads();
-    for (int x = wid; x < ncol; x += nwarp)
-        if (qglob(x) < M) divide_column_t(T, T.t0 + qglob(x), lane);
     __syncthreads();
     if (c == 0) stamp_t(4);
 }
@@ -1834,6 +1869,8 @@ struct glu_handle {
     TailShape tail;
     double *tail_g = nullptr;
     unsigned long long *tail_mk = nullptr;  // structure bitmasks of the tail columns
+    i32 *tail_blk = nullptr;                // per tail column: first slot inside the block
+    double *tail_umax = nullptr;            // per tail column: max |U| above the block (scratch)
     unsigned long long *fail_batch = nullptr;
     i64 fail_batch_cap = 0;
     // optional per-launch kernel timing: a ring of event triples
@@ -2037,6 +2074,17 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
                         if (r >= 0) mk[(size_t)q * mw + (r >> 6)] |= 1ull << (r & 63);
                     }
                 UP(h->tail_mk, mk);
+                std::vector<i32> blk((size_t)m);
+                for (i64 q = 0; q < m; q++) {
+                    i64 p = col_ptr[pv.tail_t0 + q];
+                    while (p < col_ptr[pv.tail_t0 + q + 1] && row_idx[p] < pv.tail_t0) p++;
+                    blk[q] = (i32)p;
+                }
+                UP(h->tail_blk, blk);
+                if (cudaMalloc((void **)&h->tail_umax, sizeof(double) * m) != cudaSuccess) {
+                    glu::set_error("cudaMalloc(tail maxima)");
+                    return fail(GLU_ECUDA);
+                }
             }
             const size_t gstride = (size_t)tail_gstride(h->tail);
             if (cudaMalloc((void **)&h->tail_g, (size_t)h->tail.np * gstride * sizeof(double) +
@@ -2096,7 +2144,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -2343,6 +2391,8 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         T.fail_by_column = h->fail_by_column ? 1 : 0;
         T.trace = h->tail_trace;
         T.mk0 = h->tail_mk;
+        T.blk = h->tail_blk;
+        T.umax = h->tail_umax;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;

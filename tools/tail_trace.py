@@ -48,4 +48,5 @@ mean = {k: float(np.mean([r[k] for r in rows]))
         for k in ("handoff_us", "apply_us", "factor_us", "writeback_us", "publish_us")}
 print(json.dumps({"config": cfg, "panels": npan, "phases": ph, "per_panel_mean": mean,
                   "panel0_factor_us": (P[0, 3] - P[0, 1]) / 1e3,
+                  "handoff_all_us": [round(r["handoff_us"], 2) for r in rows],
                   "first_panels": rows[:6], "last_panels": rows[-4:]}, indent=1))
