@@ -1472,6 +1472,11 @@ struct SolveDfParams {
     i32 nrhs;
     i32 tblock;           // tasks per ticket grab; 0 = static round-robin over the warps
     i32 in_il, reset_il;  // multi-RHS kernel: in / reset interleaved (out always is)
+    // single-RHS dense-tail mode: CTA 0 solves the tail rows [tail_t0, n) in
+    // index order with their values also in its shared memory; the other
+    // CTAs take the rows_nt list (the rest, level order) by ticket
+    i32 tail_t0, n_tail, n_nt;
+    const i32 *rows_nt;
     unsigned int *ticket;
     unsigned int *err;
 };
@@ -1485,29 +1490,26 @@ __device__ __forceinline__ void st_relaxed_u64(double *p, unsigned long long v) 
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+constexpr int kSolveTailMax = 1024;  // dense-tail rows CTA 0 keeps in shared memory
+
+__device__ __forceinline__ unsigned long long ld_volatile_smem_u64(const unsigned long long *p) {
+    return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+
 __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) {
     __shared__ __align__(16) double pbuf[kWarps][32];
     __shared__ int icol[kWarps][kSolveRing][32], islot[kWarps][kSolveRing][32];
+    __shared__ unsigned long long ysm[kSolveTailMax];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned total = (unsigned)S.n * (unsigned)S.nrhs;
-    const unsigned nw = gridDim.x * kWarps;
-    const unsigned tb = S.tblock > 0 ? (unsigned)S.tblock : 1u;
-    // tasks [t, t_end): a block of tb tickets (dynamic) or one task (static)
-    unsigned t = 0, t_end = 0;
-    if (S.tblock > 0) {
-        if (lane == 0) t = atomicAdd(S.ticket, tb);
-        t = __shfl_sync(0xffffffffu, t, 0);
-    } else {
-        t = blockIdx.x * kWarps + w;
-    }
-    t_end = t + tb;
-    while (t < total) {
-        unsigned tn = 0;  // next block of tickets, in flight while this block runs
-        if (S.tblock > 0 && t + 1 == t_end && lane == 0) tn = atomicAdd(S.ticket, tb);
-        const int ri = (int)(t / (unsigned)S.nrhs), r = (int)(t % (unsigned)S.nrhs);
-        const int i = __ldg(S.rows + ri);
+    const bool tail_on = S.n_tail > 0;
+    // one row of one right-hand side; tail: tail columns read from ysm
+    auto row = [&](int i, int r, bool tail) -> bool {
         const double *Xin = S.out + (size_t)r * S.ld_out;  // rows read by this row (ready-or-sentinel)
         const double *V = S.v + (size_t)r * S.v_stride;    // this task's factors
+        auto ldx = [&](int c) -> unsigned long long {
+            return (tail && c >= S.tail_t0) ? ld_volatile_smem_u64(ysm + (c - S.tail_t0))
+                                            : ld_relaxed_u64(Xin + c);
+        };
         const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
         double acc = ldv(S.in + (size_t)r * S.ld_in + i);
         const int ne = e1 - e0, ng = (ne + 31) >> 5;
@@ -1527,7 +1529,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
             cp_async_wait<kSolveRing - 1>();
             __syncwarp();
             if (lane < ne) {
-                xa = ld_relaxed_u64(Xin + icol[w][0][lane]);
+                xa = ldx(icol[w][0][lane]);
                 va = ldv(V + islot[w][0][lane]);
             }
             for (int g = 0; g < ng; ++g) {
@@ -1543,15 +1545,15 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
                     while (true) {
                         const bool pend = live && xa == kSent;
                         if (!__any_sync(0xffffffffu, pend)) break;
-                        if (pend) xa = ld_relaxed_u64(Xin + c);
+                        if (pend) xa = ldx(c);
                         if (__shfl_sync(0xffffffffu, globaltimer() - t0 > kWatchdogNs, 0)) {
                             if (lane == 0) atomicExch(S.err, 1u);
-                            return;  // warp-uniform
+                            return false;  // warp-uniform
                         }
                     }
                 }
                 if (32 * (g + 1) + lane < ne) {
-                    xb = ld_relaxed_u64(Xin + icol[w][(g + 1) % kSolveRing][lane]);
+                    xb = ldx(icol[w][(g + 1) % kSolveRing][lane]);
                     vb = ldv(V + islot[w][(g + 1) % kSolveRing][lane]);
                 }
                 __syncwarp();
@@ -1587,7 +1589,41 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
             if (bits == kSent) bits |= kQuietBit;  // only an untouched input can carry it
             st_relaxed_u64(S.out + (size_t)r * S.ld_out + i, bits);
             st_relaxed_u64(S.reset + (size_t)r * S.ld_reset + i, kSent);
+            if (tail) *reinterpret_cast<volatile unsigned long long *>(ysm + (i - S.tail_t0)) = bits;
         }
+        __syncwarp();
+        return true;
+    };
+    if (tail_on && blockIdx.x == 0) {
+        // the dense tail: rows in index order (a topological order of both
+        // passes), a warp per row, hand-offs through shared memory
+        for (int k = threadIdx.x; k < S.n_tail; k += blockDim.x) ysm[k] = kSent;
+        __syncthreads();
+        for (int k = w; k < S.n_tail; k += kWarps) {
+            const int i = S.upper ? (S.tail_t0 + S.n_tail - 1 - k) : (S.tail_t0 + k);
+            if (!row(i, 0, true)) return;
+        }
+        return;
+    }
+    const i32 *rows = tail_on ? S.rows_nt : S.rows;
+    const unsigned total = (unsigned)(tail_on ? S.n_nt : S.n) * (unsigned)S.nrhs;
+    const int b0 = tail_on ? 1 : 0;  // CTA 0 is the tail's
+    const unsigned nw = (gridDim.x - b0) * kWarps;
+    const unsigned tb = S.tblock > 0 ? (unsigned)S.tblock : 1u;
+    // tasks [t, t_end): a block of tb tickets (dynamic) or one task (static)
+    unsigned t = 0, t_end = 0;
+    if (S.tblock > 0) {
+        if (lane == 0) t = atomicAdd(S.ticket, tb);
+        t = __shfl_sync(0xffffffffu, t, 0);
+    } else {
+        t = (blockIdx.x - b0) * kWarps + w;
+    }
+    t_end = t + tb;
+    while (t < total) {
+        unsigned tn = 0;  // next block of tickets, in flight while this block runs
+        if (S.tblock > 0 && t + 1 == t_end && lane == 0) tn = atomicAdd(S.ticket, tb);
+        const int ri = (int)(t / (unsigned)S.nrhs), r = (int)(t % (unsigned)S.nrhs);
+        if (!row(__ldg(rows + ri), r, false)) return;
         if (S.tblock == 0) {
             t += nw;
         } else if (++t == t_end) {
@@ -1905,6 +1941,9 @@ struct glu_handle {
     i64 solve_il_cap = 0;
     // multi-RHS task lists (level order; built per k)
     std::vector<i32> l_rows_h, u_rows_h, l_ptr_h, u_ptr_h;
+    i32 *l_rows_nt = nullptr, *u_rows_nt = nullptr;  // level order without the dense-tail rows
+    i64 n_rows_nt = 0;
+    bool solve_tail = true;  // option 14
     SolveTask *tasks_l = nullptr, *tasks_u = nullptr;
     unsigned n_tasks_l = 0, n_tasks_u = 0;
     int tasks_k = 0;
@@ -2119,6 +2158,13 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     solve_levels(n, up_, uc, true, ulp, urows, h->u_levels);
     UP(h->l_ptr, lp); UP(h->l_col, lc); UP(h->l_slot, ls); UP(h->l_lvl_ptr, llp); UP(h->l_rows, lrows);
     UP(h->u_ptr, up_); UP(h->u_col, uc); UP(h->u_slot, us); UP(h->u_lvl_ptr, ulp); UP(h->u_rows, urows);
+    {
+        std::vector<i32> lnt, unt;
+        for (i32 i : lrows) if (i < h->tail_t0) lnt.push_back(i);
+        for (i32 i : urows) if (i < h->tail_t0) unt.push_back(i);
+        h->n_rows_nt = (i64)lnt.size();
+        UP(h->l_rows_nt, lnt); UP(h->u_rows_nt, unt);
+    }
     h->l_rows_h = std::move(lrows); h->u_rows_h = std::move(urows);
     h->l_ptr_h = std::move(lp); h->u_ptr_h = std::move(up_);
 #undef UP
@@ -2144,7 +2190,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -2213,6 +2259,9 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             }
             return GLU_OK;
         }
+        case 14:  // tuning: single-RHS solves keep the dense-tail rows on CTA 0 (default 1)
+            h->solve_tail = value != 0;
+            return GLU_OK;
         case 12:  // tuning: k > 1 solves, rows longer than this run one task per right-hand side
             h->solve_long_row = (int)std::max<int64_t>(0, std::min<int64_t>(value, 1 << 30));
             h->tasks_k = 0;  // rebuild the task lists
@@ -2643,6 +2692,15 @@ static void solve_params_common(glu_handle *h, SolveDfParams &S, const double *l
     S.ticket = h->sctl;
     S.err = h->sctl + 1;
     S.in_il = S.reset_il = 0;
+    const i64 m = h->n - h->tail_t0;
+    // U pass only: its tail rows read only tail columns; an L tail row also
+    // carries ~500 entries left of the block, and funnelling those through
+    // one SM measured slower (cfg2 L 1.12 -> 1.66 ms, U 1.62 -> 1.47 ms)
+    const bool tail = h->solve_tail && upper && nrhs == 1 && m >= 128 && m <= kSolveTailMax && h->grid > 1;
+    S.tail_t0 = (i32)h->tail_t0;
+    S.n_tail = tail ? (i32)m : 0;
+    S.n_nt = (i32)h->n_rows_nt;
+    S.rows_nt = upper ? h->u_rows_nt : h->l_rows_nt;
 }
 
 // multi-RHS pass on the interleaved buffers: L reads x (caller layout) into
@@ -2674,6 +2732,7 @@ static int64_t launch_solve_df(glu_handle *h, const double *lu, double *x, bool 
     SolveDfParams S;
     solve_params_common(h, S, lu, upper, nrhs);
     S.v_stride = v_stride;
+    if (v_stride != 0) S.n_tail = 0;  // batch solves: the per-set path
     if (upper) {
         S.in = h->solve_y; S.ld_in = h->n;
         S.out = x; S.ld_out = ldx;

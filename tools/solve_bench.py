@@ -21,6 +21,8 @@ if tblock >= 0:
     fz.set_option(10, tblock)
 multi = int(os.environ.get("GLU_SOLVE_MULTI", "1"))
 fz.set_option(11, multi)
+stail = int(os.environ.get("GLU_SOLVE_TAIL", "1"))
+fz.set_option(14, stail)
 long_row = int(os.environ.get("GLU_SOLVE_LONG", "-1"))
 if long_row >= 0:
     fz.set_option(12, long_row)
@@ -29,7 +31,7 @@ assert rc == -1
 dev = torch.device("cuda", 0)
 lu_d = torch.from_numpy(lu).to(dev)
 st = torch.cuda.current_stream()
-out = {"config": cfg, "solve_mode": ["dataflow", "level-synchronous"][mode], "tblock": tblock, "multi": multi, "long_row": long_row, "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
+out = {"config": cfg, "solve_mode": ["dataflow", "level-synchronous"][mode], "tblock": tblock, "multi": multi, "tail_cta": stail, "long_row": long_row, "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
        "usolve_levels": fz.handle_info["usolve_levels"]}
 for k in (1, 8, 32):
     x = torch.randn((k, a.n), dtype=torch.float64, device=dev)
@@ -45,6 +47,20 @@ for k in (1, 8, 32):
     e1.record(st)
     torch.cuda.synchronize()
     out[f"nrhs{k}_ms"] = e0.elapsed_time(e1) / reps
+# L only / U only, one right-hand side
+for part, name in ((1, "lower1_ms"), (2, "upper1_ms")):
+    x = torch.randn((1, a.n), dtype=torch.float64, device=dev)
+    for _ in range(2):
+        _lib.lib.glu_solve_multi_device(fz.handle, glu.numeric._dptr(lu_d), glu.numeric._dptr(x), 1, a.n, part,
+                                        ctypes.c_void_p(st.cuda_stream))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(5):
+        _lib.lib.glu_solve_multi_device(fz.handle, glu.numeric._dptr(lu_d), glu.numeric._dptr(x), 1, a.n, part,
+                                        ctypes.c_void_p(st.cuda_stream))
+    e1.record(st)
+    torch.cuda.synchronize()
+    out[name] = e0.elapsed_time(e1) / 5
 # batch solves: nb sets, each its own factors (replicas here) and right-hand side
 for nbs in (8, 32):
     L = lu_d.repeat(nbs, 1).reshape(nbs, -1).contiguous()
