@@ -1476,7 +1476,9 @@ struct SolveDfParams {
     // index order with their values also in its shared memory; the other
     // CTAs take the rows_nt list (the rest, level order) by ticket
     i32 tail_t0, n_tail, n_nt;
-    const i32 *rows_nt;
+    const i32 *rows_nt;   // L: followed by the tail rows' partial tasks (n_nt + n_tail tickets)
+    const i32 *lsplit;    // L tail row k: first entry in a tail column
+    double *part;         // L tail row k: partial sum over the columns left of the block (sentinel)
     unsigned int *ticket;
     unsigned int *err;
 };
@@ -1503,15 +1505,39 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const bool tail_on = S.n_tail > 0;
     // one row of one right-hand side; tail: tail columns read from ysm
-    auto row = [&](int i, int r, bool tail) -> bool {
+    // mode 0: a whole row; 1: a tail row on CTA 0 (tail columns from ysm;
+    // in L it starts from its partial sum); 2: an L tail row's partial sum
+    // over the columns left of the block (published to S.part)
+    auto row = [&](int i, int r, int mode) -> bool {
+        const bool tail = mode == 1;
         const double *Xin = S.out + (size_t)r * S.ld_out;  // rows read by this row (ready-or-sentinel)
         const double *V = S.v + (size_t)r * S.v_stride;    // this task's factors
         auto ldx = [&](int c) -> unsigned long long {
             return (tail && c >= S.tail_t0) ? ld_volatile_smem_u64(ysm + (c - S.tail_t0))
                                             : ld_relaxed_u64(Xin + c);
         };
-        const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
-        double acc = ldv(S.in + (size_t)r * S.ld_in + i);
+        int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
+        double acc;
+        if (mode == 2) {
+            e1 = __ldg(S.lsplit + (i - S.tail_t0));
+            acc = ldv(S.in + (size_t)r * S.ld_in + i);
+        } else if (tail && !S.upper) {  // continue from the partial sum
+            e0 = __ldg(S.lsplit + (i - S.tail_t0));
+            double *pp = S.part + (i - S.tail_t0);
+            unsigned long long pb = 0;
+            const unsigned long long t0 = globaltimer();
+            if (lane == 0) {
+                while ((pb = ld_relaxed_u64(pp)) == kSent) {
+                    if (globaltimer() - t0 > kWatchdogNs) { atomicExch(S.err, 1u); break; }
+                }
+                st_relaxed_u64(pp, kSent);  // the buffer returns to the sentinel
+            }
+            pb = __shfl_sync(0xffffffffu, pb, 0);
+            if (pb == kSent) return false;  // watchdog (warp-uniform)
+            acc = __longlong_as_double((long long)pb);
+        } else {
+            acc = ldv(S.in + (size_t)r * S.ld_in + i);
+        }
         const int ne = e1 - e0, ng = (ne + 31) >> 5;
         auto ent = [&](int k) { return S.upper ? (e1 - 1 - k) : (e0 + k); };
         auto issue_idx = [&](int g) {
@@ -1583,7 +1609,11 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
             cp_async_wait<0>();
             __syncwarp();
         }
-        if (lane == 0) {
+        if (lane == 0 && mode == 2) {
+            unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
+            if (bits == kSent) bits |= kQuietBit;
+            st_relaxed_u64(S.part + (i - S.tail_t0), bits);
+        } else if (lane == 0) {
             if (S.upper) acc = __ddiv_rn(acc, ldv(V + __ldg(S.diag_pos + i)));
             unsigned long long bits = (unsigned long long)__double_as_longlong(acc);
             if (bits == kSent) bits |= kQuietBit;  // only an untouched input can carry it
@@ -1601,12 +1631,14 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
         __syncthreads();
         for (int k = w; k < S.n_tail; k += kWarps) {
             const int i = S.upper ? (S.tail_t0 + S.n_tail - 1 - k) : (S.tail_t0 + k);
-            if (!row(i, 0, true)) return;
+            if (!row(i, 0, 1)) return;
         }
         return;
     }
     const i32 *rows = tail_on ? S.rows_nt : S.rows;
-    const unsigned total = (unsigned)(tail_on ? S.n_nt : S.n) * (unsigned)S.nrhs;
+    // L with the tail on CTA 0: the tail rows' partial sums follow (tickets n_nt..)
+    const unsigned total =
+        (unsigned)(tail_on ? S.n_nt + (S.upper ? 0 : S.n_tail) : S.n) * (unsigned)S.nrhs;
     const int b0 = tail_on ? 1 : 0;  // CTA 0 is the tail's
     const unsigned nw = (gridDim.x - b0) * kWarps;
     const unsigned tb = S.tblock > 0 ? (unsigned)S.tblock : 1u;
@@ -1623,7 +1655,8 @@ __global__ void __launch_bounds__(kThreads, 1) solve_df_kernel(SolveDfParams S) 
         unsigned tn = 0;  // next block of tickets, in flight while this block runs
         if (S.tblock > 0 && t + 1 == t_end && lane == 0) tn = atomicAdd(S.ticket, tb);
         const int ri = (int)(t / (unsigned)S.nrhs), r = (int)(t % (unsigned)S.nrhs);
-        if (!row(__ldg(rows + ri), r, false)) return;
+        const int i = (tail_on && ri >= S.n_nt) ? S.tail_t0 + (ri - S.n_nt) : __ldg(rows + ri);
+        if (!row(i, r, (tail_on && ri >= S.n_nt) ? 2 : 0)) return;
         if (S.tblock == 0) {
             t += nw;
         } else if (++t == t_end) {
@@ -1942,6 +1975,8 @@ struct glu_handle {
     // multi-RHS task lists (level order; built per k)
     std::vector<i32> l_rows_h, u_rows_h, l_ptr_h, u_ptr_h;
     i32 *l_rows_nt = nullptr, *u_rows_nt = nullptr;  // level order without the dense-tail rows
+    i32 *l_split = nullptr;        // L tail row: first entry in a tail column
+    double *solve_part = nullptr;  // L tail rows' partial sums (sentinel between calls)
     i64 n_rows_nt = 0;
     bool solve_tail = true;  // option 14
     SolveTask *tasks_l = nullptr, *tasks_u = nullptr;
@@ -2164,6 +2199,23 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         for (i32 i : urows) if (i < h->tail_t0) unt.push_back(i);
         h->n_rows_nt = (i64)lnt.size();
         UP(h->l_rows_nt, lnt); UP(h->u_rows_nt, unt);
+        const i64 mt = n - h->tail_t0;
+        if (mt > 0) {
+            std::vector<i32> split((size_t)mt);
+            for (i64 k = 0; k < mt; k++) {
+                const i64 i = h->tail_t0 + k;
+                i32 e = lp[i];
+                while (e < lp[i + 1] && lc[e] < h->tail_t0) e++;
+                split[k] = e;
+            }
+            UP(h->l_split, split);
+            if (cudaMalloc((void **)&h->solve_part, sizeof(double) * mt) != cudaSuccess) {
+                glu::set_error("cudaMalloc(solve partials)");
+                return fail(GLU_ECUDA);
+            }
+            fill_sentinel_kernel<<<4, 256>>>(h->solve_part, mt);
+            if (cudaDeviceSynchronize() != cudaSuccess) { glu::set_error("fill"); return fail(GLU_ECUDA); }
+        }
     }
     h->l_rows_h = std::move(lrows); h->u_rows_h = std::move(urows);
     h->l_ptr_h = std::move(lp); h->u_ptr_h = std::move(up_);
@@ -2190,7 +2242,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->l_split, h->solve_part, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -2696,11 +2748,13 @@ static void solve_params_common(glu_handle *h, SolveDfParams &S, const double *l
     // U pass only: its tail rows read only tail columns; an L tail row also
     // carries ~500 entries left of the block, and funnelling those through
     // one SM measured slower (cfg2 L 1.12 -> 1.66 ms, U 1.62 -> 1.47 ms)
-    const bool tail = h->solve_tail && upper && nrhs == 1 && m >= 128 && m <= kSolveTailMax && h->grid > 1;
+    const bool tail = h->solve_tail && nrhs == 1 && m >= 128 && m <= kSolveTailMax && h->grid > 1;
     S.tail_t0 = (i32)h->tail_t0;
     S.n_tail = tail ? (i32)m : 0;
     S.n_nt = (i32)h->n_rows_nt;
     S.rows_nt = upper ? h->u_rows_nt : h->l_rows_nt;
+    S.lsplit = h->l_split;
+    S.part = h->solve_part;
 }
 
 // multi-RHS pass on the interleaved buffers: L reads x (caller layout) into
@@ -2798,6 +2852,7 @@ static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, 
         if (h->solve_y) fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_y, h->solve_y_cap);
         if (h->solve_yi) fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_yi, h->solve_il_cap);
         if (h->solve_zi) fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_zi, h->solve_il_cap);
+        if (h->solve_part) fill_sentinel_kernel<<<mg, 256, 0, s>>>(h->solve_part, h->n - h->tail_t0);
         cudaStreamSynchronize(s);
         glu::set_error("triangular solve: dependency wait exceeded the watchdog");
         return GLU_ECUDA;
