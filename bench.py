@@ -486,7 +486,7 @@ def run_batch(args):
     fp, s = analyze(a)
     macs, _ = glu.pattern_flops(fp)
     contract = 1 if args.contract == "B" else 0
-    fz = glu.Factorizer(fp, s.level_of, contract, tail_max=0, max_item_macs=64)
+    fz = glu.Factorizer(fp, s.level_of, contract, max_item_macs=64)  # dense tail: one cluster per set
     fz.set_input(a.col_ptr, a.row_idx)
     B = args.batch
     sets = np.stack(value_sets(a, rank, B))

@@ -866,6 +866,9 @@ struct TailParams {
     const unsigned long long *mk0;  // structure bitmasks of the tail columns (m x mw, host-built)
     const i32 *blk;     // per tail column: first slot inside the block (rows >= t0)
     double *umax;       // per tail column: max |value| above the block (final before the tail)
+    // batched launches: cluster b factors value set b (its own values,
+    // panel slots, ready flags, failure key and maxima)
+    long long set_stride, g_set;
     // diagnostics (option 13): [0..7] CTA 0 phase stamps, then per panel
     // {observed p-1, applied p-1 to it, column sweep done, written back, published} by its owner
     unsigned long long *trace;
@@ -883,7 +886,17 @@ __device__ __forceinline__ unsigned mbits(const unsigned long long *mk, int s, i
 }
 
 
-__global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T) {
+__global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(TailParams T0) {
+    TailParams T = T0;
+    {
+        const int set = (int)(blockIdx.x / cg::this_cluster().num_blocks());
+        T.v += (size_t)set * T.set_stride;
+        T.G += (size_t)set * T.g_set;
+        T.ready = reinterpret_cast<unsigned *>(T.G + (size_t)T.np * T.gstride);
+        T.fail += set;
+        T.umax += (size_t)set * T.m;
+        if (set > 0) T.trace = nullptr;
+    }
     extern __shared__ __align__(16) double tsm[];
     __shared__ double tri[kTailB * kTailB];   // panel rows' divided L values (row-major [i][s])
     __shared__ unsigned tribits[kTailB];      // L structure of panel row i over the panel sources
@@ -1246,6 +1259,11 @@ struct TailShape {
 
 int tail_gstride(const TailShape &t) {
     return (int)((((size_t)t.b * t.mpad + (size_t)t.mpad / 2 + 1) + 31) & ~(size_t)31);
+}
+// one value set's tail scratch: np panel slots, then np ready flags (+ pad)
+constexpr int kMaxTailSets = 8;  // = kMaxBatchPerLaunch
+long long tail_set_doubles(const TailShape &t) {
+    return (long long)t.np * tail_gstride(t) + ((long long)t.np + 32 + 1) / 2 + 16;
 }
 
 TailShape tail_shape(int m, int C, int b) {
@@ -2155,14 +2173,13 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
                     blk[q] = (i32)p;
                 }
                 UP(h->tail_blk, blk);
-                if (cudaMalloc((void **)&h->tail_umax, sizeof(double) * m) != cudaSuccess) {
+                if (cudaMalloc((void **)&h->tail_umax, sizeof(double) * m * kMaxTailSets) != cudaSuccess) {
                     glu::set_error("cudaMalloc(tail maxima)");
                     return fail(GLU_ECUDA);
                 }
             }
-            const size_t gstride = (size_t)tail_gstride(h->tail);
-            if (cudaMalloc((void **)&h->tail_g, (size_t)h->tail.np * gstride * sizeof(double) +
-                                                    sizeof(unsigned) * (h->tail.np + 32)) != cudaSuccess) {
+            if (cudaMalloc((void **)&h->tail_g, sizeof(double) * tail_set_doubles(h->tail) * kMaxTailSets) !=
+                cudaSuccess) {
                 glu::set_error("cudaMalloc(tail buffer)");
                 return fail(GLU_ECUDA);
             }
@@ -2406,8 +2423,8 @@ extern "C" int64_t glu_scatter_device(glu_handle *h, const double *a_vals, doubl
 static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream_t s,
                              unsigned long long *fail = nullptr, int nb = 1) {
     if (!fail) fail = h->fail;
-    if (nb > 1 && h->tail_t0 < h->n) {
-        glu::set_error("batched launch needs a plan without a dense tail");
+    if (nb > kMaxTailSets && h->tail_t0 < h->n) {
+        glu::set_error("batched launch: at most 8 value sets per launch with a dense tail");
         return GLU_EINVAL;
     }
     GLU_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long) * nb, s));
@@ -2485,8 +2502,13 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         T.ncl = h->tail.ncl;
         T.gstride = tail_gstride(h->tail);
         T.G = h->tail_g;
+        T.g_set = tail_set_doubles(h->tail);
+        T.set_stride = h->nnz;
         T.ready = reinterpret_cast<unsigned *>(h->tail_g + (size_t)h->tail.np * T.gstride);
-        GLU_CUDA(cudaMemsetAsync(T.ready, 0, sizeof(unsigned) * h->tail.np, s));
+        for (int b = 0; b < nb; ++b)  // every set's panel flags
+            GLU_CUDA(cudaMemsetAsync(reinterpret_cast<unsigned *>(h->tail_g + (size_t)b * T.g_set +
+                                                                  (size_t)h->tail.np * T.gstride),
+                                     0, sizeof(unsigned) * h->tail.np, s));
         T.thresh = thresh;
         T.fail = fail;
         T.fail_by_column = h->fail_by_column ? 1 : 0;
@@ -2500,7 +2522,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         attr[0].val.clusterDim.x = h->tail.C;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(h->tail.C);
+        cfg.gridDim = dim3(h->tail.C * nb);  // one cluster per value set
         cfg.blockDim = dim3(kTailThreads);
         cfg.dynamicSmemBytes = h->tail.smem;
         cfg.stream = s;
@@ -2595,14 +2617,11 @@ extern "C" int64_t glu_factor_batch_device(glu_handle *h, int64_t batch, double 
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = ensure_batch(h, std::max<int64_t>(batch, 1));
     if (rc != GLU_OK) return rc;
-    if (h->tail_t0 < h->n) {  // plan with a dense tail: one launch pair per set
-        for (int64_t b = 0; b < batch; b++)
-            if ((rc = launch_factor(h, v + b * h->nnz, thresh, s, h->fail_batch + b)) != GLU_OK) return rc;
-    } else {  // sets share each item's static loads, dependency wait and release
-        for (int64_t b0 = 0; b0 < batch; b0 += kMaxBatchPerLaunch) {
-            const int nb = (int)std::min<int64_t>(kMaxBatchPerLaunch, batch - b0);
-            if ((rc = launch_factor(h, v + b0 * h->nnz, thresh, s, h->fail_batch + b0, nb)) != GLU_OK) return rc;
-        }
+    // up to 8 sets per launch: they share each item's static loads,
+    // dependency wait and release; a dense tail runs one cluster per set
+    for (int64_t b0 = 0; b0 < batch; b0 += kMaxBatchPerLaunch) {
+        const int nb = (int)std::min<int64_t>(kMaxBatchPerLaunch, batch - b0);
+        if ((rc = launch_factor(h, v + b0 * h->nnz, thresh, s, h->fail_batch + b0, nb)) != GLU_OK) return rc;
     }
     return batch_status(h, batch, fail_cols, s);
 }
@@ -2618,7 +2637,7 @@ extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const dou
     if (rc != GLU_OK) return rc;
     if ((rc = ensure_batch(h, std::max<int64_t>(batch, 1))) != GLU_OK) return rc;
     cudaStream_t s = h->stream;
-    const bool batched = h->tail_t0 >= h->n;  // tail-less plan: sets share a launch
+    const bool batched = true;  // sets share a launch (a dense tail: one cluster per set)
     const int chunk = batched ? kMaxBatchPerLaunch : 1;
     if (batched && !h->d_vb) {
         GLU_CUDA(cudaMalloc((void **)&h->d_vb, sizeof(double) * h->nnz * chunk));

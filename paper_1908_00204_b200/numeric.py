@@ -310,16 +310,17 @@ def _digest(a: np.ndarray) -> bytes:
 def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int,
                    tail: bool = True) -> Factorizer:
     """Cached Factorizer for (fp, schedule, contract); dropped with fp.
-    tail=False builds the plan without the dense cluster tail, which lets a
-    launch factor several value sets at once (batch refactorization)."""
+    tail=False builds the batch plan (64-MAC items: the kernel variant that
+    loads two value sets per round); either plan keeps the dense cluster
+    tail, run as one cluster per value set in batched launches."""
     key = (id(fp), contract, _digest(level_of), tail)
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
         if hit is not None and hit[0]() is fp:
             return hit[1]
-        # batch plans: no dense tail, 64-MAC items (the kernel variant that
+        # batch plans: 64-MAC items (the kernel variant that
         # loads two value sets per round)
-        fz = Factorizer(fp, level_of, contract, tail_max=None if tail else 0,
+        fz = Factorizer(fp, level_of, contract, tail_max=None,
                         max_item_macs=0 if tail else 64)
 
         def _drop(_ref, key=key):
