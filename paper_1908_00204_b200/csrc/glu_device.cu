@@ -1261,7 +1261,7 @@ int tail_gstride(const TailShape &t) {
     return (int)((((size_t)t.b * t.mpad + (size_t)t.mpad / 2 + 1) + 31) & ~(size_t)31);
 }
 // one value set's tail scratch: np panel slots, then np ready flags (+ pad)
-constexpr int kMaxTailSets = 8;  // = kMaxBatchPerLaunch
+constexpr int kMaxTailSets = 16;  // = kMaxBatchPerLaunch
 long long tail_set_doubles(const TailShape &t) {
     return (long long)t.np * tail_gstride(t) + ((long long)t.np + 32 + 1) / 2 + 16;
 }
@@ -2424,7 +2424,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
                              unsigned long long *fail = nullptr, int nb = 1) {
     if (!fail) fail = h->fail;
     if (nb > kMaxTailSets && h->tail_t0 < h->n) {
-        glu::set_error("batched launch: at most 8 value sets per launch with a dense tail");
+        glu::set_error("batched launch: at most 16 value sets per launch with a dense tail");
         return GLU_EINVAL;
     }
     GLU_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long) * nb, s));
@@ -2583,7 +2583,7 @@ static int64_t ensure_staging(glu_handle *h);
 // batch-major (set b at v + b * nnz); every set is factored in stream order
 // by the same resident plan, each with its own failure slot, and the
 // statuses are read back once for the whole batch.
-constexpr int kMaxBatchPerLaunch = 8;
+constexpr int kMaxBatchPerLaunch = 16;  // 8: 322 /s, 16: 343 /s, 32: 341 /s (cfg2)
 
 static int64_t ensure_batch(glu_handle *h, int64_t batch) {
     if (batch <= h->fail_batch_cap) return GLU_OK;

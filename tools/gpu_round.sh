@@ -14,8 +14,8 @@ timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_$
 cat gpurun_out/bench_${TAG}.json | cut -c1-400
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_${TAG}.json 2>&1; echo "ref rc=$?"
 cut -c1-300 gpurun_out/bench_ref_${TAG}.json
-timeout 600 python bench.py --batch 8 --steps 5 --warmup 3 > gpurun_out/bench_batch8_${TAG}.json 2> gpurun_out/bench_batch8_${TAG}.err; echo "batch rc=$?"
-cut -c1-300 gpurun_out/bench_batch8_${TAG}.json
+timeout 600 python bench.py --batch 32 --steps 5 --warmup 3 > gpurun_out/bench_batch32_${TAG}.json 2> gpurun_out/bench_batch32_${TAG}.err; echo "batch rc=$?"
+cut -c1-300 gpurun_out/bench_batch32_${TAG}.json
 timeout 900 python bench.py --config cfg3 --steps 10 --warmup 3 > gpurun_out/bench_cfg3_${TAG}.json 2> gpurun_out/bench_cfg3_${TAG}.err; echo "cfg3 rc=$?"
 cut -c1-300 gpurun_out/bench_cfg3_${TAG}.json
 timeout 300 python tools/solve_bench.py cfg2 > gpurun_out/solve_${TAG}.json 2>&1; echo "solve rc=$?"; cut -c1-300 gpurun_out/solve_${TAG}.json
