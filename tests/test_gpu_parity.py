@@ -443,3 +443,40 @@ def test_solve_batch_per_set_bitwise(check_refusal):
         if bad == -1:
             assert np.array_equal(X[k], xr), k
     assert status[4] >= 0 and (status[[0, 1, 2, 3, 5]] == -1).all()
+
+
+def test_batched_tail_failure_in_one_set():
+    """A batched launch whose dense tail fails for one value set only: that
+    set reports the single launch's failing column (inside the tail), the
+    other sets' factors are bitwise the single launches'."""
+    import torch
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a)
+    cols = np.repeat(np.arange(a.n), np.diff(a.col_ptr))
+    vals = np.stack([synthetic.perturb_values(a, 2000 + b) for b in range(6)])
+    last = a.n - 1
+    th = 1e-14
+    ref = glu.get_factorizer(fp, s.level_of, 1)
+    ref.set_input(a.col_ptr, a.row_idx)
+    lu3, rc3 = ref.factor_host(vals[3], th)
+    assert rc3 == -1
+    # subtract set 3's final pivot of the last (tail) column from its A entry:
+    # the recomputed pivot cancels to rounding level and breaks down there
+    vals[3][(a.row_idx == last) & (cols == last)] -= lu3[fp.diag_pos[last]]
+    fz = glu.get_factorizer(fp, s.level_of, 1, tail=False)
+    assert fz.plan_info["tail_t0"] < a.n  # the batch plan has a dense tail
+    fz.set_input(a.col_ptr, a.row_idx)
+    dev = torch.device("cuda")
+    v = torch.empty((len(vals), fp.nnz), dtype=torch.float64, device=dev)
+    for b in range(len(vals)):
+        fz.scatter_device(torch.from_numpy(vals[b]).to(dev), v[b])
+    fails = fz.factor_batch_device(v, th)
+    for b in range(len(vals)):
+        single, rc = ref.factor_host(vals[b], th)
+        assert int(fails[b]) == rc, b
+        if rc == -1:
+            assert np.array_equal(v[b].cpu().numpy(), single), b
+    assert int(fails[3]) >= fz.plan_info["tail_t0"]
+    assert all(int(fails[b]) == -1 for b in (0, 1, 2, 4, 5))
