@@ -134,6 +134,47 @@ void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
                      int64_t *chunks, int64_t *deep, uint8_t *map8, int64_t *tgt);
 void glu_plan_free(glu_plan *p);
 
+/* Supernodal plan: the same MACs and per-target MAC order as a contract-A
+   plan (_kernels.py:37-76 left-looking order), indexed per (fundamental
+   supernode, target column) -- ~0.1 B per MAC instead of ~3 -- for patterns
+   whose per-MAC plan does not fit (the G3-like cfg4: 3.8e10 MACs).  A
+   handle created from it runs the supernodal kernel (panels of <= 32
+   columns, dense in-panel blocks, relative row maps).  level_of is the
+   caller's schedule (it orders pivot failures, numeric.py:279-285).
+   Returns GLU_OK, GLU_MISMATCH (pattern not closed under fill) or
+   GLU_EINVAL. */
+int64_t glu_plan_build_sn(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                          const int64_t *diag_pos, const int64_t *row_ptr, const int64_t *col_idx,
+                          const int64_t *csc_pos, const int64_t *level_of, int32_t n_threads,
+                          glu_plan **out);
+/* info[0..9] = supernodes, panels, (supernode, column) pairs, relative-map
+   entries, pushes, tasks, phases, stages, MACs, plan bytes (all 0 for a
+   per-MAC plan). */
+void glu_sn_plan_info(const glu_plan *p, int64_t *info);
+/* Copies a supernodal plan out (sizes from glu_sn_plan_info; int32 x4
+   records): sn {s0, s1, |R_S|, first pair}, pan {p0, p1, supernode, rows
+   below}, pairs {k, a, base, map}, relmap, push {panel, pair0, pair1,
+   target panel}, tasks {index, chunk, kind, phase}, phase_ptr[phases+1],
+   col_a[n].  Any pointer may be NULL. */
+void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *pairs,
+                        int32_t *relmap, int32_t *push, int32_t *tasks, int32_t *phase_ptr,
+                        int32_t *col_a);
+
+/* Checks a caller's level schedule for factor_parallel (numeric.py:241-351
+   accepts any LevelSchedule) and refines it for contract B.  A source
+   column (U(i,j) != 0, L(:,i) non-empty) in a later level than its target
+   returns GLU_ESTRUCT with bad[0] = i, bad[1] = j (the reference would read
+   an unfinished column).  Contract A: phase_of = level_of.  Contract B:
+   levels are cut into sub-levels of consecutive columns wherever a column
+   depends on an earlier column of its own level (the reference's single
+   owner applies a level's sources in ascending order, _kernels.py:119-149),
+   so the phase-ordered plan reproduces the reference's reads.  Returns the
+   phase count. */
+int64_t glu_schedule_refine(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                            const int64_t *diag_pos, const int64_t *row_ptr, const int64_t *col_idx,
+                            const int64_t *level_of, int32_t contract, int64_t *phase_of,
+                            int64_t *bad);
+
 /* ---- device handle ---------------------------------------------------- */
 
 /* Uploads pattern, level schedule and plan (with its u8 scatter map) to the
@@ -149,6 +190,10 @@ void glu_destroy(glu_handle *h);
    failing-pivot order: 0 = earliest level then min column (factor_parallel,
    numeric.py:279-285), 1 = min column (sequential paths, numeric.py:129-159). */
 int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value);
+/* Levels that order pivot failures (key 2 = 0): the caller's schedule,
+   which may differ from the one the plan was built on (contract A plans
+   on the relaxed schedule). */
+int64_t glu_set_fail_levels(glu_handle *h, const int64_t *level_of);
 /* Diagnostics: glu_set_option(h, 3, first_phase) and (h, 4, n_phases)
    record, for every item of those phases, 8 words {item | phase << 32,
    warp, t_start, t_static_loaded, t_wait_done, t_values_loaded,

@@ -47,6 +47,11 @@ SIGNATURES = {
     "glu_find_hazards": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _i64, _p]),
     "glu_plan_build": (_i64, [_i64, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _i32, _pp]),
     "glu_tail_capacity": (_i64, []),
+    "glu_plan_build_sn": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _p, _i32, _pp]),
+    "glu_sn_plan_info": (None, [_p, _p]),
+    "glu_sn_plan_export": (None, [_p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "glu_schedule_refine": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p]),
+    "glu_set_fail_levels": (_i64, [_p, _p]),
     "glu_plan_info": (None, [_p, _p]),
     "glu_trace_read": (_i64, [_p, _p, _i64]),
     "glu_tail_trace_read": (_i64, [_p, _p, _i64]),

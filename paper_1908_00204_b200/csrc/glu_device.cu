@@ -2018,6 +2018,7 @@ struct glu_handle {
     cudaStream_t stream2 = nullptr;
     i64 col_ptr_h_t0 = 0;  // first slot of the dense tail
     cudaStream_t stream = nullptr;
+    glu::SnDev *sn = nullptr;  // supernodal engine (plans from glu_plan_build_sn)
 };
 
 namespace {
@@ -2243,6 +2244,9 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         cudaMalloc((void **)&h->sctl, 2 * sizeof(unsigned)) != cudaSuccess) {
         glu::set_error("cudaMalloc(scratch)"); return fail(GLU_ECUDA);
     }
+    if (pv.sn) {
+        if ((rc = glu::sn_upload(pv.sn, &h->sn, &h->bytes)) != GLU_OK) return fail(rc);
+    }
     h->grid = std::min({coop_grid((const void *)factor_kernel<4, 1>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)factor_kernel<2, 2>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)factor_kernel<2, 1>, h->sm_count, kFactorDynSmem),
@@ -2262,6 +2266,7 @@ extern "C" void glu_destroy(glu_handle *h) {
                     h->bar, h->ifail, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->l_split, h->solve_part, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    glu::sn_free(h->sn);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->stream2) cudaStreamDestroy(h->stream2);
     if (h->ev_main) cudaEventDestroy(h->ev_main);
@@ -2347,6 +2352,13 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
     }
 }
 
+extern "C" int64_t glu_set_fail_levels(glu_handle *h, const int64_t *level_of) {
+    std::vector<i32> lv = to_i32(level_of, h->n);
+    if (!lv.empty())
+        GLU_CUDA(cudaMemcpy(h->level_of, lv.data(), sizeof(i32) * lv.size(), cudaMemcpyHostToDevice));
+    return GLU_OK;
+}
+
 extern "C" int64_t glu_kernel_times(glu_handle *h, double *ms, int64_t max_launches) {
     const i64 m = std::min<i64>({max_launches, h->kev_slots, h->kev_next});
     for (i64 k = 0; k < m; k++) {
@@ -2428,6 +2440,26 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
         return GLU_EINVAL;
     }
     GLU_CUDA(cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long) * nb, s));
+    if (h->sn) {  // supernodal engine: one launch (+ pivot-check pass) per value set
+        const size_t nl8s = (size_t)std::max<i64>(h->n_levels, 1) * 8;
+        cudaEvent_t *ke = nullptr;
+        if (h->kev_slots > 0) {
+            ke = &h->kev[3 * (h->kev_next % h->kev_slots)];
+            h->kev_next++;
+            GLU_CUDA(cudaEventRecord(ke[0], s));
+        }
+        for (int b = 0; b < nb; b++) {
+            const i64 rc = glu::sn_launch(h->sn, v + (size_t)b * h->nnz, h->col_ptr, h->diag_pos, h->level_of,
+                                          (i32)h->n, thresh, h->fail_by_column, fail + b,
+                                          (int *)(h->sync + nl8s), s);
+            if (rc != GLU_OK) return rc;
+        }
+        if (ke) {
+            GLU_CUDA(cudaEventRecord(ke[1], s));
+            GLU_CUDA(cudaEventRecord(ke[2], s));
+        }
+        return GLU_OK;
+    }
     GLU_CUDA(cudaMemsetAsync(h->sync, 0, h->sync_words * sizeof(unsigned), s));
     FactorParams P;
     P.v = v;

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -279,6 +280,88 @@ extern "C" int64_t glu_scatter_values(int64_t n, const int64_t *a_col_ptr,
         }
     }
     return GLU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Caller schedules (factor_parallel accepts any LevelSchedule,
+// numeric.py:241-351).  The update plan orders MACs by phase, so a caller's
+// levels are checked, and for contract B refined, before planning:
+//
+//  * a source column i of column j (i in U(:,j), L(:,i) non-empty) in a
+//    LATER level than j: the reference then reads j before i's updates
+//    reach it (left_columns pulls an unfinished source; push_updates_owned
+//    pushes an unfinished column that is divided before its last update) --
+//    values the dataflow kernel cannot reproduce.  GLU_ESTRUCT, bad={i,j}.
+//  * contract B, same level: the reference's single owner applies a level's
+//    sources in ascending order (_kernels.py:119-149), so a later source j
+//    of the level sees an earlier one's MACs into its own column or into
+//    its multipliers U(j,k) (i writes (j,k) when L(j,i) != 0 and k > j is in
+//    U(i,:)).  Such a level is cut into sub-levels of consecutive columns
+//    at every j that depends that way on a column of its current sub-level:
+//    per target the MACs keep the level-major, ascending-source order, and
+//    each multiplier is read after exactly the MACs that precede it.
+//
+// Contract A values are schedule independent (left-looking order), so its
+// phases are the caller's levels unchanged (the caller plans on the relaxed
+// schedule).  Writes phase_of[n]; returns the phase count or GLU_ESTRUCT.
+// ---------------------------------------------------------------------------
+extern "C" int64_t glu_schedule_refine(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                       const int64_t *diag_pos, const int64_t *row_ptr,
+                                       const int64_t *col_idx, const int64_t *level_of,
+                                       int32_t contract, int64_t *phase_of, int64_t *bad) {
+    bad[0] = bad[1] = -1;
+    auto has_l = [&](i64 c) { return col_ptr[c + 1] - diag_pos[c] > 1; };
+    i64 n_levels = 0;
+    for (i64 j = 0; j < n; j++) {
+        if (level_of[j] < 0) {
+            set_error("negative level");
+            return GLU_EINVAL;
+        }
+        n_levels = std::max(n_levels, level_of[j] + 1);
+        for (i64 m = col_ptr[j]; m < diag_pos[j]; m++) {
+            const i64 i = row_idx[m];
+            if (has_l(i) && level_of[i] > level_of[j]) {
+                bad[0] = i;
+                bad[1] = j;
+                set_error("a source column sits in a later level than its target");
+                return GLU_ESTRUCT;
+            }
+        }
+    }
+    if (contract != GLU_CONTRACT_B) {
+        for (i64 j = 0; j < n; j++) phase_of[j] = level_of[j];
+        return n_levels;
+    }
+    // last U column of every row (row i's U part ends at its last CSR entry)
+    std::vector<i64> cnt(n_levels + 1, 0), order(n);
+    for (i64 j = 0; j < n; j++) cnt[level_of[j] + 1]++;
+    for (i64 l = 0; l < n_levels; l++) cnt[l + 1] += cnt[l];
+    for (i64 j = 0; j < n; j++) order[cnt[level_of[j]]++] = j;  // ascending within a level
+    std::vector<i64> sub(n, -1);
+    i64 phase = -1;
+    for (i64 l = 0, x = 0; l < n_levels; l++) {
+        const i64 end = x + (l == 0 ? cnt[0] : cnt[l] - cnt[l - 1]);
+        phase++;
+        for (; x < end; x++) {
+            const i64 j = order[x];
+            bool cut = false;
+            for (i64 m = col_ptr[j]; m < diag_pos[j] && !cut; m++) {
+                const i64 i = row_idx[m];
+                cut = sub[i] == phase && has_l(i);
+            }
+            if (!cut && has_l(j)) {
+                for (i64 t = row_ptr[j]; t < row_ptr[j + 1] && !cut; t++) {
+                    const i64 i = col_idx[t];
+                    if (i >= j) break;
+                    cut = sub[i] == phase && col_idx[row_ptr[i + 1] - 1] > j;
+                }
+            }
+            if (cut) phase++;
+            sub[j] = phase;
+        }
+    }
+    for (i64 j = 0; j < n; j++) phase_of[j] = sub[j];
+    return phase + 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -576,6 +659,7 @@ struct glu_plan {
     i64 deferred = 0;
     i64 n_deep_items = 0;
     i64 n_epochs = 0;
+    std::unique_ptr<glu::SnPlan> sn;  // supernodal engine (glu_plan_build_sn): no items above
 };
 
 static constexpr i64 kMaxSpan = 65535;
@@ -1042,6 +1126,66 @@ extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int6
 
 extern "C" void glu_plan_free(glu_plan *p) { delete p; }
 
+// Supernodal plan (glu_snode.cpp): the same MACs, in the same per-target
+// order (contract A), indexed per (supernode, target column) instead of per
+// MAC.  The round-1 item arrays stay empty; level_of only sizes the
+// per-level bookkeeping the handle keeps.
+extern "C" int64_t glu_plan_build_sn(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                     const int64_t *diag_pos, const int64_t *row_ptr,
+                                     const int64_t *col_idx, const int64_t *csc_pos,
+                                     const int64_t *level_of, int32_t n_threads, glu_plan **out) {
+    *out = nullptr;
+    auto *plan = new glu_plan();
+    plan->sn = std::make_unique<glu::SnPlan>();
+    const i64 rc = glu::sn_build(n, col_ptr, row_idx, diag_pos, row_ptr, col_idx, csc_pos, n_threads,
+                                 plan->sn.get());
+    if (rc != GLU_OK) {
+        delete plan;
+        return rc;
+    }
+    i64 n_levels = 0;
+    for (i64 j = 0; j < n; j++) n_levels = std::max<i64>(n_levels, level_of[j] + 1);
+    plan->n_levels = n_levels;
+    plan->level_item_ptr.assign(n_levels + 1, 0);
+    plan->col_total.assign(n, 0);
+    plan->tail_t0 = n;
+    *out = plan;
+    return GLU_OK;
+}
+
+extern "C" void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *pairs,
+                                   int32_t *relmap, int32_t *push, int32_t *tasks, int32_t *phase_ptr,
+                                   int32_t *col_a) {
+    const glu::SnPlan *s = p->sn.get();
+    if (!s) return;
+    auto cp4 = [](const std::vector<glu::I4> &v, int32_t *dst) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(glu::I4));
+    };
+    auto cp1 = [](const std::vector<int32_t> &v, int32_t *dst) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(int32_t));
+    };
+    cp4(s->sn, sn); cp4(s->pan, pan); cp4(s->pairs, pairs); cp1(s->relmap, relmap);
+    cp4(s->push, push); cp4(s->tasks, tasks); cp1(s->phase_ptr, phase_ptr); cp1(s->col_a, col_a);
+}
+
+extern "C" void glu_sn_plan_info(const glu_plan *p, int64_t *info) {
+    std::memset(info, 0, sizeof(int64_t) * 12);
+    const glu::SnPlan *s = p->sn.get();
+    if (!s) return;
+    info[0] = (i64)s->sn.size();
+    info[1] = (i64)s->pan.size();
+    info[2] = (i64)s->pairs.size();
+    info[3] = (i64)s->relmap.size();
+    info[4] = (i64)s->push.size();
+    info[5] = (i64)s->tasks.size();
+    info[6] = (i64)s->phase_ptr.size() - 1;
+    info[7] = s->n_stages;
+    info[8] = s->macs;
+    info[9] = (i64)((s->sn.size() + s->pan.size() + s->pairs.size() + s->push.size() + s->tasks.size()) *
+                        sizeof(glu::I4) +
+                    (s->relmap.size() + s->phase_ptr.size()) * sizeof(int32_t));
+}
+
 namespace glu {
 const glu_plan_view plan_view(const glu_plan *p) {
     glu_plan_view v;
@@ -1064,6 +1208,7 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.max_push_macs = p->max_push_macs;
     v.n_cdeps = (i64)p->cdeps.size();
     v.express_R = p->express_R;
+    v.sn = p->sn.get();
     return v;
 }
 }  // namespace glu

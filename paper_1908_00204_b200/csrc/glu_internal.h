@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <vector>
 
 struct glu_plan;
 
@@ -62,6 +63,40 @@ struct alignas(16) DeepRef {
 };
 static_assert(sizeof(DeepRef) == 16, "DeepRef layout");
 
+// ---------------------------------------------------------------------------
+// Supernodal engine (glu_snode.cpp / glu_snode.cu): the plan for patterns
+// whose per-MAC plan above does not fit (cfg4: 3.8e10 MACs).  Columns are
+// grouped into fundamental supernodes S = [s0, s1) (L(:,c-1) = {c} u L(:,c),
+// U(c-1,c) != 0), whose columns share the rows R_S below the supernode, and
+// cut into panels of <= kSnW columns.  Index records are 16-byte vectors.
+// ---------------------------------------------------------------------------
+constexpr int kSnW = 32;  // panel width: one warp lane per panel column / row
+
+struct alignas(16) I4 {
+    int32_t x, y, z, w;
+};
+
+enum SnTaskKind : int32_t {
+    kSnDiag = 0,  // factor a panel's w x w diagonal block (+ column maxima above it)
+    kSnTrsm = 1,  // 32 rows below a panel: divide, in-panel updates
+    kSnTri = 2,   // U(P, K): forward substitution inside a push's source panel
+    kSnRect = 3,  // 32 rows below the source panel into every column of a push
+};
+
+struct SnPlan {
+    int64_t n = 0, nnz = 0;
+    std::vector<I4> sn;      // {s0, s1, |R_S|, first pair}
+    std::vector<I4> pan;     // {p0, p1, supernode, rows below the panel}
+    std::vector<I4> pairs;   // per (supernode S, target column k): {k, a, base, map}
+    std::vector<int32_t> relmap;  // positions of R_S's rows in column k (absolute slots)
+    std::vector<I4> push;    // {source panel, first pair, end pair, target panel}
+    std::vector<I4> tasks;   // {index, chunk, kind, phase} in phase order
+    std::vector<int32_t> phase_ptr;  // tasks of phase p: [phase_ptr[p], phase_ptr[p+1])
+    std::vector<int32_t> col_a;      // per column c: first row of c's supernode present in c
+    int64_t n_stages = 0;
+    int64_t macs = 0;
+};
+
 struct glu_plan_view {
     int64_t n_levels;
     const int64_t *level_item_ptr;
@@ -82,9 +117,25 @@ struct glu_plan_view {
     int64_t n_cdeps;
     int64_t max_push_macs;     // largest push item (selects the kernel variant)
     int64_t express_R;         // SMs reserved for the express queue
+    const SnPlan *sn;          // supernodal engine (no items above), or null
 };
 
 const glu_plan_view plan_view(const glu_plan *p);
+// glu_snode.cpp: builds the supernodal plan; GLU_OK, GLU_MISMATCH or GLU_EINVAL
+int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, const int64_t *diag_pos,
+                 const int64_t *row_ptr, const int64_t *col_idx, const int64_t *csc_pos,
+                 int n_threads, SnPlan *out);
 void set_error(const std::string &s);
+
+// glu_snode.cu: device side of the supernodal engine
+struct SnDev;
+int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
+void sn_free(SnDev *d);
+int sn_grid(int sm_count);
+// one factorization of v (A_s values after the scatter); pivot failures
+// are min-reduced into *fail as (fail_level << 32 | column) or column
+int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *diag_pos,
+                  const int32_t *fail_level, int32_t n, double thresh, bool by_column,
+                  unsigned long long *fail, int *err, void *stream);
 
 }  // namespace glu

@@ -130,18 +130,29 @@ class Factorizer:
 
     def __init__(self, fp: FilledPattern, level_of: np.ndarray, contract: int,
                  max_item_macs: int = 0, threads: int = 0, deep_min: int = 0,
-                 tail_max: int | None = None):
+                 tail_max: int | None = None, engine: str = "plan"):
         self.n = fp.n
         self.nnz = fp.nnz
         self.contract = contract
+        self.engine = engine
         cp, ri, dp = _lib.i64(fp.full.col_ptr), _lib.i64(fp.full.row_idx), _lib.i64(fp.diag_pos)
         rp, ci, cs = _lib.i64(fp.csr.row_ptr), _lib.i64(fp.csr.col_idx), _lib.i64(fp.csr.csc_pos)
         lv = _lib.i64(level_of)
         plan = ctypes.c_void_p()
-        rc = _lib.check(_lib.lib.glu_plan_build(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
-                                                _lib.ptr(lv), contract, max_item_macs, deep_min,
-                                                _tail_capacity() if tail_max is None else tail_max,
-                                                threads, ctypes.byref(plan)), "glu_plan_build")
+        if engine == "sn":
+            if contract != _lib.CONTRACT_A:
+                raise ValueError("the supernodal engine computes contract A (ascending-source) values")
+            rc = _lib.check(_lib.lib.glu_plan_build_sn(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
+                                                       _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(cs),
+                                                       _lib.ptr(lv), threads, ctypes.byref(plan)),
+                            "glu_plan_build_sn")
+        elif engine == "plan":
+            rc = _lib.check(_lib.lib.glu_plan_build(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
+                                                    _lib.ptr(lv), contract, max_item_macs, deep_min,
+                                                    _tail_capacity() if tail_max is None else tail_max,
+                                                    threads, ctypes.byref(plan)), "glu_plan_build")
+        else:
+            raise ValueError(f"unknown engine {engine!r} (plan | sn)")
         if rc == _lib.GLU_MISMATCH:
             raise PatternMismatchError("update targeted a structurally absent slot")
         try:
@@ -152,6 +163,12 @@ class Factorizer:
                                        "deep_macs", "epochs", "push_macs", "targets", "tail_t0",
                                        "tail_macs", "express_items"),
                                       info.tolist()))
+            if engine == "sn":
+                sinfo = np.zeros(12, dtype=np.int64)
+                _lib.lib.glu_sn_plan_info(plan, _lib.ptr(sinfo))
+                self.sn_info = dict(zip(("supernodes", "panels", "pairs", "map", "pushes", "tasks",
+                                         "phases", "stages", "macs", "plan_bytes"), sinfo[:10].tolist()))
+                self.plan_info.update(macs=self.sn_info["macs"], plan_bytes=self.sn_info["plan_bytes"])
             h = ctypes.c_void_p()
             rc = _lib.check(_lib.lib.glu_create(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
                                                 _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(cs),
@@ -164,6 +181,7 @@ class Factorizer:
         self._h = h
         self._finalizer = weakref.finalize(self, _lib.lib.glu_destroy, h)
         self._input_key = None
+        self._fail_key = _digest(level_of)
         self._lock = threading.Lock()
         if "GLU_POLL_NS" in os.environ:  # tuning: ns between dependency polls (option 6)
             self.set_option(6, int(os.environ["GLU_POLL_NS"]))
@@ -184,6 +202,15 @@ class Factorizer:
 
     def set_option(self, key: int, value: int):
         _lib.check(_lib.lib.glu_set_option(self._h, key, value), "glu_set_option")
+
+    def set_fail_levels(self, level_of: np.ndarray):
+        """Levels that order pivot failures (factor_parallel reports the
+        earliest failing level of the CALLER's schedule, numeric.py:279-285)."""
+        key = _digest(level_of)
+        if key != self._fail_key:
+            _lib.check(_lib.lib.glu_set_fail_levels(self._h, _lib.ptr(_lib.i64(level_of))),
+                       "glu_set_fail_levels")
+            self._fail_key = key
 
     def set_input(self, a_col_ptr: np.ndarray, a_row_idx: np.ndarray):
         """Install the A -> A_s slot map (device scatter); cached per A pattern."""
@@ -307,13 +334,39 @@ def _digest(a: np.ndarray) -> bytes:
     return hashlib.sha1(np.ascontiguousarray(a, dtype=np.int64).tobytes()).digest()
 
 
+# Per-MAC plans cost ~3.3 B per MAC on the device (and ~2x that on the host
+# while building): above this many MACs contract A runs on the supernodal
+# engine, whose plan is ~0.1-0.4 B per MAC (cfg4: 3.8e10 MACs).
+SN_MIN_MACS = int(os.environ.get("GLU_SN_MIN_MACS", 2_000_000_000))
+# contract B has no supernodal form: refuse a per-MAC plan beyond this
+PLAN_MAX_MACS = int(os.environ.get("GLU_PLAN_MAX_MACS", 12_000_000_000))
+
+
+def pick_engine(fp: FilledPattern, contract: int) -> str:
+    """'sn' (supernodal) or 'plan' (per-MAC items): GLU_ENGINE forces one."""
+    forced = os.environ.get("GLU_ENGINE", "auto")
+    macs = _flops_cached(fp)[0]
+    if contract != _lib.CONTRACT_A:
+        if macs > PLAN_MAX_MACS:
+            raise _lib.GluError(f"atomic-mode (contract B) factorization needs a per-MAC plan; "
+                                f"{macs} MACs exceed GLU_PLAN_MAX_MACS={PLAN_MAX_MACS}")
+        return "plan"
+    if forced in ("plan", "sn"):
+        return forced
+    return "sn" if macs >= SN_MIN_MACS else "plan"
+
+
 def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int,
-                   tail: bool = True) -> Factorizer:
-    """Cached Factorizer for (fp, schedule, contract); dropped with fp.
-    tail=False builds the batch plan (64-MAC items: the kernel variant that
-    loads two value sets per round); either plan keeps the dense cluster
-    tail, run as one cluster per value set in batched launches."""
-    key = (id(fp), contract, _digest(level_of), tail)
+                   tail: bool = True, engine: str | None = None) -> Factorizer:
+    """Cached Factorizer for (fp, schedule, contract, engine); dropped with
+    fp.  tail=False builds the batch plan (64-MAC items: the kernel variant
+    that loads two value sets per round); either plan keeps the dense
+    cluster tail, run as one cluster per value set in batched launches."""
+    if engine is None:
+        engine = pick_engine(fp, contract)
+    if engine == "sn":
+        tail = True  # one plan serves single and batched launches
+    key = (id(fp), contract, _digest(level_of), tail, engine)
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
         if hit is not None and hit[0]() is fp:
@@ -321,7 +374,7 @@ def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int,
         # batch plans: 64-MAC items (the kernel variant that
         # loads two value sets per round)
         fz = Factorizer(fp, level_of, contract, tail_max=None,
-                        max_item_macs=0 if tail else 64)
+                        max_item_macs=0 if tail else 64, engine=engine)
 
         def _drop(_ref, key=key):
             with _CACHE_LOCK:
@@ -360,19 +413,61 @@ def _check(err: int) -> None:
         raise PivotError(err)
 
 
-def _factor(a: CscMatrix, fp: FilledPattern, level_of: np.ndarray, contract: int,
-            thresh: float, by_column: bool) -> tuple[np.ndarray, Factorizer]:
+def plan_levels(fp: FilledPattern, level_of: np.ndarray | None, contract: int) -> np.ndarray:
+    """The phase schedule the device plan is built on for a caller's level
+    schedule (None: the sequential paths).  Contract A values do not depend
+    on the schedule (left-looking order), so it always runs on the relaxed
+    schedule; contract B runs on the caller's levels, checked and cut into
+    sub-levels where the reference's in-level order matters
+    (glu_schedule_refine).  A schedule that puts a source column after its
+    target -- the reference would read an unfinished column -- raises
+    ScheduleHazardError instead of returning different bits."""
+    if level_of is None:
+        return _relaxed_levels(fp)
+    lv = _lib.i64(level_of)
+    key = (id(fp), _digest(lv), contract)
+    hit = _PHASES.get(key)
+    if hit is not None and hit[0]() is fp:
+        return hit[1]
+    out = _refine(fp, lv, contract)
+    _PHASES[key] = (weakref.ref(fp, lambda _r, k=key: _PHASES.pop(k, None)), out)
+    return out
+
+
+_PHASES: dict = {}
+
+
+def _refine(fp: FilledPattern, lv: np.ndarray, contract: int) -> np.ndarray:
+    if len(lv) != fp.n:
+        raise ValueError("level_of must have one entry per column")
+    out = np.empty(fp.n, dtype=np.int64)
+    bad = np.full(2, -1, dtype=np.int64)
+    cp, ri, dp = _lib.i64(fp.full.col_ptr), _lib.i64(fp.full.row_idx), _lib.i64(fp.diag_pos)
+    rp, ci = _lib.i64(fp.csr.row_ptr), _lib.i64(fp.csr.col_idx)
+    rc = _lib.check(_lib.lib.glu_schedule_refine(fp.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
+                                                 _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(lv), contract,
+                                                 _lib.ptr(out), _lib.ptr(bad)), "glu_schedule_refine")
+    if rc == _lib.GLU_ESTRUCT:
+        i, j = int(bad[0]), int(bad[1])
+        raise ScheduleHazardError([Hazard(writer=i, reader=j, element=(i, j), level=int(lv[j]))])
+    return _relaxed_levels(fp) if contract == _lib.CONTRACT_A else out
+
+
+def _factor(a: CscMatrix, fp: FilledPattern, level_of: np.ndarray | None, contract: int,
+            thresh: float, by_column: bool, stamps: bool = False) -> tuple[np.ndarray, Factorizer, np.ndarray]:
     _require_f64(a)
     if a.n != fp.n:
         raise PatternMismatchError("matrix and pattern sizes differ")
-    fz = get_factorizer(fp, level_of, contract)
+    phases = plan_levels(fp, level_of, contract)
+    fz = get_factorizer(fp, phases, contract)
     with fz._lock:
         fz.set_input(a.col_ptr, a.row_idx)
+        fz.set_fail_levels(phases if level_of is None or contract != _lib.CONTRACT_A else level_of)
         fz.set_option(2, 1 if by_column else 0)
-        fz.set_option(1, 0 if by_column else 1)
+        fz.set_option(1, 1 if stamps else 0)
         vals, rc = fz.factor_host(a.values, thresh)
     _check(rc)
-    return vals, fz
+    return vals, fz, phases
 
 
 def factor_left_looking(a: CscMatrix, fp: FilledPattern,
@@ -380,7 +475,7 @@ def factor_left_looking(a: CscMatrix, fp: FilledPattern,
     """Left-looking result (levlu/numeric.py:129-142), computed by the level
     kernel in contract-A order: bitwise the reference's values, failing
     pivot = first failing column."""
-    vals, _ = _factor(a, fp, _relaxed_levels(fp), _lib.CONTRACT_A, opts.zero_pivot_threshold, True)
+    vals, _, _ = _factor(a, fp, None, _lib.CONTRACT_A, opts.zero_pivot_threshold, True)
     return LuFactors(fp, vals)
 
 
@@ -421,16 +516,33 @@ def factor_parallel(a: CscMatrix, fp: FilledPattern, schedule: LevelSchedule,
         if hz:
             raise ScheduleHazardError(hz)
     contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
-    vals, fz = _factor(a, fp, schedule.level_of, contract, opts.zero_pivot_threshold, False)
+    stamps = os.environ.get("GLU_LEVEL_TIMES", "1") != "0"
+    vals, fz, phases = _factor(a, fp, schedule.level_of, contract, opts.zero_pivot_threshold, False,
+                               stamps=stamps)
     caps = [min(concurrency_cap(p, len(c), rm), opts.worker_count, len(c))
             for p, c in zip(plans, schedule.levels)]
     stats = FactorStats(
-        level_times=fz.level_times_s(),
+        level_times=_caller_level_times(fz.level_times_s() if stamps else [], phases,
+                                        schedule.level_of, schedule.level_count),
         level_modes=[p.mode.value for p in plans],
         flop_count=sum(_flops_cached(fp)),
         peak_concurrent_columns=max(caps) if caps else 0,
     )
     return LuFactors(fp, vals), stats
+
+
+def _caller_level_times(phase_s: list, phases: np.ndarray, level_of: np.ndarray, nlev: int) -> list:
+    """Per-level GPU times in the caller's schedule from the device's
+    per-phase times: a level completes when the last phase holding one of
+    its columns completes (the plan may run on refined or relaxed phases)."""
+    if not phase_s or len(phases) == 0:
+        return [0.0] * nlev
+    done = np.cumsum(np.asarray(phase_s, dtype=np.float64))
+    ph = np.minimum(np.asarray(phases, dtype=np.int64), len(done) - 1)
+    comp = np.zeros(nlev)
+    np.maximum.at(comp, np.asarray(level_of, dtype=np.int64), done[ph])
+    comp = np.maximum.accumulate(comp)
+    return np.diff(np.concatenate([[0.0], comp])).tolist()
 
 
 _FLOPS: dict = {}
@@ -449,10 +561,10 @@ def refactorize(lu: LuFactors, a_new: CscMatrix, schedule: LevelSchedule | None 
                 opts: FactorOptions = FactorOptions()) -> LuFactors:
     """New values, same pattern: reuses the device-resident
     pattern, plan and scatter map; only A's values cross the bus."""
-    level_of = schedule.level_of if schedule is not None else _relaxed_levels(lu.pattern)
+    level_of = schedule.level_of if schedule is not None else None
     contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
-    vals, _ = _factor(a_new, lu.pattern, level_of, contract, opts.zero_pivot_threshold,
-                      schedule is None)
+    vals, _, _ = _factor(a_new, lu.pattern, level_of, contract, opts.zero_pivot_threshold,
+                         schedule is None)
     return LuFactors(lu.pattern, vals)
 
 
@@ -471,11 +583,13 @@ def refactorize_batch(lu: LuFactors, a_pattern: CscMatrix, values: np.ndarray,
     vals = np.ascontiguousarray(values, dtype=np.float64)
     if vals.ndim != 2 or vals.shape[1] != len(a_pattern.row_idx):
         raise ValueError("values must be [batch, nz(A)]")
-    level_of = schedule.level_of if schedule is not None else _relaxed_levels(lu.pattern)
     contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
-    fz = get_factorizer(lu.pattern, level_of, contract, tail=False)
+    phases = plan_levels(lu.pattern, schedule.level_of if schedule is not None else None, contract)
+    fz = get_factorizer(lu.pattern, phases, contract, tail=False)
     with fz._lock:
         fz.set_input(a_pattern.col_ptr, a_pattern.row_idx)
+        fz.set_fail_levels(schedule.level_of if schedule is not None and contract == _lib.CONTRACT_A
+                           else phases)
         fz.set_option(2, 1 if schedule is None else 0)
         fz.set_option(1, 0)
         out, fails = fz.factor_batch_host(vals, opts.zero_pivot_threshold)

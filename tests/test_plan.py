@@ -151,3 +151,56 @@ def test_contract_a_defers_only_when_needed():
     pb = export_plan(fp, g["level_of"], _lib.CONTRACT_B)
     assert pb["info"][6] == 0
     assert 0 < pa["info"][6] < pa["info"][3]
+
+
+def _levels_arrays(level_of):
+    order = np.argsort(level_of, kind="stable")
+    counts = np.bincount(level_of)
+    return np.concatenate([[0], np.cumsum(counts)]).astype(np.int64), order.astype(np.int64)
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("workers", [1, 2])
+def test_upward_schedule_matches_reference(case, workers):
+    """factor_parallel accepts any LevelSchedule (levlu/numeric.py:241-351).
+    Under levelize(detect_upward(fp)) the reference's deterministic mode
+    still gives left-looking values, and its atomic mode reads multipliers
+    that same-level sources update first: the plan (contract A on the
+    relaxed schedule, contract B on the refined sub-levels) must give the
+    oracle's factor_parallel values bit for bit."""
+    from oracle import oracle as orc
+
+    g = load_golden(case)
+    a = csc_from_golden(g)
+    fp = glu.symbolic_fillin(a.pattern)
+    s = glu.levelize(glu.detect_upward(fp))
+    lp, lc = _levels_arrays(s.level_of)
+    pat = orc.Pattern.from_fp(fp)
+    thresh = float(g["thresh"])
+    for det, contract in ((True, _lib.CONTRACT_A), (False, _lib.CONTRACT_B)):
+        ref, bad = orc.scatter(pat, a.col_ptr, a.row_idx, a.values)
+        caps = np.full(len(lp) - 1, workers, dtype=np.int64)
+        err = orc.factor_parallel(pat, ref, lp, lc, caps, det, thresh)
+        phases = glu.numeric.plan_levels(fp, s.level_of, contract)
+        if contract == _lib.CONTRACT_B:
+            # sub-levels keep the caller's level order
+            assert np.all(np.diff(s.level_of[np.argsort(phases, kind="stable")]) >= 0)
+        plan = export_plan(fp, phases, contract)
+        v, _ = orc.scatter(pat, a.col_ptr, a.row_idx, a.values)
+        fail = emulate(fp, s.level_of if contract == _lib.CONTRACT_A else phases, plan, v, thresh,
+                       np.random.default_rng(1))
+        if err >= 0:
+            assert fail is not None and fail[1] == err
+        else:
+            assert fail is None and np.array_equal(v, ref), (case, det)
+
+
+def test_schedule_with_late_source_raises():
+    """A source column placed after its target: the reference would read an
+    unfinished column; the B200 path refuses instead of returning other bits."""
+    g = load_golden("conflict8")
+    fp = glu.symbolic_fillin(csc_from_golden(g).pattern)
+    lv = np.zeros(fp.n, dtype=np.int64)
+    lv[0] = 1  # column 0 is a source of column 1 (conflict8 deps)
+    with pytest.raises(glu.ScheduleHazardError):
+        glu.numeric.plan_levels(fp, lv, _lib.CONTRACT_A)

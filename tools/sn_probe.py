@@ -1,0 +1,96 @@
+"""Supernodal vs per-MAC engine on one config: device time per
+refactorization (CUDA events), plan size and setup time, bitwise parity vs
+the CPU oracle (factor_parallel deterministic on all host cores).
+
+    python tools/sn_probe.py g400 [cfg4 ...] [--engines sn,plan] [--reps 5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import pathlib
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("configs", nargs="+")
+    p.add_argument("--engines", default="sn,plan")
+    p.add_argument("--reps", type=int, default=5)
+    p.add_argument("--no-parity", action="store_true")
+    args = p.parse_args()
+    import torch
+
+    import paper_1908_00204_b200 as glu
+    from paper_1908_00204_b200 import numeric, synthetic
+    from oracle import oracle as orc
+
+    dev = torch.device("cuda", 0)
+    for name in args.configs:
+        t0 = time.perf_counter()
+        a = synthetic.make(name) if name in synthetic.CONFIGS else synthetic.grid5(int(name[1:]), seed=0)
+        fp = glu.symbolic_fillin(a.pattern)
+        lv = numeric._relaxed_levels(fp)
+        t_an = time.perf_counter() - t0
+        macs = numeric.pattern_flops(fp)[0]
+        ref = None
+        if not args.no_parity:
+            t0 = time.perf_counter()
+            pat = orc.Pattern.from_fp(fp)
+            ref, bad = orc.scatter(pat, a.col_ptr, a.row_idx, a.values)
+            s = glu.levelize(glu.detect_relaxed(fp))
+            lp = np.concatenate([[0], np.cumsum([len(c) for c in s.levels])]).astype(np.int64)
+            lc = np.concatenate(s.levels).astype(np.int64)
+            ncpu = orc.cpu_count()
+            caps = orc.concurrency_caps([int(x) for x in np.diff(lp)], ncpu, n=a.n)
+            assert orc.factor_parallel(pat, ref, lp, lc, caps, True) == -1
+            t_ref = time.perf_counter() - t0
+        for eng in args.engines.split(","):
+            if eng == "plan" and macs > 1.5e10:
+                continue
+            t0 = time.perf_counter()
+            fz = numeric.Factorizer(fp, lv, 0, engine=eng)
+            t_setup = time.perf_counter() - t0
+            fz.set_input(a.col_ptr, a.row_idx)
+            fz.set_option(1, 0)
+            fz.set_option(2, 1)
+            a_d = torch.from_numpy(a.values).to(dev)
+            v = torch.empty(fp.nnz, dtype=torch.float64, device=dev)
+            st = torch.cuda.current_stream()
+            ts = []
+            for r in range(args.reps + 1):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                fz.scatter_device(a_d, v, st)
+                e0.record(st)
+                fz.factor_device_async(v, 1e-14, st)
+                e1.record(st)
+                torch.cuda.synchronize()
+                rc = fz.status(st)
+                assert rc == -1, rc
+                if r:
+                    ts.append(e0.elapsed_time(e1))
+            out = v.cpu().numpy()
+            par = None
+            if ref is not None:
+                par = "bitwise" if np.array_equal(out, ref) else \
+                    f"MISMATCH max|d|={np.max(np.abs(out - ref)):.3e} n_diff={int(np.sum(out != ref))}"
+            rec = dict(config=name, engine=eng, n=a.n, nnz=fp.nnz, macs=macs, analysis_s=round(t_an, 2),
+                       setup_s=round(t_setup, 2), ms=min(ts), ms_all=[round(x, 3) for x in ts],
+                       parity=par, plan=fz.plan_info.get("plan_bytes"),
+                       sn=getattr(fz, "sn_info", None), device_bytes=fz.handle_info["device_bytes"],
+                       ref_s=round(t_ref, 2) if ref is not None else None)
+            print(json.dumps(rec), flush=True)
+            fz.close()
+            del v, a_d
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
