@@ -154,7 +154,8 @@ void glu_sn_plan_info(const glu_plan *p, int64_t *info);
 /* Copies a supernodal plan out (sizes from glu_sn_plan_info; int32 x4
    records): sn {s0, s1, |R_S|, first pair}, pan {p0, p1, supernode, rows
    below}, pairs {k, a, base, map}, relmap, push {panel, pair0, pair1,
-   target panel}, tasks {index, chunk, kind, phase}, phase_ptr[phases+1],
+   target panel}, tasks (2 records each) {kind << 28 | chunk, phase, p0, p1,
+   s1, rows below the panel, pair0, pair1}, phase_ptr[phases+1],
    col_a[n].  Any pointer may be NULL. */
 void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *pairs,
                         int32_t *relmap, int32_t *push, int32_t *tasks, int32_t *phase_ptr,
@@ -194,6 +195,11 @@ int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value);
    which may differ from the one the plan was built on (contract A plans
    on the relaxed schedule). */
 int64_t glu_set_fail_levels(glu_handle *h, const int64_t *level_of);
+/* Diagnostics of the supernodal engine: after glu_set_option(h, 15, 1),
+   out[0] = kernel start and out[1 + p] = completion of phase p
+   (%globaltimer ns) of the last factorization.  Returns the words written
+   (0 for a per-MAC handle). */
+int64_t glu_sn_stamps(glu_handle *h, int64_t *out, int64_t max);
 /* Diagnostics: glu_set_option(h, 3, first_phase) and (h, 4, n_phases)
    record, for every item of those phases, 8 words {item | phase << 32,
    warp, t_start, t_static_loaded, t_wait_done, t_values_loaded,

@@ -1177,7 +1177,7 @@ extern "C" void glu_sn_plan_info(const glu_plan *p, int64_t *info) {
     info[2] = (i64)s->pairs.size();
     info[3] = (i64)s->relmap.size();
     info[4] = (i64)s->push.size();
-    info[5] = (i64)s->tasks.size();
+    info[5] = (i64)s->tasks.size() / 2;
     info[6] = (i64)s->phase_ptr.size() - 1;
     info[7] = s->n_stages;
     info[8] = s->macs;

@@ -90,7 +90,7 @@ struct SnPlan {
     std::vector<I4> pairs;   // per (supernode S, target column k): {k, a, base, map}
     std::vector<int32_t> relmap;  // positions of R_S's rows in column k (absolute slots)
     std::vector<I4> push;    // {source panel, first pair, end pair, target panel}
-    std::vector<I4> tasks;   // {index, chunk, kind, phase} in phase order
+    std::vector<I4> tasks;   // 2 per task, phase order: {kind << 28 | chunk, phase, p0, p1}, {s1, h, pair0, pair1}
     std::vector<int32_t> phase_ptr;  // tasks of phase p: [phase_ptr[p], phase_ptr[p+1])
     std::vector<int32_t> col_a;      // per column c: first row of c's supernode present in c
     int64_t n_stages = 0;
@@ -132,6 +132,8 @@ struct SnDev;
 int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
 void sn_free(SnDev *d);
 int sn_grid(int sm_count);
+int64_t sn_set_stamps(SnDev *d, bool on);
+int64_t sn_read_stamps(SnDev *d, int64_t *out, int64_t max);
 // one factorization of v (A_s values after the scatter); pivot failures
 // are min-reduced into *fail as (fail_level << 32 | column) or column
 int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *diag_pos,

@@ -308,19 +308,24 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         if (remap[f] >= 0) P->phase_ptr[remap[f] + 1] = (i32)cnt[f];
     for (i64 f = 0; f < live; f++) P->phase_ptr[f + 1] += P->phase_ptr[f];
     std::vector<i32> fill(P->phase_ptr.begin(), P->phase_ptr.end() - 1);
-    P->tasks.resize(total);
-    auto put = [&](i64 f, i32 idx, i32 chunk, i32 kind) {
+    // two records per task: {kind << 28 | chunk, phase, p0, p1}, {s1, rows below p1, pair0, pair1}
+    P->tasks.resize(2 * total);
+    auto put = [&](i64 f, i32 pi, i32 chunk, i32 kind, i32 r0, i32 r1) {
         const i32 ph = remap[f];
-        P->tasks[fill[ph]++] = I4{idx, chunk, kind, ph};
+        const I4 pn = P->pan[pi];
+        const i64 at = 2 * (i64)fill[ph]++;
+        P->tasks[at] = I4{(kind << 28) | chunk, ph, pn.x, pn.y};
+        P->tasks[at + 1] = I4{(i32)s1_of(pn.z), pn.w, r0, r1};
     };
     for (i64 p = 0; p < np; p++) {
-        put(3 * fstage[p], (i32)p, 0, kSnDiag);
-        for (i64 c = 0; c < chunks(P->pan[p].w); c++) put(3 * fstage[p] + 1, (i32)p, (i32)c, kSnTrsm);
+        put(3 * fstage[p], (i32)p, 0, kSnDiag, 0, 0);
+        for (i64 c = 0; c < chunks(P->pan[p].w); c++) put(3 * fstage[p] + 1, (i32)p, (i32)c, kSnTrsm, 0, 0);
     }
     for (i64 x = 0; x < npush; x++) {
-        if (push_tri[x]) put(3 * push_stage[x] + 1, (i32)x, 0, kSnTri);
-        for (i64 c = 0; c < chunks(P->pan[P->push[x].x].w); c++)
-            put(3 * push_stage[x] + 2, (i32)x, (i32)c, kSnRect);
+        const I4 ps = P->push[x];
+        if (push_tri[x]) put(3 * push_stage[x] + 1, ps.x, 0, kSnTri, ps.y, ps.z);
+        for (i64 c = 0; c < chunks(P->pan[ps.x].w); c++)
+            put(3 * push_stage[x] + 2, ps.x, (i32)c, kSnRect, ps.y, ps.z);
     }
     return GLU_OK;
 }

@@ -39,17 +39,21 @@ namespace {
 constexpr int kSnThreads = 256;
 constexpr int kSnWarps = kSnThreads / 32;
 constexpr int kDoneStride = 8;  // u32 words between phase counters
+constexpr int kGdoneRep = 8;    // replicas of the phases-complete counter (spread the pollers)
+constexpr int kLine = 32;       // u32 words per 128-byte line
 constexpr unsigned long long kSnWatchdogNs = 4000000000ull;
 
 struct SnParams {
     double *v;
     const i32 *col_ptr, *diag_pos, *col_a, *fail_level;
-    const int4 *sn, *pan, *pairs, *push, *tasks;
+    const int4 *pairs, *tasks;  // tasks: 2 records each (glu_internal.h SnPlan::tasks)
     const i32 *relmap, *phase_ptr;
     i32 n_tasks;
-    unsigned *done;
+    unsigned *done;   // per phase: counted tasks (kDoneStride apart)
+    unsigned *gdone;  // phases complete, kGdoneRep replicas kLine apart
     unsigned long long *cmax;
     int *err;
+    unsigned long long *stamps;  // optional: [0] kernel start, [1 + p] completion of phase p
 };
 
 __device__ __forceinline__ double ldv(const double *p) { return __ldcg(p); }
@@ -62,13 +66,12 @@ __device__ __forceinline__ unsigned long long absbits(double x) {
     const double a = fabs(x);
     return a == a ? (unsigned long long)__double_as_longlong(a) : 0ull;
 }
+// max over the warp of non-negative double bit patterns: (hi, lo) lexicographic
 __device__ __forceinline__ unsigned long long warp_max(unsigned long long m) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
-        m = y > m ? y : m;
-    }
-    return m;
+    const unsigned hi = (unsigned)(m >> 32);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)m : 0u);
+    return ((unsigned long long)mh << 32) | ml;
 }
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -86,74 +89,81 @@ struct WarpSmem {
     int clo[kSnW];             // per panel column: first panel row present
 };
 
-// first panel row present in column p0 + c (U rows of a supernode are a suffix)
-__device__ __forceinline__ int panel_clo(const SnParams &P, int p0, int c) {
-    return max(__ldg(P.col_a + p0 + c) - p0, 0);
+// Panel metadata, lane = panel column: its diagonal slot and the first
+// panel row present in it (a supernode's U rows in a column are a suffix).
+// Loaded lane-parallel so the block loads below issue back to back.
+__device__ __forceinline__ void panel_cols(const SnParams &P, int p0, int w, int lane, int &dc, int &clo) {
+    dc = 0;
+    clo = kSnW;
+    if (lane < w) {
+        dc = __ldg(P.diag_pos + p0 + lane);
+        clo = max(__ldg(P.col_a + p0 + lane) - p0, 0);
+    }
 }
 
-// DIAG: column maxima above the block, then the w x w block factored in
-// shared memory: step j divides column j below the diagonal and updates
-// every later column (lanes = rows), each element receiving j ascending.
-__device__ void task_diag(const SnParams &P, WarpSmem &S, int pi, int lane) {
-    const int4 pn = __ldg(P.pan + pi);
-    const int p0 = pn.x, w = pn.y - pn.x;
+// DIAG: the w x w block of the panel, lane = block row r holding its row
+// in registers.  Step j: row j is final for columns >= j (U part), lane j
+// broadcasts it; every lane r > j takes column j's undivided value (the
+// column maximum over the block's L part -- the U rows are taken by the
+// check pass), divides it by the pivot and updates its later columns, so
+// every element receives its sources j in ascending order.
+__device__ void task_diag(const SnParams &P, int4 ta, int lane) {
+    const int p0 = ta.z, w = ta.w - ta.z;
+    int dcl, clol;
+    panel_cols(P, p0, w, lane, dcl, clol);
+    double x[kSnW];
+#pragma unroll
+    for (int c = 0; c < kSnW; c++) {
+        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
+        x[c] = (c < w && lane < w && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
+    }
     unsigned long long mymax = 0;
-    for (int c = 0; c < w; c++) {
-        const int dc = __ldg(P.diag_pos + p0 + c);
-        const int clo = panel_clo(P, p0, c);
-        if (lane == 0) S.clo[c] = clo;
-        const int pre_end = dc - (c - clo);
-        unsigned long long m = 0;
-        for (int q = __ldg(P.col_ptr + p0 + c) + lane; q < pre_end; q += 32) {
-            const unsigned long long b = absbits(ldv(P.v + q));
-            m = b > m ? b : m;
+#pragma unroll
+    for (int j = 0; j < kSnW; j++) {
+        if (j < w) {
+            const unsigned long long m = warp_max(lane > j && lane < w ? absbits(x[j]) : 0ull);
+            if (lane == j) mymax = m;
+            const double piv = __shfl_sync(0xffffffffu, x[j], j);
+            const bool below = lane > j && lane < w;
+            const double l = __ddiv_rn(x[j], piv);
+            if (below) x[j] = l;
+#pragma unroll
+            for (int c = j + 1; c < kSnW; c++) {
+                if (c < w) {
+                    const double ujc = __shfl_sync(0xffffffffu, x[c], j);
+                    const int clo = __shfl_sync(0xffffffffu, clol, c);
+                    if (below && j >= clo) x[c] = msub(x[c], l, ujc);
+                }
+            }
         }
-        m = warp_max(m);
-        if (lane == c) mymax = m;
-        if (lane < w && lane >= clo) S.b[c][lane] = ldv(P.v + dc + (lane - c));
     }
-    __syncwarp();
-    for (int j = 0; j < w; j++) {
-        const int cj = S.clo[j];
-        const unsigned long long m = warp_max(lane < w && lane >= cj ? absbits(S.b[j][lane]) : 0ull);
-        if (lane == j) mymax = m > mymax ? m : mymax;
-        const double piv = S.b[j][j];
-        if (lane > j && lane < w) S.b[j][lane] = __ddiv_rn(S.b[j][lane], piv);
-        __syncwarp();
-        if (lane > j && lane < w) {
-            const double l = S.b[j][lane];
-            for (int c = j + 1; c < w; c++)
-                if (j >= S.clo[c]) S.b[c][lane] = msub(S.b[c][lane], l, S.b[c][j]);
-        }
-        __syncwarp();
+#pragma unroll
+    for (int c = 0; c < kSnW; c++) {
+        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
+        if (c < w && lane < w && lane >= clo) stv(P.v + dc + (lane - c), x[c]);
     }
-    for (int c = 0; c < w; c++) {
-        const int clo = S.clo[c];
-        if (lane < w && lane >= clo) stv(P.v + __ldg(P.diag_pos + p0 + c) + (lane - c), S.b[c][lane]);
-    }
-    if (lane < w) atomicMax(P.cmax + p0 + lane, mymax);
-    __syncwarp();
+    if (lane < w && mymax) atomicMax(P.cmax + p0 + lane, mymax);
 }
 
 // TRSM: 32 rows below the panel; lane = row, the row's w values in
 // registers; step j takes the undivided value's maximum, divides, and
 // updates the later columns with U(j, c) from the factored block.
-__device__ void task_trsm(const SnParams &P, WarpSmem &S, int pi, int chunk, int lane) {
-    const int4 pn = __ldg(P.pan + pi);
-    const int p0 = pn.x, p1 = pn.y, w = p1 - p0, h = pn.w;
-    for (int c = 0; c < w; c++) {
-        const int dc = __ldg(P.diag_pos + p0 + c);
-        const int clo = panel_clo(P, p0, c);
-        if (lane == 0) S.clo[c] = clo;
-        if (lane <= c && lane >= clo) S.b[c][lane] = ldv(P.v + dc + (lane - c));
-    }
-    __syncwarp();
+__device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
+    const int chunk = ta.x & 0x0fffffff;
+    const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
+    int dcl, clol;
+    panel_cols(P, p0, w, lane, dcl, clol);
+    S.clo[lane] = clol;
     const int t = chunk * 32 + lane;
     const bool act = t < h;
     double x[kSnW];
 #pragma unroll
-    for (int c = 0; c < kSnW; c++)
-        x[c] = (act && c < w) ? ldv(P.v + __ldg(P.diag_pos + p0 + c) + (p1 - p0 - c) + t) : 0.0;
+    for (int c = 0; c < kSnW; c++) {
+        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
+        if (c < w && lane <= c && lane >= clo) S.b[c][lane] = ldv(P.v + dc + (lane - c));
+        x[c] = (act && c < w) ? ldv(P.v + dc + (p1 - p0 - c) + t) : 0.0;
+    }
+    __syncwarp();
     unsigned long long mymax = 0;
 #pragma unroll
     for (int j = 0; j < kSnW; j++) {
@@ -169,32 +179,36 @@ __device__ void task_trsm(const SnParams &P, WarpSmem &S, int pi, int chunk, int
     }
     if (act) {
 #pragma unroll
-        for (int c = 0; c < kSnW; c++)
-            if (c < w) stv(P.v + __ldg(P.diag_pos + p0 + c) + (p1 - p0 - c) + t, x[c]);
+        for (int c = 0; c < kSnW; c++) {
+            const int dc = __shfl_sync(0xffffffffu, dcl, c);
+            if (c < w) stv(P.v + dc + (p1 - p0 - c) + t, x[c]);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < kSnW; c++) (void)__shfl_sync(0xffffffffu, dcl, c);
     }
-    if (lane < w) atomicMax(P.cmax + p0 + lane, mymax);
+    if (lane < w && mymax) atomicMax(P.cmax + p0 + lane, mymax);
     __syncwarp();
 }
 
 // TRI: U(P, k) for every target column k of the push (lane = column):
 // forward substitution with the panel's unit-lower block, j ascending.
-__device__ void task_tri(const SnParams &P, WarpSmem &S, int xi, int lane) {
-    const int4 ps = __ldg(P.push + xi);
-    const int4 pn = __ldg(P.pan + ps.x);
-    const int p0 = pn.x, p1 = pn.y, w = p1 - p0;
-    const int s1 = __ldg(P.sn + pn.z).y;
-    for (int j = 0; j < w; j++)
-        if (lane > j && lane < w) S.b[j][lane] = ldv(P.v + __ldg(P.diag_pos + p0 + j) + (lane - j));
-    __syncwarp();
-    const int q = ps.y + lane;
+__device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
+    const int p0 = ta.z, p1 = ta.w, w = p1 - p0, s1 = tb.x;
+    const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
+    const int q = tb.z + lane;
     int4 pr = make_int4(0, p1, 0, -1);
-    if (q < ps.z) pr = __ldg(P.pairs + q);
+    if (q < tb.w) pr = __ldg(P.pairs + q);
     const bool act = pr.y < p1;
     const int lo = max(pr.y - p0, 0);
     double u[kSnW];
 #pragma unroll
-    for (int r = 0; r < kSnW; r++)
-        u[r] = (act && r < w && r >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + r))) : 0.0;
+    for (int j = 0; j < kSnW; j++) {
+        const int dj = __shfl_sync(0xffffffffu, dcl, j);
+        if (j < w && lane > j && lane < w) S.b[j][lane] = ldv(P.v + dj + (lane - j));
+        u[j] = (act && j < w && j >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + j))) : 0.0;
+    }
+    __syncwarp();
 #pragma unroll
     for (int j = 0; j < kSnW; j++) {
         if (j < w && act && j >= lo) {
@@ -213,112 +227,197 @@ __device__ void task_tri(const SnParams &P, WarpSmem &S, int xi, int lane) {
 }
 
 // RECT: 32 rows below the source panel into every target column of the
-// push: lane = row, its divided L row in registers, U(j, k) broadcast by
-// shuffle, the chain over j ascending.
-__device__ void task_rect(const SnParams &P, int xi, int chunk, int lane) {
-    const int4 ps = __ldg(P.push + xi);
-    const int4 pn = __ldg(P.pan + ps.x);
-    const int p0 = pn.x, p1 = pn.y, w = p1 - p0, h = pn.w;
-    const int4 sn = __ldg(P.sn + pn.z);
-    const int s1 = sn.y, in_sn = s1 - p1;
+// push: lane = row, its divided L row in registers; target columns in
+// batches of kRectB (their U(j, k), target slots and values loaded
+// together, kRectB independent chains per lane), U(j, k) broadcast by
+// shuffle, each chain over j ascending.
+constexpr int kRectB = 4;
+
+__device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
+    const int chunk = ta.x & 0x0fffffff;
+    const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
+    const int s1 = tb.x, in_sn = s1 - p1;
     const int t = chunk * 32 + lane;
     const bool act = t < h;
+    const int npair = tb.w - tb.z;
+    int4 myp = make_int4(0, p1, 0, -1);
+    if (lane < npair) myp = __ldg(P.pairs + tb.z + lane);
+    const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
     double L[kSnW];
 #pragma unroll
-    for (int j = 0; j < kSnW; j++)
-        L[j] = (act && j < w) ? ldv(P.v + __ldg(P.diag_pos + p0 + j) + (p1 - p0 - j) + t) : 0.0;
-    for (int q = ps.y; q < ps.z; q++) {
-        const int4 pr = __ldg(P.pairs + q);
-        if (pr.y >= p1) continue;
-        const int lo = max(pr.y - p0, 0);
-        const double uval = (lane < w && lane >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + lane))) : 0.0;
-        int pos = 0;
-        if (act) {
-            if (t < in_sn) pos = pr.z - (in_sn - t);
-            else pos = pr.w >= 0 ? __ldg(P.relmap + pr.w + (t - in_sn)) : pr.z + (t - in_sn);
+    for (int j = 0; j < kSnW; j++) {
+        const int dj = __shfl_sync(0xffffffffu, dcl, j);
+        L[j] = (act && j < w) ? ldv(P.v + dj + (p1 - p0 - j) + t) : 0.0;
+    }
+    for (int q0 = 0; q0 < npair; q0 += kRectB) {
+        double uv[kRectB], x[kRectB];
+        int pos[kRectB], lo[kRectB];
+#pragma unroll
+        for (int b = 0; b < kRectB; b++) {
+            const int q = q0 + b;
+            const int a = __shfl_sync(0xffffffffu, myp.y, q & 31);
+            const int base = __shfl_sync(0xffffffffu, myp.z, q & 31);
+            const int map = __shfl_sync(0xffffffffu, myp.w, q & 31);
+            const bool ok = q < npair && a < p1;
+            lo[b] = ok ? max(a - p0, 0) : kSnW;
+            uv[b] = (ok && lane < w && lane >= lo[b]) ? ldv(P.v + base - (s1 - (p0 + lane))) : 0.0;
+            pos[b] = -1;
+            if (ok && act)
+                pos[b] = t < in_sn ? base - (in_sn - t)
+                                   : (map >= 0 ? __ldg(P.relmap + map + (t - in_sn)) : base + (t - in_sn));
         }
-        double x = act ? ldv(P.v + pos) : 0.0;
+#pragma unroll
+        for (int b = 0; b < kRectB; b++) x[b] = pos[b] >= 0 ? ldv(P.v + pos[b]) : 0.0;
 #pragma unroll
         for (int j = 0; j < kSnW; j++) {
-            if (j < w && j >= lo) {
-                const double uj = __shfl_sync(0xffffffffu, uval, j);
-                x = msub(x, L[j], uj);
+            if (j < w) {
+#pragma unroll
+                for (int b = 0; b < kRectB; b++) {
+                    if (j >= lo[b]) {
+                        const double uj = __shfl_sync(0xffffffffu, uv[b], j);
+                        x[b] = msub(x[b], L[j], uj);
+                    }
+                }
             }
         }
-        if (act) stv(P.v + pos, x);
+#pragma unroll
+        for (int b = 0; b < kRectB; b++)
+            if (pos[b] >= 0) stv(P.v + pos[b], x[b]);
     }
+}
+
+// A warp leaving phase p counts its tasks of p (release: fence, then add);
+// the warp that completes p advances the phases-complete counter.  Phases
+// complete in order (a phase's tasks start after the previous one
+// completed), and atomicMax keeps the counter monotone.
+__device__ __forceinline__ void flush_phase(const SnParams &P, int p, unsigned mine) {
+    __threadfence();
+    const unsigned old = atomicAdd(P.done + (size_t)p * kDoneStride, mine);
+    if (old + mine == (unsigned)(__ldg(P.phase_ptr + p + 1) - __ldg(P.phase_ptr + p))) {
+        if (P.stamps) P.stamps[1 + p] = globaltimer();
+#pragma unroll
+        for (int r = 0; r < kGdoneRep; r++) atomicMax(P.gdone + r * kLine, (unsigned)(p + 1));
+    }
+}
+
+struct CtaSync {
+    int known;  // phases known complete (from the last poll of this CTA)
+    int lock;   // one polling warp per CTA at a time
+};
+
+// Wait until phases [0, p) are complete.  Warps of a CTA share one poller:
+// the others read the CTA's last observation from shared memory, so an
+// SM sends at most one poll at a time to the (replicated) global counter
+// instead of one per waiting warp.  False on the watchdog / error path.
+__device__ bool wait_phase(const SnParams &P, CtaSync *cs, int p, int lane) {
+    bool ok = true;
+    if (lane == 0) {
+        volatile int *known = &cs->known;
+        if (*known < p) {
+            const unsigned *g = P.gdone + (blockIdx.x % kGdoneRep) * kLine;
+            const unsigned long long t0 = globaltimer();
+            while (*known < p) {
+                if (atomicCAS(&cs->lock, 0, 1) == 0) {
+                    const int seen = (int)ld_acquire(g);
+                    atomicMax(&cs->known, seen);
+                    atomicExch(&cs->lock, 0);
+                    if (seen >= p) break;
+                }
+                if (*(volatile int *)P.err) { ok = false; break; }
+                if (globaltimer() - t0 > kSnWatchdogNs) {
+                    atomicExch(P.err, 1);
+                    ok = false;
+                    break;
+                }
+                __nanosleep(32);
+            }
+        }
+        __threadfence_block();
+    }
+    return __shfl_sync(0xffffffffu, (int)ok, 0) != 0;
 }
 
 __global__ void __launch_bounds__(kSnThreads, 2) sn_kernel(SnParams P) {
     extern __shared__ __align__(16) unsigned char sn_smem_raw[];
     WarpSmem *smem = reinterpret_cast<WarpSmem *>(sn_smem_raw);
+    __shared__ CtaSync cs;
+    if (threadIdx.x == 0) {
+        cs.known = 0;
+        cs.lock = 0;
+        if (P.stamps && blockIdx.x == 0) P.stamps[0] = globaltimer();
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem &S = smem[wib];
     const int nw = gridDim.x * kSnWarps;
     int cur = -1;
     unsigned mine = 0;
-    for (int i = wib * gridDim.x + blockIdx.x; i < P.n_tasks; i += nw) {
-        const int4 tk = __ldg(P.tasks + i);
-        if (tk.w != cur) {
+    int i = wib * gridDim.x + blockIdx.x;
+    int4 ta = make_int4(0, 0, 0, 0), tb = ta;
+    if (i < P.n_tasks) {
+        ta = __ldg(P.tasks + 2 * (size_t)i);
+        tb = __ldg(P.tasks + 2 * (size_t)i + 1);
+    }
+    while (i < P.n_tasks) {
+        // the next task's records load while this one runs
+        const int inext = i + nw;
+        int4 na = ta, nb = tb;
+        if (inext < P.n_tasks) {
+            na = __ldg(P.tasks + 2 * (size_t)inext);
+            nb = __ldg(P.tasks + 2 * (size_t)inext + 1);
+        }
+        if (ta.y != cur) {
             if (mine) {
                 __syncwarp();
-                if (lane == 0) {
-                    __threadfence();
-                    atomicAdd(P.done + (size_t)cur * kDoneStride, mine);
-                }
+                if (lane == 0) flush_phase(P, cur, mine);
             }
             mine = 0;
-            cur = tk.w;
-            if (cur > 0) {
-                bool bail = false;
-                if (lane == 0) {
-                    const unsigned need = (unsigned)(__ldg(P.phase_ptr + cur) - __ldg(P.phase_ptr + cur - 1));
-                    const unsigned *ctr = P.done + (size_t)(cur - 1) * kDoneStride;
-                    if (ld_acquire(ctr) < need) {
-                        const unsigned long long t0 = globaltimer();
-                        while (ld_acquire(ctr) < need) {
-                            if (*(volatile int *)P.err) { bail = true; break; }
-                            __nanosleep(64);
-                            if (globaltimer() - t0 > kSnWatchdogNs) {
-                                atomicExch(P.err, 1);
-                                bail = true;
-                                break;
-                            }
-                        }
-                    }
-                }
-                if (__shfl_sync(0xffffffffu, (int)bail, 0)) return;
-            }
+            cur = ta.y;
+            if (cur > 0 && !wait_phase(P, &cs, cur, lane)) return;
         }
-        switch (tk.z) {
-            case kSnDiag: task_diag(P, S, tk.x, lane); break;
-            case kSnTrsm: task_trsm(P, S, tk.x, tk.y, lane); break;
-            case kSnTri: task_tri(P, S, tk.x, lane); break;
-            default: task_rect(P, tk.x, tk.y, lane); break;
+        switch (ta.x >> 28) {
+            case kSnDiag: task_diag(P, ta, lane); break;
+            case kSnTrsm: task_trsm(P, S, ta, tb, lane); break;
+            case kSnTri: task_tri(P, S, ta, tb, lane); break;
+            default: task_rect(P, ta, tb, lane); break;
         }
         mine++;
+        i = inext;
+        ta = na;
+        tb = nb;
     }
     if (mine) {
         __syncwarp();
-        if (lane == 0) {
-            __threadfence();
-            atomicAdd(P.done + (size_t)cur * kDoneStride, mine);
-        }
+        if (lane == 0) flush_phase(P, cur, mine);
     }
 }
 
-// pivot test of every column (_kernels.py:60-65): |piv| <= thresh * cmax
-__global__ void sn_check_kernel(const double *v, const i32 *diag_pos, const unsigned long long *cmax,
-                                const i32 *fail_level, i32 n, double thresh, int by_column,
-                                unsigned long long *fail) {
-    for (i32 c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-        const double piv = __ldcg(v + diag_pos[c]);
-        const double cm = __longlong_as_double((long long)cmax[c]);
-        if (fabs(piv) <= __dmul_rn(thresh, cm)) {
-            const unsigned long long key =
-                by_column ? (unsigned long long)c
-                          : (((unsigned long long)__ldg(fail_level + c)) << 32) | (unsigned)c;
-            atomicMin(fail, key);
+// pivot test of every column (_kernels.py:60-65): |piv| <= thresh * cmax.
+// One warp per column adds the maximum over its final U part and diagonal
+// (rows <= c, never divided) to the undivided-L maxima the tasks gathered.
+__global__ void sn_check_kernel(const double *v, const i32 *col_ptr, const i32 *diag_pos,
+                                const unsigned long long *cmax, const i32 *fail_level, i32 n,
+                                double thresh, int by_column, unsigned long long *fail) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (i32 c = gw; c < n; c += nw) {
+        const int d = __ldg(diag_pos + c);
+        unsigned long long m = 0;
+        for (int q = __ldg(col_ptr + c) + lane; q <= d; q += 32) {
+            const unsigned long long b = absbits(__ldcg(v + q));
+            m = b > m ? b : m;
+        }
+        m = warp_max(m);
+        if (lane == 0) {
+            const unsigned long long l = cmax[c];
+            m = l > m ? l : m;
+            const double piv = __ldcg(v + d);
+            if (fabs(piv) <= __dmul_rn(thresh, __longlong_as_double((long long)m))) {
+                const unsigned long long key =
+                    by_column ? (unsigned long long)c
+                              : (((unsigned long long)__ldg(fail_level + c)) << 32) | (unsigned)c;
+                atomicMin(fail, key);
+            }
         }
     }
 }
@@ -336,11 +435,12 @@ cudaError_t up(T **dst, const std::vector<T> &src, i64 *bytes) {
 }  // namespace
 
 struct SnDev {
-    int4 *sn = nullptr, *pan = nullptr, *pairs = nullptr, *push = nullptr, *tasks = nullptr;
+    int4 *pairs = nullptr, *tasks = nullptr;
     i32 *relmap = nullptr, *phase_ptr = nullptr, *col_a = nullptr;
     i64 n = 0, n_tasks = 0, n_phases = 0;
-    unsigned *done = nullptr;
+    unsigned *done = nullptr, *gdone = nullptr;
     unsigned long long *cmax = nullptr;
+    unsigned long long *stamps = nullptr;  // per-phase completion times (diagnostics)
     int grid = 0;
 };
 
@@ -357,8 +457,8 @@ int sn_grid(int sm_count) {
 
 void sn_free(SnDev *d) {
     if (!d) return;
-    void *ptrs[] = {d->sn, d->pan, d->pairs, d->push, d->tasks, d->relmap, d->phase_ptr, d->col_a,
-                    d->done, d->cmax};
+    void *ptrs[] = {d->pairs, d->tasks, d->relmap, d->phase_ptr, d->col_a, d->done, d->gdone, d->cmax,
+                    d->stamps};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete d;
@@ -372,19 +472,17 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
     };
     static_assert(sizeof(I4) == sizeof(int4), "I4 layout");
     cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = up(&d->sn, cast(p->sn), bytes);
-    if (e == cudaSuccess) e = up(&d->pan, cast(p->pan), bytes);
     if (e == cudaSuccess) e = up(&d->pairs, cast(p->pairs), bytes);
-    if (e == cudaSuccess) e = up(&d->push, cast(p->push), bytes);
     if (e == cudaSuccess) e = up(&d->tasks, cast(p->tasks), bytes);
     if (e == cudaSuccess) e = up(&d->relmap, p->relmap, bytes);
     if (e == cudaSuccess) e = up(&d->phase_ptr, p->phase_ptr, bytes);
     if (e == cudaSuccess) e = up(&d->col_a, p->col_a, bytes);
     d->n = p->n;
-    d->n_tasks = (i64)p->tasks.size();
+    d->n_tasks = (i64)p->tasks.size() / 2;
     d->n_phases = (i64)p->phase_ptr.size() - 1;
     if (e == cudaSuccess)
         e = cudaMalloc((void **)&d->done, sizeof(unsigned) * kDoneStride * std::max<i64>(d->n_phases, 1));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->gdone, sizeof(unsigned) * kGdoneRep * kLine);
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->cmax, sizeof(unsigned long long) * std::max<i64>(d->n, 1));
     if (e != cudaSuccess) {
         set_error(std::string("supernodal plan upload: ") + cudaGetErrorString(e));
@@ -404,11 +502,35 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
     return GLU_OK;
 }
 
+int64_t sn_set_stamps(SnDev *d, bool on) {
+    if (on && !d->stamps) {
+        if (cudaMalloc((void **)&d->stamps, sizeof(unsigned long long) * (d->n_phases + 1)) != cudaSuccess) {
+            set_error("cudaMalloc(phase stamps)");
+            return GLU_ECUDA;
+        }
+    } else if (!on && d->stamps) {
+        cudaFree(d->stamps);
+        d->stamps = nullptr;
+    }
+    return GLU_OK;
+}
+
+int64_t sn_read_stamps(SnDev *d, int64_t *out, int64_t max) {
+    if (!d->stamps) return 0;
+    const i64 m = std::min<i64>(max, d->n_phases + 1);
+    std::vector<unsigned long long> h((size_t)m);
+    if (cudaMemcpy(h.data(), d->stamps, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return GLU_ECUDA;
+    for (i64 i = 0; i < m; i++) out[i] = (int64_t)h[i];
+    return m;
+}
+
 int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *diag_pos,
                   const int32_t *fail_level, int32_t n, double thresh, bool by_column,
                   unsigned long long *fail, int *err, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(d->done, 0, sizeof(unsigned) * kDoneStride * std::max<i64>(d->n_phases, 1), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d->gdone, 0, sizeof(unsigned) * kGdoneRep * kLine, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d->cmax, 0, sizeof(unsigned long long) * std::max<i64>(d->n, 1), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(err, 0, sizeof(int), s);
     if (e != cudaSuccess) {
@@ -422,17 +544,16 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         P.diag_pos = diag_pos;
         P.col_a = d->col_a;
         P.fail_level = fail_level;
-        P.sn = d->sn;
-        P.pan = d->pan;
         P.pairs = d->pairs;
-        P.push = d->push;
         P.tasks = d->tasks;
+        P.gdone = d->gdone;
         P.relmap = d->relmap;
         P.phase_ptr = d->phase_ptr;
         P.n_tasks = (i32)d->n_tasks;
         P.done = d->done;
         P.cmax = d->cmax;
         P.err = err;
+        P.stamps = d->stamps;
         void *args[] = {&P};
         e = cudaLaunchCooperativeKernel((const void *)sn_kernel, dim3(d->grid), dim3(kSnThreads), args, kSnSmem, s);
         if (e != cudaSuccess) {
@@ -441,8 +562,8 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         }
     }
     if (n > 0) {
-        sn_check_kernel<<<std::min<i64>((n + 255) / 256, 1184), 256, 0, s>>>(v, diag_pos, d->cmax, fail_level, n,
-                                                                            thresh, by_column ? 1 : 0, fail);
+        sn_check_kernel<<<std::min<i64>((n + 7) / 8, 4736), 256, 0, s>>>(v, col_ptr, diag_pos, d->cmax, fail_level,
+                                                                        n, thresh, by_column ? 1 : 0, fail);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             set_error(std::string("sn_check_kernel: ") + cudaGetErrorString(e));

@@ -37,7 +37,7 @@ def build(fp, level_of=None):
         ns, npan, npair, nmap, npush, ntask, nph = (int(x) for x in info[:7])
         arr = dict(sn=np.zeros((ns, 4), np.int32), pan=np.zeros((npan, 4), np.int32),
                    pairs=np.zeros((npair, 4), np.int32), relmap=np.zeros(nmap, np.int32),
-                   push=np.zeros((npush, 4), np.int32), tasks=np.zeros((ntask, 4), np.int32),
+                   push=np.zeros((npush, 4), np.int32), tasks=np.zeros((ntask, 8), np.int32),
                    phase_ptr=np.zeros(nph + 1, np.int32), col_a=np.zeros(n, np.int32))
         _lib.lib.glu_sn_plan_export(plan, *(_lib.ptr(arr[k]) for k in
                                             ("sn", "pan", "pairs", "relmap", "push", "tasks",
@@ -74,7 +74,7 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
     n = fp.n
     v = np.array(v, dtype=np.float64)
     cmax = np.zeros(n)
-    sn, pan, pairs, relmap, push = plan["sn"], plan["pan"], plan["pairs"], plan["relmap"], plan["push"]
+    pairs, relmap = plan["pairs"], plan["relmap"]
     col_a = plan["col_a"]
     tasks, pptr = plan["tasks"], plan["phase_ptr"]
 
@@ -86,11 +86,11 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
     for ph in range(len(pptr) - 1):
         E = _Phase(v.copy())
         for ti in range(pptr[ph], pptr[ph + 1]):
-            idx, chunk, kind, tph = (int(x) for x in tasks[ti])
+            kc, tph, p0, p1, s1, h, r0, r1 = (int(x) for x in tasks[ti])
+            kind, chunk = kc >> 28, kc & ((1 << 28) - 1)
             assert tph == ph
             E.task = ti
             if kind == 0:  # DIAG
-                p0, p1, S, h = (int(x) for x in pan[idx])
                 w = p1 - p0
                 clo = [max(int(col_a[p0 + c]) - p0, 0) for c in range(w)]
                 B = {}
@@ -114,7 +114,6 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
                     for r in range(clo[c], w):
                         E.wr(int(dp[p0 + c]) + r - c, B[c, r])
             elif kind == 1:  # TRSM
-                p0, p1, S, h = (int(x) for x in pan[idx])
                 w = p1 - p0
                 clo = [max(int(col_a[p0 + c]) - p0, 0) for c in range(w)]
                 U = {}
@@ -133,10 +132,7 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
                     for c in range(w):
                         E.wr(int(dp[p0 + c]) + (p1 - p0 - c) + t, x[c])
             elif kind == 2:  # TRI
-                P, r0, r1, K = (int(x) for x in push[idx])
-                p0, p1, S, h = (int(x) for x in pan[P])
                 w = p1 - p0
-                s1 = int(sn[S][1])
                 Lb = {(j, r): E.rd(int(dp[p0 + j]) + r - j) for j in range(w) for r in range(j + 1, w)}
                 for q in range(r0, r1):
                     k, a, base, mp = (int(x) for x in pairs[q])
@@ -150,10 +146,7 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
                     for r in range(lo + 1, w):
                         E.wr(base - (s1 - (p0 + r)), u[r])
             else:  # RECT
-                P, r0, r1, K = (int(x) for x in push[idx])
-                p0, p1, S, h = (int(x) for x in pan[P])
                 w = p1 - p0
-                s1 = int(sn[S][1])
                 in_sn = s1 - p1
                 rows = range(chunk * 32, min(h, chunk * 32 + 32))
                 L = {t: [E.rd(int(dp[p0 + j]) + (p1 - p0 - j) + t) for j in range(w)] for t in rows}

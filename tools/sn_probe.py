@@ -19,12 +19,54 @@ ROOT = pathlib.Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
+def phase_profile(fz, fp, a_d, v, st):
+    """Per-phase durations from the kernel's completion stamps, grouped by
+    the kind of tasks the phase holds (0 DIAG, 1 TRSM/TRI, 2 RECT)."""
+    import torch
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    import sn_emul
+    from paper_1908_00204_b200 import _lib
+
+    plan = sn_emul.build(fp)
+    fz.set_option(15, 1)
+    fz.scatter_device(a_d, v, st)
+    fz.factor_device_async(v, 1e-14, st)
+    torch.cuda.synchronize()
+    nph = len(plan["phase_ptr"]) - 1
+    buf = np.zeros(nph + 1, dtype=np.int64)
+    _lib.lib.glu_sn_stamps(fz.handle, _lib.ptr(buf), nph + 1)
+    fz.set_option(15, 0)
+    dur = np.diff(buf).astype(np.float64) * 1e-3  # us
+    tasks, pp = plan["tasks"], plan["phase_ptr"]
+    kinds = np.array([int(tasks[pp[p], 0]) >> 28 for p in range(nph)])
+    kinds = np.where(kinds == 2, 1, np.where(kinds == 3, 2, kinds))
+    ntask = np.diff(pp)
+    out = {"total_us": float(dur.sum()), "phases": nph}
+    for k, name in ((0, "diag"), (1, "trsm_tri"), (2, "rect")):
+        d = dur[kinds == k]
+        if len(d):
+            out[name] = {"n": int(len(d)), "sum_us": float(d.sum()), "median_us": float(np.median(d)),
+                         "p90_us": float(np.percentile(d, 90)), "max_us": float(d.max()),
+                         "tasks_median": float(np.median(ntask[kinds == k]))}
+    # phases by task count
+    for lo, hi in ((1, 1), (2, 8), (9, 64), (65, 512), (513, 1 << 30)):
+        m = (ntask >= lo) & (ntask <= hi)
+        if m.any():
+            out[f"tasks_{lo}_{hi}"] = {"n": int(m.sum()), "sum_us": float(dur[m].sum()),
+                                       "median_us": float(np.median(dur[m]))}
+    top = np.argsort(dur)[::-1][:8]
+    out["top"] = [(int(p), int(kinds[p]), int(ntask[p]), round(float(dur[p]), 1)) for p in top]
+    return out
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("configs", nargs="+")
     p.add_argument("--engines", default="sn,plan")
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--no-parity", action="store_true")
+    p.add_argument("--stamps", action="store_true", help="per-phase completion profile (sn)")
     args = p.parse_args()
     import torch
 
@@ -77,6 +119,9 @@ def main():
                 if r:
                     ts.append(e0.elapsed_time(e1))
             out = v.cpu().numpy()
+            prof = None
+            if args.stamps and eng == "sn":
+                prof = phase_profile(fz, fp, a_d, v, st)
             par = None
             if ref is not None:
                 par = "bitwise" if np.array_equal(out, ref) else \
@@ -85,7 +130,7 @@ def main():
                        setup_s=round(t_setup, 2), ms=min(ts), ms_all=[round(x, 3) for x in ts],
                        parity=par, plan=fz.plan_info.get("plan_bytes"),
                        sn=getattr(fz, "sn_info", None), device_bytes=fz.handle_info["device_bytes"],
-                       ref_s=round(t_ref, 2) if ref is not None else None)
+                       ref_s=round(t_ref, 2) if ref is not None else None, phases=prof)
             print(json.dumps(rec), flush=True)
             fz.close()
             del v, a_d
