@@ -200,6 +200,9 @@ int64_t glu_set_fail_levels(glu_handle *h, const int64_t *level_of);
    (%globaltimer ns) of the last factorization.  Returns the words written
    (0 for a per-MAC handle). */
 int64_t glu_sn_stamps(glu_handle *h, int64_t *out, int64_t max);
+/* glu_set_option(h, 15, 2) also records, per task, {iteration start, wait
+   done, executed, 0} (%globaltimer ns); read with glu_sn_trace. */
+int64_t glu_sn_trace(glu_handle *h, int64_t *out, int64_t max_tasks);
 /* Diagnostics: glu_set_option(h, 3, first_phase) and (h, 4, n_phases)
    record, for every item of those phases, 8 words {item | phase << 32,
    warp, t_start, t_static_loaded, t_wait_done, t_values_loaded,

@@ -53,6 +53,7 @@ SIGNATURES = {
     "glu_schedule_refine": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p]),
     "glu_set_fail_levels": (_i64, [_p, _p]),
     "glu_sn_stamps": (_i64, [_p, _p, _i64]),
+    "glu_sn_trace": (_i64, [_p, _p, _i64]),
     "glu_plan_info": (None, [_p, _p]),
     "glu_trace_read": (_i64, [_p, _p, _i64]),
     "glu_tail_trace_read": (_i64, [_p, _p, _i64]),

@@ -2345,7 +2345,7 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             return GLU_OK;
         case 15:  // diagnostics: supernodal engine per-phase completion stamps (glu_sn_stamps)
             if (!h->sn) { glu::set_error("option 15 needs a supernodal handle"); return GLU_EINVAL; }
-            return glu::sn_set_stamps(h->sn, value != 0);
+            return glu::sn_set_stamps(h->sn, (int)value);
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
             return GLU_OK;
@@ -2358,6 +2358,11 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
 extern "C" int64_t glu_sn_stamps(glu_handle *h, int64_t *out, int64_t max) {
     if (!h->sn) return 0;
     return glu::sn_read_stamps(h->sn, out, max);
+}
+
+extern "C" int64_t glu_sn_trace(glu_handle *h, int64_t *out, int64_t max_tasks) {
+    if (!h->sn) return 0;
+    return glu::sn_read_trace(h->sn, out, max_tasks);
 }
 
 extern "C" int64_t glu_set_fail_levels(glu_handle *h, const int64_t *level_of) {

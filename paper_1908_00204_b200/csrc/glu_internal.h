@@ -132,7 +132,8 @@ struct SnDev;
 int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
 void sn_free(SnDev *d);
 int sn_grid(int sm_count);
-int64_t sn_set_stamps(SnDev *d, bool on);
+int64_t sn_set_stamps(SnDev *d, int mode);
+int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks);
 int64_t sn_read_stamps(SnDev *d, int64_t *out, int64_t max);
 // one factorization of v (A_s values after the scatter); pivot failures
 // are min-reduced into *fail as (fail_level << 32 | column) or column

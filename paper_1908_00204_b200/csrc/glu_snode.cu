@@ -54,6 +54,7 @@ struct SnParams {
     unsigned long long *cmax;
     int *err;
     unsigned long long *stamps;  // optional: [0] kernel start, [1 + p] completion of phase p
+    unsigned long long *trace;   // optional: per task {iteration start, wait done, executed, 0}
 };
 
 __device__ __forceinline__ double ldv(const double *p) { return __ldcg(p); }
@@ -87,6 +88,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 struct WarpSmem {
     double b[kSnW][kSnW + 1];  // panel block, column-major [column][row]
     int clo[kSnW];             // per panel column: first panel row present
+    double pad[16 * kSnW - kSnW + 8];  // RectSmem (task_rect_tile) overlays this region
 };
 
 // Panel metadata, lane = panel column: its diagonal slot and the first
@@ -101,44 +103,52 @@ __device__ __forceinline__ void panel_cols(const SnParams &P, int p0, int w, int
     }
 }
 
+// The unrolled task variants below run every loop to the class width WM
+// without per-width branches: registers of columns / rows >= w hold
+// garbage that is never stored (and never feeds a stored value -- a column
+// only receives updates from lower columns), so the FP64 chains are free
+// of branches and the compiler can interleave them.  Structural
+// predicates that change stored values (a supernode's partial U suffix,
+// col_a) become selects, never a subtraction of a zero product: x - l * 0
+// is not always x (x = -0 with l < 0, or l = inf).
+
 // DIAG: the w x w block of the panel, lane = block row r holding its row
 // in registers.  Step j: row j is final for columns >= j (U part), lane j
 // broadcasts it; every lane r > j takes column j's undivided value (the
 // column maximum over the block's L part -- the U rows are taken by the
 // check pass), divides it by the pivot and updates its later columns, so
 // every element receives its sources j in ascending order.
+template <int WM>
 __device__ void task_diag(const SnParams &P, int4 ta, int lane) {
     const int p0 = ta.z, w = ta.w - ta.z;
     int dcl, clol;
     panel_cols(P, p0, w, lane, dcl, clol);
-    double x[kSnW];
+    const bool full = __all_sync(0xffffffffu, clol <= 0 || lane >= w);
+    double x[WM];
 #pragma unroll
-    for (int c = 0; c < kSnW; c++) {
+    for (int c = 0; c < WM; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
         x[c] = (c < w && lane < w && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
     }
     unsigned long long mymax = 0;
 #pragma unroll
-    for (int j = 0; j < kSnW; j++) {
-        if (j < w) {
-            const unsigned long long m = warp_max(lane > j && lane < w ? absbits(x[j]) : 0ull);
-            if (lane == j) mymax = m;
-            const double piv = __shfl_sync(0xffffffffu, x[j], j);
-            const bool below = lane > j && lane < w;
-            const double l = __ddiv_rn(x[j], piv);
-            if (below) x[j] = l;
+    for (int j = 0; j < WM; j++) {
+        const bool below = lane > j && lane < w;
+        const unsigned long long m = warp_max(below ? absbits(x[j]) : 0ull);
+        if (lane == j) mymax = m;
+        const double piv = __shfl_sync(0xffffffffu, x[j], j);
+        const double l = __ddiv_rn(x[j], piv);
+        x[j] = below ? l : x[j];
 #pragma unroll
-            for (int c = j + 1; c < kSnW; c++) {
-                if (c < w) {
-                    const double ujc = __shfl_sync(0xffffffffu, x[c], j);
-                    const int clo = __shfl_sync(0xffffffffu, clol, c);
-                    if (below && j >= clo) x[c] = msub(x[c], l, ujc);
-                }
-            }
+        for (int c = j + 1; c < WM; c++) {
+            const double ujc = __shfl_sync(0xffffffffu, x[c], j);
+            const double y = msub(x[c], l, ujc);
+            if (full) x[c] = below ? y : x[c];
+            else x[c] = (below && j >= __shfl_sync(0xffffffffu, clol, c)) ? y : x[c];
         }
     }
 #pragma unroll
-    for (int c = 0; c < kSnW; c++) {
+    for (int c = 0; c < WM; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
         if (c < w && lane < w && lane >= clo) stv(P.v + dc + (lane - c), x[c]);
     }
@@ -147,45 +157,48 @@ __device__ void task_diag(const SnParams &P, int4 ta, int lane) {
 
 // TRSM: 32 rows below the panel; lane = row, the row's w values in
 // registers; step j takes the undivided value's maximum, divides, and
-// updates the later columns with U(j, c) from the factored block.
+// updates the later columns with U(j, c) from the factored block (shared
+// memory, broadcast reads).
+template <int WM>
 __device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
     const int chunk = ta.x & 0x0fffffff;
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     int dcl, clol;
     panel_cols(P, p0, w, lane, dcl, clol);
     S.clo[lane] = clol;
+    const bool full = __all_sync(0xffffffffu, clol <= 0 || lane >= w);
     const int t = chunk * 32 + lane;
     const bool act = t < h;
-    double x[kSnW];
+    double x[WM];
 #pragma unroll
-    for (int c = 0; c < kSnW; c++) {
+    for (int c = 0; c < WM; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
-        if (c < w && lane <= c && lane >= clo) S.b[c][lane] = ldv(P.v + dc + (lane - c));
+        S.b[c][lane] = (c < w && lane <= c && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
         x[c] = (act && c < w) ? ldv(P.v + dc + (p1 - p0 - c) + t) : 0.0;
     }
     __syncwarp();
     unsigned long long mymax = 0;
 #pragma unroll
-    for (int j = 0; j < kSnW; j++) {
-        if (j < w) {
-            const unsigned long long m = warp_max(act ? absbits(x[j]) : 0ull);
-            if (lane == j) mymax = m;
-            const double d = __ddiv_rn(x[j], S.b[j][j]);
-            x[j] = d;
+    for (int j = 0; j < WM; j++) {
+        const unsigned long long m = warp_max(act && j < w ? absbits(x[j]) : 0ull);
+        if (lane == j) mymax = m;
+        const double d = __ddiv_rn(x[j], S.b[j][j]);
+        x[j] = d;
+        if (full) {
 #pragma unroll
-            for (int c = j + 1; c < kSnW; c++)
-                if (c < w && j >= S.clo[c]) x[c] = msub(x[c], d, S.b[c][j]);
+            for (int c = j + 1; c < WM; c++) x[c] = msub(x[c], d, S.b[c][j]);
+        } else {
+#pragma unroll
+            for (int c = j + 1; c < WM; c++) {
+                const double y = msub(x[c], d, S.b[c][j]);
+                x[c] = j >= S.clo[c] ? y : x[c];
+            }
         }
     }
-    if (act) {
 #pragma unroll
-        for (int c = 0; c < kSnW; c++) {
-            const int dc = __shfl_sync(0xffffffffu, dcl, c);
-            if (c < w) stv(P.v + dc + (p1 - p0 - c) + t, x[c]);
-        }
-    } else {
-#pragma unroll
-        for (int c = 0; c < kSnW; c++) (void)__shfl_sync(0xffffffffu, dcl, c);
+    for (int c = 0; c < WM; c++) {
+        const int dc = __shfl_sync(0xffffffffu, dcl, c);
+        if (act && c < w) stv(P.v + dc + (p1 - p0 - c) + t, x[c]);
     }
     if (lane < w && mymax) atomicMax(P.cmax + p0 + lane, mymax);
     __syncwarp();
@@ -193,6 +206,7 @@ __device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int 
 
 // TRI: U(P, k) for every target column k of the push (lane = column):
 // forward substitution with the panel's unit-lower block, j ascending.
+template <int WM>
 __device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, s1 = tb.x;
     const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
@@ -201,38 +215,39 @@ __device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int l
     if (q < tb.w) pr = __ldg(P.pairs + q);
     const bool act = pr.y < p1;
     const int lo = max(pr.y - p0, 0);
-    double u[kSnW];
+    double u[WM];
 #pragma unroll
-    for (int j = 0; j < kSnW; j++) {
+    for (int j = 0; j < WM; j++) {
         const int dj = __shfl_sync(0xffffffffu, dcl, j);
-        if (j < w && lane > j && lane < w) S.b[j][lane] = ldv(P.v + dj + (lane - j));
+        S.b[j][lane] = (j < w && lane > j && lane < w) ? ldv(P.v + dj + (lane - j)) : 0.0;
         u[j] = (act && j < w && j >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + j))) : 0.0;
     }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < kSnW; j++) {
-        if (j < w && act && j >= lo) {
-            const double uj = u[j];
+    for (int j = 0; j < WM; j++) {
+        const double uj = u[j];
+        const bool on = j >= lo;
 #pragma unroll
-            for (int r = j + 1; r < kSnW; r++)
-                if (r < w) u[r] = msub(u[r], S.b[j][r], uj);
+        for (int r = j + 1; r < WM; r++) {
+            const double y = msub(u[r], S.b[j][r], uj);
+            u[r] = on ? y : u[r];
         }
     }
     if (act) {
 #pragma unroll
-        for (int r = 0; r < kSnW; r++)
+        for (int r = 0; r < WM; r++)
             if (r < w && r > lo) stv(P.v + pr.z - (s1 - (p0 + r)), u[r]);
     }
     __syncwarp();
 }
 
-// RECT: 32 rows below the source panel into every target column of the
-// push: lane = row, its divided L row in registers; target columns in
-// batches of kRectB (their U(j, k), target slots and values loaded
-// together, kRectB independent chains per lane), U(j, k) broadcast by
-// shuffle, each chain over j ascending.
+// RECT for narrow panels (WM <= 8): lane = row, its divided L row in
+// registers; target columns in batches of kRectB (their U(j, k), target
+// slots and values loaded together, kRectB independent chains per lane),
+// U(j, k) broadcast by shuffle, each chain over j ascending.
 constexpr int kRectB = 4;
 
+template <int WM>
 __device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
     const int chunk = ta.x & 0x0fffffff;
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
@@ -243,9 +258,9 @@ __device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
     int4 myp = make_int4(0, p1, 0, -1);
     if (lane < npair) myp = __ldg(P.pairs + tb.z + lane);
     const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
-    double L[kSnW];
+    double L[WM];
 #pragma unroll
-    for (int j = 0; j < kSnW; j++) {
+    for (int j = 0; j < WM; j++) {
         const int dj = __shfl_sync(0xffffffffu, dcl, j);
         L[j] = (act && j < w) ? ldv(P.v + dj + (p1 - p0 - j) + t) : 0.0;
     }
@@ -259,7 +274,7 @@ __device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
             const int base = __shfl_sync(0xffffffffu, myp.z, q & 31);
             const int map = __shfl_sync(0xffffffffu, myp.w, q & 31);
             const bool ok = q < npair && a < p1;
-            lo[b] = ok ? max(a - p0, 0) : kSnW;
+            lo[b] = ok ? max(a - p0, 0) : WM;
             uv[b] = (ok && lane < w && lane >= lo[b]) ? ldv(P.v + base - (s1 - (p0 + lane))) : 0.0;
             pos[b] = -1;
             if (ok && act)
@@ -269,21 +284,150 @@ __device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
 #pragma unroll
         for (int b = 0; b < kRectB; b++) x[b] = pos[b] >= 0 ? ldv(P.v + pos[b]) : 0.0;
 #pragma unroll
-        for (int j = 0; j < kSnW; j++) {
-            if (j < w) {
+        for (int j = 0; j < WM; j++) {
 #pragma unroll
-                for (int b = 0; b < kRectB; b++) {
-                    if (j >= lo[b]) {
-                        const double uj = __shfl_sync(0xffffffffu, uv[b], j);
-                        x[b] = msub(x[b], L[j], uj);
-                    }
-                }
+            for (int b = 0; b < kRectB; b++) {
+                const double uj = __shfl_sync(0xffffffffu, uv[b], j);
+                const double y = msub(x[b], L[j], uj);
+                x[b] = (j >= lo[b] && j < w) ? y : x[b];
             }
         }
 #pragma unroll
         for (int b = 0; b < kRectB; b++)
             if (pos[b] >= 0) stv(P.v + pos[b], x[b]);
     }
+}
+
+// RECT for wide panels (w > 8): register-tiled blocks C[32 rows x 16
+// target columns] -= L[32 x w] * U[w x 16] (two halves for > 16 target
+// columns), every element's chain over j ascending.  Lane (ry, cx) =
+// (lane / 4, lane % 4) holds rows ry + 8 i and columns cx + 4 k (i, k < 4);
+// per j it reads 4 L and 4 U values from shared memory (conflict-free
+// broadcasts) for 16 MACs.  Columns whose U suffix starts inside the panel
+// (lo > 0, only in structurally unsymmetric patterns) take the select path.
+struct RectSmem {
+    double l[kSnW][kSnW];  // [j][row]
+    double u[kSnW][16];    // [j][column of the half]
+    int lo[16];
+};
+
+static_assert(sizeof(RectSmem) <= sizeof(WarpSmem), "RectSmem overlays WarpSmem");
+
+__device__ void task_rect_tile(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int lane) {
+    const int chunk = ta.x & 0x0fffffff;
+    const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
+    const int s1 = tb.x, in_sn = s1 - p1;
+    const int npair = tb.w - tb.z;
+    const int t = chunk * 32 + lane;
+    int4 myp = make_int4(0, p1, 0, -1);
+    if (lane < npair) myp = __ldg(P.pairs + tb.z + lane);
+    const bool colok = lane < npair && myp.y < p1;
+    const int mylo = colok ? max(myp.y - p0, 0) : kSnW;
+    const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
+#pragma unroll 8
+    for (int j = 0; j < kSnW; j++) {
+        const int dj = __shfl_sync(0xffffffffu, dcl, j);
+        R.l[j][lane] = (t < h && j < w) ? ldv(P.v + dj + (p1 - p0 - j) + t) : 0.0;
+    }
+    const int ry = lane >> 2, cx = lane & 3;
+    for (int half = 0; half * 16 < npair; half++) {
+        const int qh = lane - 16 * half;  // this lane's column in the half (lanes 16h .. 16h+15)
+        __syncwarp();
+        if (qh >= 0 && qh < 16) {
+            R.lo[qh] = mylo;
+#pragma unroll 8
+            for (int j = 0; j < kSnW; j++)
+                R.u[j][qh] = (colok && j < w && j >= mylo) ? ldv(P.v + myp.z - (s1 - (p0 + j))) : 0.0;
+        }
+        const bool anylo = __any_sync(0xffffffffu, qh >= 0 && qh < 16 && colok && mylo > 0);
+        double c[4][4];
+        int pos[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int q = 16 * half + cx + 4 * k;
+            const int base = __shfl_sync(0xffffffffu, myp.z, q & 31), map = __shfl_sync(0xffffffffu, myp.w, q & 31);
+            const bool cok = __shfl_sync(0xffffffffu, (int)colok, q & 31) != 0 && q < 32;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int tt = chunk * 32 + ry + 8 * i;
+                int ps = -1;
+                if (cok && tt < h)
+                    ps = tt < in_sn ? base - (in_sn - tt)
+                                    : (map >= 0 ? __ldg(P.relmap + map + (tt - in_sn)) : base + (tt - in_sn));
+                pos[i][k] = ps;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int i = 0; i < 4; i++) c[i][k] = pos[i][k] >= 0 ? ldv(P.v + pos[i][k]) : 0.0;
+        __syncwarp();
+        if (!anylo) {
+#pragma unroll 4
+            for (int j = 0; j < w; j++) {
+                double l[4], u[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
+#pragma unroll
+                for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int k = 0; k < 4; k++) c[i][k] = msub(c[i][k], l[i], u[k]);
+            }
+        } else {
+            int clo[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) clo[k] = R.lo[cx + 4 * k];
+            for (int j = 0; j < w; j++) {
+                double l[4], u[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
+#pragma unroll
+                for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const double y = msub(c[i][k], l[i], u[k]);
+                        c[i][k] = j >= clo[k] ? y : c[i][k];
+                    }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                if (pos[i][k] >= 0) stv(P.v + pos[i][k], c[i][k]);
+    }
+    __syncwarp();
+}
+
+// Panel widths in classes 1, 2, 4, 8, 16, 32: every task runs the variant
+// unrolled for its class, so the code a phase executes stays small (one
+// fully unrolled 32-wide kernel is ~700 KB of SASS, far beyond the
+// instruction cache, and most panels are one column wide).
+template <int WM>
+__device__ __forceinline__ void run_kind(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
+    switch (ta.x >> 28) {
+        case kSnDiag: task_diag<WM>(P, ta, lane); break;
+        case kSnTrsm: task_trsm<WM>(P, S, ta, tb, lane); break;
+        case kSnTri: task_tri<WM>(P, S, ta, tb, lane); break;
+        default:
+            if (WM > 8) task_rect_tile(P, *reinterpret_cast<RectSmem *>(&S), ta, tb, lane);
+            else task_rect<WM>(P, ta, tb, lane);
+            break;
+    }
+}
+
+__device__ __forceinline__ void run_task(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
+    const int w = ta.w - ta.z;
+    if (w <= 1) run_kind<1>(P, S, ta, tb, lane);
+    else if (w <= 2) run_kind<2>(P, S, ta, tb, lane);
+    else if (w <= 4) run_kind<4>(P, S, ta, tb, lane);
+    else if (w <= 8) run_kind<8>(P, S, ta, tb, lane);
+    else if (w <= 16) run_kind<16>(P, S, ta, tb, lane);
+    else run_kind<32>(P, S, ta, tb, lane);
 }
 
 // A warp leaving phase p counts its tasks of p (release: fence, then add);
@@ -366,6 +510,8 @@ __global__ void __launch_bounds__(kSnThreads, 2) sn_kernel(SnParams P) {
             na = __ldg(P.tasks + 2 * (size_t)inext);
             nb = __ldg(P.tasks + 2 * (size_t)inext + 1);
         }
+        unsigned long long t_start = 0;
+        if (P.trace) t_start = globaltimer();
         if (ta.y != cur) {
             if (mine) {
                 __syncwarp();
@@ -375,11 +521,15 @@ __global__ void __launch_bounds__(kSnThreads, 2) sn_kernel(SnParams P) {
             cur = ta.y;
             if (cur > 0 && !wait_phase(P, &cs, cur, lane)) return;
         }
-        switch (ta.x >> 28) {
-            case kSnDiag: task_diag(P, ta, lane); break;
-            case kSnTrsm: task_trsm(P, S, ta, tb, lane); break;
-            case kSnTri: task_tri(P, S, ta, tb, lane); break;
-            default: task_rect(P, ta, tb, lane); break;
+        unsigned long long t_wait = 0;
+        if (P.trace) t_wait = globaltimer();
+        run_task(P, S, ta, tb, lane);
+        if (P.trace && lane == 0) {
+            __syncwarp(1u);
+            unsigned long long *tr = P.trace + 4 * (size_t)i;
+            tr[0] = t_start;
+            tr[1] = t_wait;
+            tr[2] = globaltimer();
         }
         mine++;
         i = inext;
@@ -441,6 +591,7 @@ struct SnDev {
     unsigned *done = nullptr, *gdone = nullptr;
     unsigned long long *cmax = nullptr;
     unsigned long long *stamps = nullptr;  // per-phase completion times (diagnostics)
+    unsigned long long *trace = nullptr;   // per-task timestamps (diagnostics)
     int grid = 0;
 };
 
@@ -458,7 +609,7 @@ int sn_grid(int sm_count) {
 void sn_free(SnDev *d) {
     if (!d) return;
     void *ptrs[] = {d->pairs, d->tasks, d->relmap, d->phase_ptr, d->col_a, d->done, d->gdone, d->cmax,
-                    d->stamps};
+                    d->stamps, d->trace};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete d;
@@ -502,17 +653,36 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
     return GLU_OK;
 }
 
-int64_t sn_set_stamps(SnDev *d, bool on) {
-    if (on && !d->stamps) {
+int64_t sn_set_stamps(SnDev *d, int mode) {
+    // 1: per-phase stamps, 2: + per-task trace, 0: off
+    if (mode && !d->stamps) {
         if (cudaMalloc((void **)&d->stamps, sizeof(unsigned long long) * (d->n_phases + 1)) != cudaSuccess) {
             set_error("cudaMalloc(phase stamps)");
             return GLU_ECUDA;
         }
-    } else if (!on && d->stamps) {
+    } else if (!mode && d->stamps) {
         cudaFree(d->stamps);
         d->stamps = nullptr;
     }
+    if (mode == 2 && !d->trace) {
+        if (cudaMalloc((void **)&d->trace, sizeof(unsigned long long) * 4 * std::max<i64>(d->n_tasks, 1)) !=
+            cudaSuccess) {
+            set_error("cudaMalloc(task trace)");
+            return GLU_ECUDA;
+        }
+    } else if (mode != 2 && d->trace) {
+        cudaFree(d->trace);
+        d->trace = nullptr;
+    }
     return GLU_OK;
+}
+
+int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks) {
+    if (!d->trace) return 0;
+    const i64 m = std::min<i64>(max_tasks, d->n_tasks);
+    if (cudaMemcpy(out, d->trace, sizeof(unsigned long long) * 4 * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return GLU_ECUDA;
+    return m;
 }
 
 int64_t sn_read_stamps(SnDev *d, int64_t *out, int64_t max) {
@@ -554,6 +724,7 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         P.cmax = d->cmax;
         P.err = err;
         P.stamps = d->stamps;
+        P.trace = d->trace;
         void *args[] = {&P};
         e = cudaLaunchCooperativeKernel((const void *)sn_kernel, dim3(d->grid), dim3(kSnThreads), args, kSnSmem, s);
         if (e != cudaSuccess) {

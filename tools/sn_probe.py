@@ -29,13 +29,16 @@ def phase_profile(fz, fp, a_d, v, st):
     from paper_1908_00204_b200 import _lib
 
     plan = sn_emul.build(fp)
-    fz.set_option(15, 1)
+    fz.set_option(15, 2)
     fz.scatter_device(a_d, v, st)
     fz.factor_device_async(v, 1e-14, st)
     torch.cuda.synchronize()
     nph = len(plan["phase_ptr"]) - 1
     buf = np.zeros(nph + 1, dtype=np.int64)
     _lib.lib.glu_sn_stamps(fz.handle, _lib.ptr(buf), nph + 1)
+    ntasks = len(plan["tasks"])
+    tr = np.zeros((ntasks, 4), dtype=np.int64)
+    _lib.lib.glu_sn_trace(fz.handle, _lib.ptr(tr), ntasks)
     fz.set_option(15, 0)
     dur = np.diff(buf).astype(np.float64) * 1e-3  # us
     tasks, pp = plan["tasks"], plan["phase_ptr"]
@@ -55,6 +58,43 @@ def phase_profile(fz, fp, a_d, v, st):
         if m.any():
             out[f"tasks_{lo}_{hi}"] = {"n": int(m.sum()), "sum_us": float(dur[m].sum()),
                                        "median_us": float(np.median(dur[m]))}
+    # per phase: wake (previous phase complete -> first / last task past its
+    # wait), execution (longest task), flush (last task done -> phase complete)
+    ph_of = np.repeat(np.arange(nph), ntask)
+    t1, t2 = tr[:, 1].astype(np.float64), tr[:, 2].astype(np.float64)
+    first_wait = np.full(nph, np.inf)
+    last_wait = np.zeros(nph)
+    last_done = np.zeros(nph)
+    exec_max = np.zeros(nph)
+    np.minimum.at(first_wait, ph_of, t1)
+    np.maximum.at(last_wait, ph_of, t1)
+    np.maximum.at(last_done, ph_of, t2)
+    np.maximum.at(exec_max, ph_of, t2 - t1)
+    prev = buf[:-1].astype(np.float64)
+    comp = {"wake_first_us": (first_wait - prev) * 1e-3, "wake_last_us": (last_wait - prev) * 1e-3,
+            "exec_max_us": exec_max * 1e-3, "flush_us": (buf[1:] - last_done) * 1e-3}
+    for k, x in comp.items():
+        out[k] = {"sum": float(x.sum()), "median": float(np.median(x)), "p90": float(np.percentile(x, 90))}
+    kinds_t = (tasks[:, 0] >> 28)
+    for k, name in ((0, "diag"), (1, "trsm"), (2, "tri"), (3, "rect")):
+        m = kinds_t == k
+        if m.any():
+            d = (t2[m] - t1[m]) * 1e-3
+            out[f"task_{name}_us"] = {"n": int(m.sum()), "median": float(np.median(d)),
+                                     "p90": float(np.percentile(d, 90)), "max": float(d.max())}
+    wd = tasks[:, 3] - tasks[:, 2]
+    wcls = np.select([wd <= 1, wd <= 2, wd <= 4, wd <= 8, wd <= 16], [1, 2, 4, 8, 16], 32)
+    npair = tasks[:, 7] - tasks[:, 6]
+    by = {}
+    for k, name in ((0, "diag"), (1, "trsm"), (2, "tri"), (3, "rect")):
+        for wc in (1, 2, 4, 8, 16, 32):
+            m = (kinds_t == k) & (wcls == wc)
+            if m.any():
+                d = (t2[m] - t1[m]) * 1e-3
+                by[f"{name}{wc}"] = [int(m.sum()), round(float(np.median(d)), 2),
+                                     round(float(np.percentile(d, 90)), 2), round(float(d.max()), 2),
+                                     round(float(npair[m].mean()), 1)]
+    out["by_kind_width[n,med,p90,max,npair]"] = by
     top = np.argsort(dur)[::-1][:8]
     out["top"] = [(int(p), int(kinds[p]), int(ntask[p]), round(float(dur[p]), 1)) for p in top]
     return out
