@@ -70,7 +70,7 @@ static_assert(sizeof(DeepRef) == 16, "DeepRef layout");
 // U(c-1,c) != 0), whose columns share the rows R_S below the supernode, and
 // cut into panels of <= kSnW columns.  Index records are 16-byte vectors.
 // ---------------------------------------------------------------------------
-constexpr int kSnW = 32;  // panel width: one warp lane per panel column / row
+constexpr int kSnW = 16;  // panel width: one warp lane per panel column / row
 
 struct alignas(16) I4 {
     int32_t x, y, z, w;

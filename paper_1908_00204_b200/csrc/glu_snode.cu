@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -85,18 +86,32 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     return v;
 }
 
+constexpr int kB = 32;  // lanes: shared-memory block dimension
 struct WarpSmem {
-    double b[kSnW][kSnW + 1];  // panel block, column-major [column][row]
-    int clo[kSnW];             // per panel column: first panel row present
-    double pad[16 * kSnW - kSnW + 8];  // RectSmem (task_rect_tile) overlays this region
+    double b[kB][kB + 1];  // panel block, column-major [column][row]
+    int clo[kB];           // per panel column: first panel row present
+    double pad[16 * kB - kB + 8];  // RectSmem (task_rect_tile) overlays this region
 };
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E).  The
+// FP64 chains below index register arrays with the loop counter, which
+// must be a constant after unrolling (a nest of #pragma unroll loops whose
+// body holds the division's slow-path call is left rolled by nvcc, and the
+// arrays then live in local memory).
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
 
 // Panel metadata, lane = panel column: its diagonal slot and the first
 // panel row present in it (a supernode's U rows in a column are a suffix).
 // Loaded lane-parallel so the block loads below issue back to back.
 __device__ __forceinline__ void panel_cols(const SnParams &P, int p0, int w, int lane, int &dc, int &clo) {
     dc = 0;
-    clo = kSnW;
+    clo = kB;
     if (lane < w) {
         dc = __ldg(P.diag_pos + p0 + lane);
         clo = max(__ldg(P.col_a + p0 + lane) - p0, 0);
@@ -123,7 +138,6 @@ __device__ void task_diag(const SnParams &P, int4 ta, int lane) {
     const int p0 = ta.z, w = ta.w - ta.z;
     int dcl, clol;
     panel_cols(P, p0, w, lane, dcl, clol);
-    const bool full = __all_sync(0xffffffffu, clol <= 0 || lane >= w);
     double x[WM];
 #pragma unroll
     for (int c = 0; c < WM; c++) {
@@ -131,9 +145,11 @@ __device__ void task_diag(const SnParams &P, int4 ta, int lane) {
         x[c] = (c < w && lane < w && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
     }
     unsigned long long mymax = 0;
-#pragma unroll
-    for (int j = 0; j < WM; j++) {
+    static_for<0, WM>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
         const bool below = lane > j && lane < w;
+        // bit c: U(j, c) present (column c's U suffix starts at or above row j)
+        const unsigned has = __ballot_sync(0xffffffffu, clol <= j);
         const unsigned long long m = warp_max(below ? absbits(x[j]) : 0ull);
         if (lane == j) mymax = m;
         const double piv = __shfl_sync(0xffffffffu, x[j], j);
@@ -143,10 +159,9 @@ __device__ void task_diag(const SnParams &P, int4 ta, int lane) {
         for (int c = j + 1; c < WM; c++) {
             const double ujc = __shfl_sync(0xffffffffu, x[c], j);
             const double y = msub(x[c], l, ujc);
-            if (full) x[c] = below ? y : x[c];
-            else x[c] = (below && j >= __shfl_sync(0xffffffffu, clol, c)) ? y : x[c];
+            x[c] = (below && ((has >> c) & 1u)) ? y : x[c];
         }
-    }
+    });
 #pragma unroll
     for (int c = 0; c < WM; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
@@ -165,8 +180,6 @@ __device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int 
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     int dcl, clol;
     panel_cols(P, p0, w, lane, dcl, clol);
-    S.clo[lane] = clol;
-    const bool full = __all_sync(0xffffffffu, clol <= 0 || lane >= w);
     const int t = chunk * 32 + lane;
     const bool act = t < h;
     double x[WM];
@@ -178,23 +191,19 @@ __device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int 
     }
     __syncwarp();
     unsigned long long mymax = 0;
-#pragma unroll
-    for (int j = 0; j < WM; j++) {
+    static_for<0, WM>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
+        const unsigned has = __ballot_sync(0xffffffffu, clol <= j);
         const unsigned long long m = warp_max(act && j < w ? absbits(x[j]) : 0ull);
         if (lane == j) mymax = m;
         const double d = __ddiv_rn(x[j], S.b[j][j]);
         x[j] = d;
-        if (full) {
 #pragma unroll
-            for (int c = j + 1; c < WM; c++) x[c] = msub(x[c], d, S.b[c][j]);
-        } else {
-#pragma unroll
-            for (int c = j + 1; c < WM; c++) {
-                const double y = msub(x[c], d, S.b[c][j]);
-                x[c] = j >= S.clo[c] ? y : x[c];
-            }
+        for (int c = j + 1; c < WM; c++) {
+            const double y = msub(x[c], d, S.b[c][j]);
+            x[c] = ((has >> c) & 1u) ? y : x[c];
         }
-    }
+    });
 #pragma unroll
     for (int c = 0; c < WM; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c);
@@ -223,8 +232,8 @@ __device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int l
         u[j] = (act && j < w && j >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + j))) : 0.0;
     }
     __syncwarp();
-#pragma unroll
-    for (int j = 0; j < WM; j++) {
+    static_for<0, WM>([&](auto jc) {
+        constexpr int j = decltype(jc)::value;
         const double uj = u[j];
         const bool on = j >= lo;
 #pragma unroll
@@ -232,7 +241,7 @@ __device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int l
             const double y = msub(u[r], S.b[j][r], uj);
             u[r] = on ? y : u[r];
         }
-    }
+    });
     if (act) {
 #pragma unroll
         for (int r = 0; r < WM; r++)
@@ -306,8 +315,8 @@ __device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
 // broadcasts) for 16 MACs.  Columns whose U suffix starts inside the panel
 // (lo > 0, only in structurally unsymmetric patterns) take the select path.
 struct RectSmem {
-    double l[kSnW][kSnW];  // [j][row]
-    double u[kSnW][16];    // [j][column of the half]
+    double l[kB][kB];  // [j][row]
+    double u[kB][16];  // [j][column of the half]
     int lo[16];
 };
 
@@ -322,7 +331,7 @@ __device__ void task_rect_tile(const SnParams &P, RectSmem &R, int4 ta, int4 tb,
     int4 myp = make_int4(0, p1, 0, -1);
     if (lane < npair) myp = __ldg(P.pairs + tb.z + lane);
     const bool colok = lane < npair && myp.y < p1;
-    const int mylo = colok ? max(myp.y - p0, 0) : kSnW;
+    const int mylo = colok ? max(myp.y - p0, 0) : kB;
     const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
 #pragma unroll 8
     for (int j = 0; j < kSnW; j++) {
@@ -426,8 +435,8 @@ __device__ __forceinline__ void run_task(const SnParams &P, WarpSmem &S, int4 ta
     else if (w <= 2) run_kind<2>(P, S, ta, tb, lane);
     else if (w <= 4) run_kind<4>(P, S, ta, tb, lane);
     else if (w <= 8) run_kind<8>(P, S, ta, tb, lane);
-    else if (w <= 16) run_kind<16>(P, S, ta, tb, lane);
-    else run_kind<32>(P, S, ta, tb, lane);
+    else if (kSnW <= 16 || w <= 16) run_kind<16>(P, S, ta, tb, lane);
+    else run_kind<(kSnW > 16 ? 32 : 16)>(P, S, ta, tb, lane);
 }
 
 // A warp leaving phase p counts its tasks of p (release: fence, then add);
