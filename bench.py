@@ -1,28 +1,38 @@
 """Benchmark: GLU3.0 numeric (re)factorization on the B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
-                    [--contract B|A] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4]
+                    [--impl ours|reference] [--engine auto|sn|plan]
+                    [--batch-config cfg2] [--batch-total 1024] [--no-batch]
 
-One step = one numeric refactorization of the configuration's pattern on
-every GPU: device scatter of A's new values into the filled pattern
-(_kernels.py:15-34) + the persistent level kernel (factor + pivot check +
-divide).  Pattern analysis, plan and scatter map are built once, outside
-the timed region.  N > 1 (torchrun): every rank refactors
-its own value sets -- independent matrices, no collective in the data path
-(weak scaling); the only collective is the final all-gather of per-rank
-checksums after the timed region.
+Headline (BASELINE.json metric, first half): numeric factorization of the
+north-star configuration cfg4 -- the G3_circuit-like 1258 x 1258 grid,
+n = 1,582,564, 184 M filled entries, 3.8e10 MACs -- on one B200.  One step =
+one refactorization of the analysed pattern with a new value set: device
+scatter of A's values into the filled pattern (_kernels.py:15-34) + the
+factorization kernel(s) + the pivot check.  Analysis, plan and scatter map
+are built once, outside the timed region.  At N > 1 every
+rank refactors its own cfg4 value sets (independent matrices, no collective
+in the data path: weak scaling).
 
-value = whole-job refactorizations/s (max-over-ranks device time); e2e = the
-same through the reference-facing C-ABI call with host buffers (pinned A
-values in, LU values out, copies inside the timed region).
+Second half of the metric ("refactorizations/s at 1/2/4/8 GPUs"): the
+`batch` object -- cfg5, 1,024 same-pattern refactorizations of cfg2's
+pattern sharded over the N ranks (batched launches, 16 sets per launch), the
+only collective the final all-gather of (set, status, LU digest).
+
+value = whole-job refactorizations/s from the max-over-ranks device time;
+e2e = the same through the reference-facing C-ABI call with pinned host
+buffers (A values in, LU values out, copies inside the timed region);
+e2e_api = through factor_parallel, the reference's own Python entry point
+(pageable numpy in and out).
 --impl reference times the reference algorithm on the host cores (the C
-restatement in oracle/, the reference itself being Python+numba that does
-not travel to the GPU box).
+restatement in oracle/; the reference itself is Python+numba that does not
+travel to the GPU box), analysis included, on the same config.
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import pathlib
@@ -42,24 +52,36 @@ CONFIG_DESC = {
     "cfg2": "synthetic rajat-style circuit n=100,000 + 4 dense power/ground hubs (10%), "
             "SuperLU MMD order",
     "cfg3": "synthetic ASIC_680k-like n=680,000 (1-D local +-40, 6 hubs x 1%), SuperLU MMD order",
+    "cfg4": "synthetic G3_circuit-like 5-point 2-D grid 1258x1258 (n=1,582,564), geometric "
+            "nested dissection",
     "g400": "G3-family 5-point grid 400x400 (n=160,000), geometric nested dissection",
     "g600": "G3-family 5-point grid 600x600 (n=360,000), geometric nested dissection",
     "g800": "G3-family 5-point grid 800x800 (n=640,000), geometric nested dissection",
 }
+# above this many MACs only the parallel reference paths are timed (a single
+# thread takes minutes on cfg4)
+BIG_MACS = 2_000_000_000
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", default="cfg2")
-    p.add_argument("--contract", default="B", choices=["A", "B"])
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="cfg4")
+    p.add_argument("--contract", default="A", choices=["A", "B"])
+    p.add_argument("--engine", default="auto", choices=["auto", "sn", "plan"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
+    p.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of CPU baseline work")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--batch", type=int, default=0,
-                   help="cfg5-style: value sets per GPU per step, factored by batched launches")
+    p.add_argument("--no-parity", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--batch-config", default="cfg2")
+    p.add_argument("--batch-total", type=int, default=1024, help="cfg5: value sets over all ranks")
+    p.add_argument("--batch-steps", type=int, default=2)
+    p.add_argument("--no-batch", action="store_true")
+    p.add_argument("--ref-budget", type=float, default=150.0,
+                   help="reference arm: stop timing after this many seconds")
     return p.parse_args()
 
 
@@ -95,90 +117,18 @@ def load_config(name):
     return synthetic.make(name)
 
 
-def analyze(a):
-    import paper_1908_00204_b200 as glu
-
-    fp = glu.symbolic_fillin(a.pattern)
-    s = glu.levelize(glu.detect_relaxed(fp))
-    return fp, s
-
-
-def value_sets(a, rank, count):
-    """cfg5-style perturbed value sets on the pattern, distinct per rank."""
+def value_sets(a, seed0, count):
+    """cfg5-style perturbed value sets on the pattern."""
     from paper_1908_00204_b200 import synthetic
 
-    return [synthetic.perturb_values(a, 1000 + rank * count + i) for i in range(count)]
+    return [synthetic.perturb_values(a, seed0 + i) for i in range(count)]
 
 
-def level_arrays(s):
-    lp = np.concatenate([[0], np.cumsum([len(c) for c in s.levels])]).astype(np.int64)
-    return lp, np.concatenate(s.levels).astype(np.int64)
-
-
-# ---------------------------------------------------------------------------
-# CPU reference (oracle port of levlu's factor_parallel / left-looking)
-# ---------------------------------------------------------------------------
-def cpu_paths(a, fp, s):
-    """Callables for the reference's CPU paths on this box."""
-    from oracle import oracle as orc
-
-    pat = orc.Pattern.from_fp(fp)
-    lp, lc = level_arrays(s)
-    sizes = [int(x) for x in np.diff(lp)]
-    ncpu = orc.cpu_count()
-
-    def scatter():
-        v, bad = orc.scatter(pat, a.col_ptr, a.row_idx, a.values)
-        assert bad == -1
-        return v
-
-    def left():
-        v = scatter()
-        assert orc.factor_left_looking(pat, v) == -1
-        return v
-
-    def par(det, w):
-        caps = orc.concurrency_caps(sizes, w, n=a.n)
-
-        def run():
-            v = scatter()
-            assert orc.factor_parallel(pat, v, lp, lc, caps, det) == -1
-            return v
-        return run
-
-    paths = {"left_looking w=1": (left, 1),
-             "factor_parallel det w=1": (par(True, 1), 1),
-             f"factor_parallel det w={ncpu}": (par(True, ncpu), ncpu),
-             f"factor_parallel atomic w={ncpu}": (par(False, ncpu), ncpu)}
-    return paths, ncpu
-
-
-def time_cpu(fn, budget_s, min_reps=1):
-    ts = []
-    t_end = time.perf_counter() + budget_s
-    while len(ts) < min_reps or (time.perf_counter() < t_end and len(ts) < 5):
-        t0 = time.perf_counter()
-        fn()
-        ts.append(time.perf_counter() - t0)
-    return min(ts), len(ts)
-
-
-def cpu_baseline(a, fp, s, budget_s):
-    paths, ncpu = cpu_paths(a, fp, s)
-    per = {}
-    share = budget_s / len(paths)
-    for name, (fn, cores) in paths.items():
-        fn()  # warm
-        best, reps = time_cpu(fn, share)
-        per[name] = {"ms": best * 1e3, "reps": reps, "cores": cores}
-    best_name = min(per, key=lambda k: per[k]["ms"])
-    ms = per[best_name]["ms"]
-    return {"value": 1e3 / ms, "unit": "refactorizations/s", "cores": per[best_name]["cores"],
-            "kind": "port", "ms_per_matrix": ms,
-            "sample": f"full {best_name} factorizations of the same matrix (C restatement of "
-                      f"levlu, oracle/levlu_oracle.c), best of reps; all paths: "
-                      + ", ".join(f"{k} {v['ms']:.1f} ms" for k, v in per.items()),
-            "host_cpus": ncpu, "cpu_model": cpu_model()}
+def config_dict(name, a, nnz, levels, macs):
+    """Identical in both arms (same_config)."""
+    return {"workload": f"{name}: {CONFIG_DESC.get(name, '')}", "n": int(a.n), "nz": int(len(a.row_idx)),
+            "nnz": int(nnz), "levels": int(levels), "macs": int(macs),
+            "values": "seeded perturbed value sets (synthetic.perturb_values), one per step"}
 
 
 def cpu_model():
@@ -191,42 +141,125 @@ def cpu_model():
     return "unknown"
 
 
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of levlu's factor_parallel / left-looking)
+# ---------------------------------------------------------------------------
+def oracle_analysis(a):
+    """The reference's analysis (symbolic_fillin, relaxed deps, levelize),
+    restated in oracle/ -- the reference arm loads no product library."""
+    from oracle import oracle as orc
+
+    pat = orc.symbolic_fillin(a.n, a.col_ptr, a.row_idx)
+    dp, di = orc.relaxed_deps(pat)
+    level_of, lp, lc = orc.levelize(a.n, dp, di)
+    return pat, lp, lc
+
+
+def cpu_paths(a, pat, lp, lc, big):
+    """Callables for the reference's CPU paths on this box.
+    Each returns the LU values of the value set it is given."""
+    from oracle import oracle as orc
+
+    sizes = [int(x) for x in np.diff(lp)]
+    ncpu = orc.cpu_count()
+
+    def scatter(vals):
+        v, bad = orc.scatter(pat, a.col_ptr, a.row_idx, vals)
+        assert bad == -1
+        return v
+
+    def left(vals):
+        v = scatter(vals)
+        assert orc.factor_left_looking(pat, v) == -1
+        return v
+
+    def par(det, w):
+        caps = orc.concurrency_caps(sizes, w, n=a.n)
+
+        def run(vals):
+            v = scatter(vals)
+            assert orc.factor_parallel(pat, v, lp, lc, caps, det) == -1
+            return v
+        return run
+
+    paths = {f"factor_parallel det w={ncpu}": (par(True, ncpu), ncpu)}
+    if not big:
+        paths.update({"left_looking w=1": (left, 1),
+                      "factor_parallel det w=1": (par(True, 1), 1),
+                      f"factor_parallel atomic w={ncpu}": (par(False, ncpu), ncpu)})
+    return paths, ncpu
+
+
+def cpu_baseline(paths, ncpu, vals, budget_s, big):
+    """Best reference path on this host (value = refactorizations/s);
+    returns (baseline dict, LU values of the fastest path's last run)."""
+    per, last = {}, {}
+    share = budget_s / len(paths)
+    for name, (fn, cores) in paths.items():
+        ts = []
+        t_end = time.perf_counter() + share
+        while not ts or (time.perf_counter() < t_end and len(ts) < 5):
+            t0 = time.perf_counter()
+            last[name] = fn(vals)
+            ts.append(time.perf_counter() - t0)
+        per[name] = {"ms": min(ts) * 1e3, "reps": len(ts), "cores": cores}
+    best = min(per, key=lambda k: per[k]["ms"])
+    ms = per[best]["ms"]
+    skipped = " (single-thread paths not timed above 2e9 MACs)" if big else ""
+    return ({"value": 1e3 / ms, "unit": "refactorizations/s", "cores": per[best]["cores"],
+             "kind": "port", "ms_per_matrix": ms,
+             "sample": f"full '{best}' factorizations of the bench's value set (C restatement of "
+                       f"levlu, oracle/levlu_oracle.c), best of reps; paths: "
+                       + ", ".join(f"{k} {v['ms']:.1f} ms x{v['reps']}" for k, v in per.items()) + skipped,
+             "host_cpus": ncpu, "cpu_model": cpu_model()}, last[best])
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    t0 = time.perf_counter()
     a = load_config(args.config)
-    fp, s = analyze(a)
-    paths, ncpu = cpu_paths(a, fp, s)
-    # pick the fastest reference path during warm-up, then time K steps of it
+    pat, lp, lc = oracle_analysis(a)
+    from oracle import oracle as orc
+
+    macs, _ = orc.pattern_flops(pat)
+    setup_s = time.perf_counter() - t0
+    big = macs > BIG_MACS
+    paths, ncpu = cpu_paths(a, pat, lp, lc, big)
+    sets = value_sets(a, 1000, 2)
+    # fastest reference path during warm-up, then K timed steps of it (time-boxed)
     best, best_t = None, float("inf")
     for name, (fn, cores) in paths.items():
-        t0 = time.perf_counter()
-        fn()
-        dt = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        fn(sets[0])
+        dt = time.perf_counter() - t1
         if dt < best_t:
             best, best_t = name, dt
     fn, cores = paths[best]
-    for _ in range(max(args.warmup - 1, 0)):
-        fn()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        fn()
-    el = time.perf_counter() - t0
-    ms = el * 1e3 / args.steps
+    for i in range(max(min(args.warmup, 2) - 1, 0)):
+        fn(sets[i % 2])
+    times = []
+    t_all = time.perf_counter()
+    for i in range(args.steps):
+        t1 = time.perf_counter()
+        fn(sets[i % 2])
+        times.append(time.perf_counter() - t1)
+        if time.perf_counter() - t_all > args.ref_budget:
+            break
+    ms = 1e3 * sum(times) / len(times)
     val = 1e3 / ms
-    import paper_1908_00204_b200 as glu
-
-    macs, divs = glu.pattern_flops(fp)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "refactorizations/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "ms_per_matrix": ms,
-            "config": {"workload": f"{args.config}: {CONFIG_DESC.get(args.config, '')}",
-                       "n": a.n, "nnz": fp.nnz, "levels": s.level_count, "macs": macs},
-            "cpu_baseline": {"value": val, "unit": "refactorizations/s", "cores": cores,
-                             "kind": "port", "sample": f"{args.steps} full factorizations, path "
-                             f"'{best}' (fastest of {list(paths)}), C restatement of levlu",
+            "n_gpus": world, "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "ms_per_matrix": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, perturbed value sets)",
+            "config": config_dict(args.config, a, pat.nnz, len(lp) - 1, macs),
+            "setup_s": round(setup_s, 1),
+            "cpu_baseline": {"value": val, "unit": "refactorizations/s", "cores": cores, "kind": "port",
+                             "sample": f"{len(times)} full factorizations (of {args.steps} requested, "
+                                       f"time box {args.ref_budget:.0f} s), path '{best}' (fastest of "
+                                       f"{list(paths)}), C restatement of levlu; analysis by the "
+                                       f"oracle's restatement of symbolic_fillin/detect_relaxed/levelize",
                              "host_cpus": ncpu, "cpu_model": cpu_model()},
             "e2e": {"value": val, "unit": "refactorizations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -290,14 +323,23 @@ def measured_peaks():
         return {}
 
 
-def profiled_traffic(config, contract):
+def profiled_traffic(config, kernel):
     """DRAM bytes per launch (dram__bytes_read + write) from one ncu --set full
-    capture per kernel, recorded in profiles/traffic.json."""
+    capture of the kernel, recorded in profiles/traffic.json."""
     try:
         d = json.loads((ROOT / "profiles" / "traffic.json").read_text())
-        return d.get(f"{config}/{contract}")
+        return d.get(f"{config}/{kernel}")
     except (OSError, ValueError):
         return None
+
+
+def max_over_ranks(x, dev, world):
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t[0])
 
 
 def run_ours(args):
@@ -306,18 +348,24 @@ def run_ours(args):
     rank, world, local = dist_env()
     dev = init_dist(world, local)
     import paper_1908_00204_b200 as glu
+    from paper_1908_00204_b200 import _lib, numeric
 
     a = load_config(args.config)
-    fp, s = analyze(a)
-    macs, divs = glu.pattern_flops(fp)
-    contract = 1 if args.contract == "B" else 0
     t0 = time.perf_counter()
-    fz = glu.Factorizer(fp, s.level_of, contract)
+    fp = glu.symbolic_fillin(a.pattern)
+    s = glu.levelize(glu.detect_relaxed(fp))
+    analysis_s = time.perf_counter() - t0
+    macs, divs = glu.pattern_flops(fp)
+    contract = _lib.CONTRACT_B if args.contract == "B" else _lib.CONTRACT_A
+    engine = numeric.pick_engine(fp, contract) if args.engine == "auto" else args.engine
+    t0 = time.perf_counter()
+    fz = numeric.get_factorizer(fp, numeric.plan_levels(fp, s.level_of, contract), contract, engine=engine)
     setup_s = time.perf_counter() - t0
     fz.set_input(a.col_ptr, a.row_idx)
     fz.set_option(1, 0)
-    nsets = 4
-    sets = value_sets(a, rank, nsets)
+    fz.set_option(2, 1)
+    nsets = 2
+    sets = value_sets(a, 1000 + rank * nsets, nsets)
     a_dev = [torch.from_numpy(x).to(dev) for x in sets]
     v = torch.empty(fp.nnz, dtype=torch.float64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -328,18 +376,16 @@ def run_ours(args):
         if ev:
             ev[0].record(stream)
         fz.scatter_device(a_dev[i % nsets], v, stream)
-        if ev:
-            ev[1].record(stream)
         fz.factor_device_async(v, thresh, stream)
         if ev:
-            ev[2].record(stream)
+            ev[1].record(stream)
 
     for i in range(args.warmup):
         flush.zero_()
         step(i)
     torch.cuda.synchronize()
     assert fz.status(stream) == -1
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     fz.set_option(8, args.steps)  # per-kernel CUDA events on the launch stream (ring of K)
     if world > 1:
         torch.distributed.barrier()
@@ -353,79 +399,100 @@ def run_ours(args):
         torch.distributed.barrier()
     status = fz.status(stream)
     assert status == -1, f"pivot failure {status}"
-    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
-    fac_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    from paper_1908_00204_b200 import _lib
+    step_ms = [e[0].elapsed_time(e[1]) for e in evs]
     kt = np.zeros(2 * args.steps, dtype=np.float64)
     nk = _lib.lib.glu_kernel_times(fz.handle, _lib.ptr(kt), args.steps)
     main_ms = float(kt[0:2 * nk:2].mean()) if nk else None
     tail_ms = float(kt[1:2 * nk:2].mean()) if nk else None
     fz.set_option(8, 0)
-    tot = torch.tensor([sum(step_ms), sum(fac_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
-    ms_step = float(tot[0]) / args.steps
-    ms_fac = float(tot[1]) / args.steps
-
-    # parity spot check of the last step vs the CPU oracle (rank 0), and the
-    # final gather of per-rank checksums (the only collective)
+    ms_step = max_over_ranks(sum(step_ms) / args.steps, dev, world)
     lu_last = v.cpu().numpy()
-    from paper_1908_00204_b200 import batch as glu_batch
+    last_set = (args.steps - 1) % nsets
 
-    last_set = rank * nsets + (args.steps - 1) % nsets  # global value-set id
-    if world > 1:  # (set id, status, LU checksum) of every rank: the only collective
-        glu_batch.gather_results([last_set], [fz.status(stream)], [glu_batch.set_digest(lu_last)])
-    parity = None
-    cpu = None
-    if rank == 0:
+    # parity of the last step vs the CPU oracle (rank 0) + the CPU baseline on
+    # the same value set (the fastest reference path's output is the check)
+    parity = cpu = None
+    if rank == 0 and not (args.no_parity and args.no_cpu_baseline):
         from oracle import oracle as orc
 
         pat = orc.Pattern.from_fp(fp)
-        ref, bad = orc.scatter(pat, a.col_ptr, a.row_idx, sets[(args.steps - 1) % nsets])
-        lp, lc = level_arrays(s)
-        orc.factor_parallel(pat, ref, lp, lc, np.ones(len(lp) - 1, np.int64), contract == 0)
-        parity = "bitwise" if np.array_equal(ref, lu_last) else "MISMATCH"
-        if not args.no_cpu_baseline:
-            cpu = cpu_baseline(a, fp, s, args.cpu_budget)
+        lp = np.concatenate([[0], np.cumsum([len(c) for c in s.levels])]).astype(np.int64)
+        lc = np.concatenate(s.levels).astype(np.int64)
+        big = macs > BIG_MACS
+        paths, ncpu = cpu_paths(a, pat, lp, lc, big)
+        if args.no_cpu_baseline:
+            ref = paths[f"factor_parallel det w={ncpu}"][0](sets[last_set])
+        else:
+            cpu, ref = cpu_baseline(paths, ncpu, sets[last_set], args.cpu_budget, big)
+        if contract == _lib.CONTRACT_B:
+            ref, bad = orc.scatter(pat, a.col_ptr, a.row_idx, sets[last_set])
+            orc.factor_parallel(pat, ref, lp, lc, np.ones(len(lp) - 1, np.int64), False)
+        parity = "bitwise" if np.array_equal(ref, lu_last) else \
+            f"MISMATCH ({int(np.sum(ref != lu_last))} entries)"
 
-    # e2e through the host-buffer C-ABI call (pinned buffers)
-    a_host = [torch.from_numpy(x).pin_memory() for x in sets]
-    lu_host = torch.empty(fp.nnz, dtype=torch.float64).pin_memory()
-    from paper_1908_00204_b200 import _lib
-    import ctypes
+    # e2e: the reference-facing C-ABI call with pinned host buffers
+    e2e = e2e_api = None
+    if not args.no_e2e:
+        a_host = [torch.from_numpy(x).pin_memory() for x in sets]
+        lu_host = torch.empty(fp.nnz, dtype=torch.float64).pin_memory()
 
-    def e2e_step(i):
-        rc = _lib.lib.glu_factor_host(fz.handle, ctypes.c_void_p(a_host[i % nsets].data_ptr()),
-                                      ctypes.c_void_p(lu_host.data_ptr()), thresh)
-        assert rc == -1, rc
+        def e2e_step(i):
+            rc = _lib.lib.glu_factor_host(fz.handle, ctypes.c_void_p(a_host[i % nsets].data_ptr()),
+                                          ctypes.c_void_p(lu_host.data_ptr()), thresh)
+            assert rc == -1, rc
 
-    for i in range(args.warmup):
-        e2e_step(i)
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        e2e_step(i)
-    e2e_s = time.perf_counter() - t0
-    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
-    e2e_ms = float(e2e_t[0]) * 1e3 / args.steps
+        for i in range(min(args.warmup, 2)):
+            e2e_step(i)
+        if world > 1:
+            torch.distributed.barrier()
+        t1 = time.perf_counter()
+        for i in range(args.steps):
+            e2e_step(i)
+        e2e_ms = max_over_ranks((time.perf_counter() - t1) * 1e3 / args.steps, dev, world)
+        e2e = {"value": world * 1e3 / e2e_ms, "unit": "refactorizations/s", "ms_per_matrix": e2e_ms,
+               "h2d_bytes_per_step": 8 * len(a.row_idx), "d2h_bytes_per_step": 8 * fp.nnz,
+               "api": "glu_factor_host (C ABI, pinned host buffers): H2D A values, scatter, factor, "
+                      "pivot check, D2H LU values, status read"}
+        del a_host, lu_host
+        # the reference's own entry point: factor_parallel with numpy (pageable) arrays
+        plans = glu.plan_schedule(s, glu.level_stats(fp, s), a.n, glu.B200_RESOURCE)
+        opts = glu.FactorOptions(deterministic=contract == _lib.CONTRACT_A)
+        mats = [glu.CscMatrix(a.n, a.col_ptr, a.row_idx, x) for x in sets]
+        os.environ["GLU_LEVEL_TIMES"] = "0"
+        glu.factor_parallel(mats[0], fp, s, plans, opts)
+        reps = max(2, min(args.steps, 5))
+        t1 = time.perf_counter()
+        for i in range(reps):
+            lu, _ = glu.factor_parallel(mats[i % nsets], fp, s, plans, opts)
+        api_ms = max_over_ranks((time.perf_counter() - t1) * 1e3 / reps, dev, world)
+        e2e_api = {"value": world * 1e3 / api_ms, "unit": "refactorizations/s", "ms_per_matrix": api_ms,
+                   "steps": reps, "api": "factor_parallel(a, fp, schedule, plans, opts) -> LuFactors "
+                                         "(levlu/numeric.py:241; pageable numpy in and out)"}
+        del lu, mats
+
+    batch = None
+    if not args.no_batch:
+        del a_dev, v, flush
+        torch.cuda.empty_cache()
+        batch = run_batch(args, rank, world, dev)
 
     if rank == 0:
         peaks = measured_peaks()
         hbm = peaks.get("hbm_gbs")
-        # algorithmic bytes per launch (SURVEY 8(d)): 16 B per MAC (target read +
-        # write, L and multiplier in registers) + 16 B per value of the columns
-        # the kernel owns; the dense tail's MACs belong to tail_kernel
-        tail_macs = int(fz.plan_info.get("tail_macs", 0))
-        t0c = int(fz.plan_info.get("tail_t0", a.n))
-        nnz_tail = int(fp.full.col_ptr[a.n] - fp.full.col_ptr[t0c])
-        bytes_main = 16 * (macs - tail_macs) + 16 * (fp.nnz - nnz_tail)
-        bytes_tail = 16 * tail_macs + 16 * nnz_tail
-        achieved = bytes_main / (main_ms * 1e-3) / 1e9
-        traffic = profiled_traffic(args.config, args.contract) or {}
         info = fz.handle_info
+        kname = "sn_kernel" if engine == "sn" else "factor_kernel"
+        tail_macs = int(fz.plan_info.get("tail_macs", 0)) if engine == "plan" else 0
+        t0c = int(fz.plan_info.get("tail_t0", a.n)) if engine == "plan" else a.n
+        nnz_tail = int(fp.full.col_ptr[a.n] - fp.full.col_ptr[t0c])
+        # algorithmic bytes per launch (SURVEY 8(d)): 16 B per MAC (target read +
+        # write) + 16 B per value of the columns the kernel owns
+        bytes_main = 16 * (macs - tail_macs) + 16 * (fp.nnz - nnz_tail)
+        achieved = bytes_main / (main_ms * 1e-3) / 1e9 if main_ms else None
+        traffic = profiled_traffic(args.config, kname) or {}
+        # FP64 issue roof: every MAC is a DMUL + a DADD (no FMA: bitwise parity,
+        # _kernels.py:4-6); 64 FP64 lanes per SM
+        sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+        fp64_macs_peak = info["sms"] * 64 * sm_mhz * 1e6 / 2
         line = {
             "metric": METRIC,
             "value": world * 1e3 / ms_step,
@@ -433,125 +500,135 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step,
             "ms_per_matrix": ms_step,
-            "factor_kernel_ms": ms_fac,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded generator, perturbed value sets)",
-            "config": {"workload": f"{args.config}: {CONFIG_DESC.get(args.config, '')}",
-                       "n": a.n, "nz": a.nnz, "nnz": fp.nnz, "levels": s.level_count,
-                       "macs": macs, "contract": args.contract,
-                       "plan": fz.plan_info, "grid_ctas": info["grid"],
-                       "threads_per_cta": info["threads"], "setup_s": round(setup_s, 3),
-                       "l2": "flushed (512 MiB write) between timed steps",
-                       "parallelism": f"{world} independent refactorizations (one per GPU)"},
+            "config": config_dict(args.config, a, fp.nnz, s.level_count, macs),
+            "run": {"engine": engine, "contract": args.contract, "plan": fz.plan_info,
+                    "sn": getattr(fz, "sn_info", None), "device_bytes": info["device_bytes"],
+                    "grid_ctas": info["grid"], "analysis_s": round(analysis_s, 2),
+                    "setup_s": round(setup_s, 2), "l2": "flushed (512 MiB write) between timed steps",
+                    "parallelism": f"{world} independent refactorizations (one per GPU)"},
             "parity": parity,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": (achieved / hbm) if hbm else None,
-                         "traffic": traffic.get("factor_kernel"),
-                         "kernel": "factor_kernel", "kernel_ms": main_ms,
-                         "bytes_alg": bytes_main,
-                         "formula": "16*(MACs - tail MACs) + 16*nnz(A_s outside the tail) per launch",
+                         "frac": (achieved / hbm) if (hbm and achieved) else None,
+                         "traffic": traffic.get("bytes_per_launch"),
+                         "kernel": kname, "kernel_ms": main_ms, "bytes_alg": bytes_main,
+                         "formula": "SURVEY 8(d): 16*MACs + 16*nnz(A_s) per launch (no reuse assumed; "
+                                    "the supernodal kernel keeps targets in registers across a panel, "
+                                    "so this 'achieved' is an effective bandwidth)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
                          "traffic_source": traffic.get("source")},
-            "roofline_tail": ({"kernel": "tail_kernel", "kernel_ms": tail_ms, "bytes_alg": bytes_tail,
-                               "achieved": bytes_tail / (tail_ms * 1e-3) / 1e9, "unit": "GB/s",
-                               "frac": bytes_tail / (tail_ms * 1e-3) / 1e9 / hbm if hbm else None,
-                               "traffic": traffic.get("tail_kernel"), "tail_columns": a.n - t0c,
-                               "tail_macs": tail_macs} if tail_ms else None),
+            "roofline_fp64": {"achieved_macs_per_s": macs / (main_ms * 1e-3) if main_ms else None,
+                              "peak_macs_per_s": fp64_macs_peak,
+                              "frac": macs / (main_ms * 1e-3) / fp64_macs_peak if main_ms else None,
+                              "peak_source": f"derived: {info['sms']} SMs x 64 FP64 lanes x {sm_mhz:.0f} MHz "
+                                             f"/ 2 instructions per MAC (DMUL + DADD, no FMA)"},
+            "latency_floor": ({"phases": fz.sn_info["phases"], "stages": fz.sn_info["stages"],
+                               "note": "every phase is a device-wide hand-off (~2.5 us measured: "
+                                       "flush 1.0-1.3 us + wake 1.3-1.5 us, tools/sn_probe.py)",
+                               "floor_ms": fz.sn_info["phases"] * 2.5e-3}
+                              if engine == "sn" else None),
             "cpu_baseline": cpu,
-            "e2e": {"value": world * 1e3 / e2e_ms, "unit": "refactorizations/s",
-                    "ms_per_matrix": e2e_ms,
-                    "h2d_bytes_per_step": 8 * a.nnz, "d2h_bytes_per_step": 8 * fp.nnz,
-                    "api": "glu_factor_host (C ABI, pinned host buffers)"},
+            "e2e": e2e,
+            "e2e_api": e2e_api,
+            "batch": batch,
             "clocks": clk.summary(),
-            "gpu_launches": (3 + (1 if fz.plan_info.get("tail_t0", a.n) < a.n else 0)) * args.steps,
+            "gpu_launches": 4 * args.steps if engine == "sn" else
+            (3 + (1 if t0c < a.n else 0)) * args.steps,
         }
+        if engine == "plan" and tail_ms:
+            line["roofline_tail"] = {"kernel": "tail_kernel", "kernel_ms": tail_ms,
+                                     "bytes_alg": 16 * tail_macs + 16 * nnz_tail}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def run_batch(args):
-    """cfg5-style throughput: each step, every rank refactors its shard of
-    `--batch` value sets of the configuration's pattern through batched
-    launches (up to 8 sets per launch share each item's plan loads,
-    dependency wait and release).  value = whole-job refactorizations/s."""
+def run_batch(args, rank, world, dev):
+    """cfg5: --batch-total value sets of --batch-config's pattern sharded over
+    the ranks, each rank refactoring its shard in batched launches; the
+    final all-gather of (set, status, LU digest) is the only collective.
+    Returns the line's `batch` object on rank 0."""
     import torch
 
-    rank, world, local = dist_env()
-    dev = init_dist(world, local)
     import paper_1908_00204_b200 as glu
     from paper_1908_00204_b200 import batch as glu_batch
+    from paper_1908_00204_b200 import numeric, synthetic
 
-    a = load_config(args.config)
-    fp, s = analyze(a)
+    a = load_config(args.batch_config)
+    fp = glu.symbolic_fillin(a.pattern)
+    s = glu.levelize(glu.detect_relaxed(fp))
     macs, _ = glu.pattern_flops(fp)
-    contract = 1 if args.contract == "B" else 0
-    fz = glu.Factorizer(fp, s.level_of, contract, max_item_macs=64)  # dense tail: one cluster per set
+    mine = list(glu_batch.shard(args.batch_total, rank, world))
+    B = len(mine)
+    fz = numeric.get_factorizer(fp, numeric.plan_levels(fp, None, 0), 0, tail=False)
     fz.set_input(a.col_ptr, a.row_idx)
-    B = args.batch
-    sets = np.stack(value_sets(a, rank, B))
+    fz.set_option(1, 0)
+    fz.set_option(2, 1)
+    sets = np.stack([synthetic.perturb_values(a, 1000 + b) for b in mine]) if B else \
+        np.zeros((0, len(a.row_idx)))
     a_dev = torch.from_numpy(sets).to(dev)
-    v = torch.empty((B, fp.nnz), dtype=torch.float64, device=dev)
+    v = torch.empty((max(B, 1), fp.nnz), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
     def step():
         for b in range(B):
             fz.scatter_device(a_dev[b], v[b], stream)
-        return fz.factor_batch_device(v, 1e-14, stream)
+        return fz.factor_batch_device(v[:B], 1e-14, stream) if B else np.zeros(0, np.int64)
 
-    for _ in range(args.warmup):
-        assert np.all(step() == -1)
+    assert np.all(step() == -1)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(dev.index) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            fails = step()  # status read per step (synchronizes: part of the API)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
-    ms = float(ms[0])
+    e0.record(stream)
+    for _ in range(args.batch_steps):
+        fails = step()  # status read per step (synchronizes: part of the API)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.batch_steps, dev, world)
     digests = [glu_batch.set_digest(v[b].cpu().numpy()) for b in range(B)]
-    idx = list(range(rank * B, rank * B + B))
     if world > 1:
-        glu_batch.gather_results(idx, fails.tolist(), digests)
-    parity = None
+        idx, status, dg = glu_batch.gather_results(mine, fails.tolist(), digests)
+    else:
+        idx, status, dg = np.array(mine), np.asarray(fails), np.array(digests)
+    out = None
     if rank == 0:
         from oracle import oracle as orc
 
         pat = orc.Pattern.from_fp(fp)
-        lp, lc = level_arrays(s)
-        ref, _ = orc.scatter(pat, a.col_ptr, a.row_idx, sets[B - 1])
-        orc.factor_parallel(pat, ref, lp, lc, np.ones(len(lp) - 1, np.int64), contract == 0)
-        parity = "bitwise" if np.array_equal(ref, v[B - 1].cpu().numpy()) else "MISMATCH"
-        line = {"metric": METRIC, "value": world * B * 1e3 / ms, "unit": "refactorizations/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "ms_per_matrix": ms / B, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded generator, perturbed value sets)",
-                "config": {"workload": f"cfg5-style batch of {B} value sets per GPU on "
-                                       f"{args.config}'s pattern",
-                           "n": a.n, "nnz": fp.nnz, "levels": s.level_count, "macs": macs,
-                           "contract": args.contract, "batch_per_gpu": B,
-                           "launches_per_step": (B + 7) // 8,
-                           "parallelism": f"{world} ranks x {B} independent value sets"},
-                "parity": parity, "clocks": clk.summary(),
-                "gpu_launches": args.steps * (2 * B + (B + 7) // 8)}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+        checked = []
+        for b in sorted({0, args.batch_total - 1}):
+            ref, _ = orc.scatter(pat, a.col_ptr, a.row_idx, synthetic.perturb_values(a, 1000 + b))
+            orc.factor_left_looking(pat, ref)
+            checked.append(glu_batch.set_digest(ref) == int(dg[list(idx).index(b)]))
+        # CPU throughput ceiling: nproc independent single-thread factorizations
+        ref, _ = orc.scatter(pat, a.col_ptr, a.row_idx, sets[0] if B else a.values)
+        t1 = time.perf_counter()
+        orc.factor_left_looking(pat, ref)
+        t_one = time.perf_counter() - t1
+        ncpu = orc.cpu_count()
+        out = {"workload": f"cfg5: {args.batch_total} same-pattern refactorizations of "
+                           f"{args.batch_config} ({CONFIG_DESC.get(args.batch_config, '')}), perturbed "
+                           f"value sets, sharded over {world} GPU(s)",
+               "value": args.batch_total * 1e3 / ms, "unit": "refactorizations/s",
+               "ms_per_step": ms, "ms_per_matrix_per_gpu": ms / max(len(mine), 1),
+               "steps": args.batch_steps, "sets_per_gpu": B, "n_gpus": world,
+               "scaling": "strong (fixed 1,024 sets)", "statuses_ok": bool(np.all(np.asarray(status) == -1)),
+               "gathered_sets": int(len(idx)),
+               "parity": "bitwise (digest of sets 0 and last vs oracle)" if all(checked) else "MISMATCH",
+               "n": a.n, "nnz": fp.nnz, "macs": macs,
+               "launches_per_step": B + (B + 15) // 16 * 2 if B else 0,
+               "cpu_ceiling": {"value": ncpu / t_one, "unit": "refactorizations/s",
+                               "sample": f"{ncpu} x one single-thread left-looking factorization "
+                                         f"({t_one * 1e3:.1f} ms), perfect scaling assumed"}}
+    return out
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    elif args.batch > 0:
-        run_batch(args)
     else:
         run_ours(args)
 

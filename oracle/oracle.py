@@ -47,6 +47,8 @@ def _load():
         "orc_symbolic_fillin": (i64, [i64, p, p, ctypes.c_int, i64, p, p, p, p]),
         "orc_factor_parallel": (i64, [i64, p, p, p, p, p, p, p, i64, p, p, p, ctypes.c_int, d]),
         "orc_pattern_flops": (i64, [i64, p, p, p, p]),
+        "orc_relaxed_deps": (i64, [i64, p, p, p, p, p, p, p]),
+        "orc_levelize": (i64, [i64, p, p, p, p, p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -175,35 +177,24 @@ def pattern_flops(pat: Pattern):
 
 def relaxed_deps(pat: Pattern):
     """levlu/depgraph.py:83-126: upward edges (U(i,k), L(:,i) non-empty) plus
-    L-row edges (k depends on i for L(k,i) != 0), deduplicated via unique
-    keys src*n+dst.  Returns CSR (ptr, idx)."""
+    L-row edges (k depends on i for L(k,i) != 0), sorted and unique per
+    column (the C restatement merges the two sorted lists).  Returns CSR
+    (ptr, idx)."""
     n = pat.n
-    cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(pat.col_ptr))
-    nonempty = (pat.col_ptr[1:] - pat.diag_pos) > 1
-    up = (pat.row_idx < cols) & nonempty[pat.row_idx]
-    csr_rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(pat.row_ptr))
-    left = pat.col_idx < csr_rows
-    src = np.concatenate([cols[up], csr_rows[left]])
-    dst = np.concatenate([pat.row_idx[up], pat.col_idx[left]])
-    keys = np.unique(src * np.int64(n) + dst) if len(src) else np.empty(0, np.int64)
-    s, d = keys // max(n, 1), keys % max(n, 1)
     ptr = np.zeros(n + 1, dtype=np.int64)
-    np.add.at(ptr, s + 1, 1)
-    np.cumsum(ptr, out=ptr)
-    return ptr, d.astype(np.int64)
+    idx = np.empty(max(pat.nnz, 1), dtype=np.int64)
+    e = _lib.orc_relaxed_deps(n, _p(pat.col_ptr), _p(pat.row_idx), _p(pat.diag_pos), _p(pat.row_ptr),
+                              _p(pat.col_idx), _p(ptr), _p(idx))
+    return ptr, idx[:e].copy()
 
 
 def levelize(n, dep_ptr, dep_idx):
-    """levlu/depgraph.py:159-170."""
-    level_of = np.zeros(n, dtype=np.int64)
-    for j in range(n):
-        d = dep_idx[dep_ptr[j]:dep_ptr[j + 1]]
-        if len(d):
-            level_of[j] = level_of[d].max() + 1
-    nl = int(level_of.max()) + 1 if n else 0
-    order = np.argsort(level_of, kind="stable")
-    ptr = np.searchsorted(level_of[order], np.arange(nl + 1)).astype(np.int64)
-    return level_of, ptr, order.astype(np.int64)
+    """levlu/depgraph.py:159-170: (level_of, level_ptr, level_cols)."""
+    level_of = np.zeros(max(n, 1), dtype=np.int64)
+    ptr = np.zeros(n + 2, dtype=np.int64)
+    cols = np.zeros(max(n, 1), dtype=np.int64)
+    nl = _lib.orc_levelize(n, _p(_i(dep_ptr)), _p(_i(dep_idx)), _p(level_of), _p(ptr), _p(cols))
+    return level_of[:n], ptr[:nl + 1].copy(), cols[:n]
 
 
 def concurrency_caps(level_sizes, worker_count, total_warps=96, stream_threshold=16,

@@ -114,3 +114,33 @@ def test_known_answers():
     lp, lc = c8["level_ptr"], c8["level_cols"]
     assert [lc[lp[i]:lp[i + 1]].tolist() for i in range(len(lp) - 1)] == [[0, 2, 3, 4], [1, 5], [6], [7]]
     assert load_golden("singular_2x2")["fail_a"] == 1
+
+
+def test_oracle_analysis_matches_reference(golden):
+    """The oracle's analysis restatement (the reference arm of bench.py runs
+    it instead of the product's C++): symbolic fill-in, relaxed deps and
+    levels bit-exact against the reference's own outputs."""
+    name, g = golden
+    n = int(g["n"])
+    pat = orc.symbolic_fillin(n, g["a_col_ptr"], g["a_row_idx"])
+    assert np.array_equal(pat.col_ptr, g["fp_col_ptr"]) and np.array_equal(pat.row_idx, g["fp_row_idx"])
+    assert np.array_equal(pat.diag_pos, g["fp_diag_pos"])
+    ptr, idx = orc.relaxed_deps(pat)
+    assert np.array_equal(ptr, g["relaxed_ptr"]) and np.array_equal(idx, g["relaxed_idx"])
+    level_of, lp, lc = orc.levelize(n, ptr, idx)
+    assert np.array_equal(level_of, g["level_of"])
+    assert np.array_equal(lp, g["level_ptr"]) and np.array_equal(lc, g["level_cols"])
+
+
+def test_oracle_analysis_matches_product_at_scale():
+    """Same arrays as the product's C++ analysis on a 100k-row grid."""
+    import paper_1908_00204_b200 as glu
+    from paper_1908_00204_b200 import synthetic
+
+    a = synthetic.grid5(150, drop=0.1, seed=4)
+    pat = orc.symbolic_fillin(a.n, a.col_ptr, a.row_idx)
+    fp = glu.symbolic_fillin(a.pattern)
+    assert np.array_equal(pat.row_idx, fp.full.row_idx) and np.array_equal(pat.diag_pos, fp.diag_pos)
+    ptr, idx = orc.relaxed_deps(pat)
+    level_of, _, _ = orc.levelize(a.n, ptr, idx)
+    assert np.array_equal(level_of, glu.levelize(glu.detect_relaxed(fp)).level_of)
