@@ -231,7 +231,8 @@ CONFIGS = {
     "cfg2": lambda: circuit_like(100_000, hubs=4, hub_frac=0.10, seed=0),
     "cfg3": lambda: asic_like(680_000, seed=0),
     "cfg4": lambda: grid5(1258, seed=0),
-    # G3-family data point at a size whose plan fits (cfg4's does not yet)
+    # G3-family grids between cfg1 and cfg4 (parity at intermediate sizes)
+    "g200": lambda: grid5(200, seed=0),
     "g400": lambda: grid5(400, seed=0),
     "g600": lambda: grid5(600, seed=0),
     "g800": lambda: grid5(800, seed=0),
