@@ -77,6 +77,12 @@ int64_t glu_detect_relaxed(int64_t n, const int64_t *col_ptr, const int64_t *row
 int64_t glu_detect_upward(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                           const int64_t *diag_pos, int64_t *dep_ptr, int64_t *dep_idx);
 
+/* depgraph.py:129-156 detect_double_u_exact (same output convention): the
+   exact GLU2.0 detector, kept as a debugging oracle. */
+int64_t glu_detect_double_u_exact(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                  const int64_t *diag_pos, const int64_t *row_ptr,
+                                  const int64_t *col_idx, int64_t *dep_ptr, int64_t *dep_idx);
+
 /* depgraph.py:159-170 levelize.  Returns the level count; level_cols lists
    the columns level by level, ascending within each level. */
 int64_t glu_levelize(int64_t n, const int64_t *dep_ptr, const int64_t *dep_idx,

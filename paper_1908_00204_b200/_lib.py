@@ -42,6 +42,7 @@ SIGNATURES = {
     "glu_csr_view": (_i64, [_i64, _p, _p, _p, _p, _p]),
     "glu_detect_relaxed": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _p]),
     "glu_detect_upward": (_i64, [_i64, _p, _p, _p, _p, _p]),
+    "glu_detect_double_u_exact": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _p]),
     "glu_levelize": (_i64, [_i64, _p, _p, _p, _p, _p]),
     "glu_scatter_values": (_i64, [_i64, _p, _p, _p, _p, _p, _p]),
     "glu_find_hazards": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _i64, _p]),

@@ -1900,6 +1900,10 @@ __global__ void solve_xmove_kernel(double *src, long long ld_src, int il_src, do
     }
 }
 
+// batched launches: OR each launch's watchdog word into a sticky one (the
+// next launch's memset clears the per-launch word)
+__global__ void err_or_kernel(int *acc, const int *err) { *acc |= *err; }
+
 __global__ void fill_sentinel_kernel(double *p, long long m) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (long long)gridDim.x * blockDim.x)
@@ -1981,6 +1985,7 @@ struct glu_handle {
     unsigned long long *fail = nullptr;
     unsigned int *bar = nullptr;
     int *ifail = nullptr;
+    int *err_acc = nullptr;  // sticky watchdog word across the launches of one batched call
     // dataflow solves: sentinel-managed y buffer, [ticket, err] words
     double *solve_y = nullptr;
     i64 solve_y_cap = 0;
@@ -2086,6 +2091,19 @@ int coop_grid(const void *kernel, int sm_count, size_t dyn_smem = 0) {
 }
 
 }  // namespace
+
+// Every entry point runs on the handle's device, whatever the caller's
+// current device is (restored on return).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const glu_handle *h) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != h->device) cudaSetDevice(h->device);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 extern "C" const char *glu_version(void) { return "glu_b200 0.1 sm_100a"; }
 
@@ -2241,6 +2259,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     if (cudaMalloc((void **)&h->fail, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc((void **)&h->bar, sizeof(unsigned int)) != cudaSuccess ||
         cudaMalloc((void **)&h->ifail, sizeof(int)) != cudaSuccess ||
+        cudaMalloc((void **)&h->err_acc, sizeof(int)) != cudaSuccess ||
         cudaMalloc((void **)&h->sctl, 2 * sizeof(unsigned)) != cudaSuccess) {
         glu::set_error("cudaMalloc(scratch)"); return fail(GLU_ECUDA);
     }
@@ -2263,7 +2282,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->l_split, h->solve_part, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->bar, h->ifail, h->err_acc, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->l_split, h->solve_part, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     glu::sn_free(h->sn);
@@ -2408,6 +2427,7 @@ extern "C" int64_t glu_level_times(const glu_handle *h, double *ms, int64_t len)
 
 extern "C" int64_t glu_set_input_pattern(glu_handle *h, int64_t nz, const int64_t *a_col_ptr,
                                          const int64_t *a_row_idx) {
+    DeviceGuard dg_(h);
     // host merge, reference semantics (_kernels.py:15-34); the slot map then
     // lets every later scatter run on the device
     std::vector<i32> rows32((size_t)h->nnz), cols32((size_t)h->n + 1);
@@ -2429,6 +2449,9 @@ extern "C" int64_t glu_set_input_pattern(glu_handle *h, int64_t nz, const int64_
     }
     if (h->a_slot) { cudaFree(h->a_slot); h->a_slot = nullptr; }
     if (h->d_a) { cudaFree(h->d_a); h->d_a = nullptr; }
+    // batched staging is sized from nz: drop it with the old pattern
+    if (h->d_ab) { cudaFree(h->d_ab); h->d_ab = nullptr; }
+    if (h->d_vb) { cudaFree(h->d_vb); h->d_vb = nullptr; }
     i64 rc = track_upload(h, &h->a_slot, slot);
     if (rc != GLU_OK) return rc;
     h->nz = nz;
@@ -2436,6 +2459,7 @@ extern "C" int64_t glu_set_input_pattern(glu_handle *h, int64_t nz, const int64_
 }
 
 extern "C" int64_t glu_scatter_device(glu_handle *h, const double *a_vals, double *v, void *stream) {
+    DeviceGuard dg_(h);
     if (h->nz < 0) { glu::set_error("glu_set_input_pattern not called"); return GLU_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
     const int blocks = h->sm_count * 4;
@@ -2461,6 +2485,7 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
             h->kev_next++;
             GLU_CUDA(cudaEventRecord(ke[0], s));
         }
+        GLU_CUDA(cudaMemsetAsync(h->sync + nl8s, 0, sizeof(int), s));  // watchdog word
         for (int b = 0; b < nb; b++) {
             const i64 rc = glu::sn_launch(h->sn, v + (size_t)b * h->nnz, h->col_ptr, h->diag_pos, h->level_of,
                                           (i32)h->n, thresh, h->fail_by_column, fail + b,
@@ -2606,6 +2631,7 @@ static int64_t read_fail(glu_handle *h, cudaStream_t s) {
 }
 
 extern "C" int64_t glu_factor_device(glu_handle *h, double *v, double thresh, void *stream) {
+    DeviceGuard dg_(h);
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = launch_factor(h, v, thresh, s);
     if (rc != GLU_OK) return rc;
@@ -2614,10 +2640,12 @@ extern "C" int64_t glu_factor_device(glu_handle *h, double *v, double thresh, vo
 
 // Asynchronous variant for timing loops: no host sync, no status read.
 extern "C" int64_t glu_factor_device_async(glu_handle *h, double *v, double thresh, void *stream) {
+    DeviceGuard dg_(h);
     return launch_factor(h, v, thresh, (cudaStream_t)stream);
 }
 
 extern "C" int64_t glu_factor_status(glu_handle *h, void *stream) {
+    DeviceGuard dg_(h);
     return read_fail(h, (cudaStream_t)stream);
 }
 
@@ -2645,7 +2673,8 @@ static int64_t batch_status(glu_handle *h, int64_t batch, int64_t *fail_cols, cu
     const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
     GLU_CUDA(cudaMemcpyAsync(keys.data(), h->fail_batch, sizeof(unsigned long long) * batch,
                              cudaMemcpyDeviceToHost, s));
-    GLU_CUDA(cudaMemcpyAsync(&err, h->sync + nl8, sizeof(int), cudaMemcpyDeviceToHost, s));
+    (void)nl8;
+    GLU_CUDA(cudaMemcpyAsync(&err, h->err_acc, sizeof(int), cudaMemcpyDeviceToHost, s));
     GLU_CUDA(cudaStreamSynchronize(s));
     if (err) {
         glu::set_error("factor kernel watchdog: a phase dependency wait exceeded 4 s");
@@ -2658,21 +2687,26 @@ static int64_t batch_status(glu_handle *h, int64_t batch, int64_t *fail_cols, cu
 
 extern "C" int64_t glu_factor_batch_device(glu_handle *h, int64_t batch, double *v, double thresh,
                                            int64_t *fail_cols, void *stream) {
+    DeviceGuard dg_(h);
     if (batch < 0 || (batch > 0 && (!v || !fail_cols))) { glu::set_error("bad batch arguments"); return GLU_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = ensure_batch(h, std::max<int64_t>(batch, 1));
     if (rc != GLU_OK) return rc;
-    // up to 8 sets per launch: they share each item's static loads,
+    // up to 16 sets per launch: they share each item's static loads,
     // dependency wait and release; a dense tail runs one cluster per set
+    const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
+    GLU_CUDA(cudaMemsetAsync(h->err_acc, 0, sizeof(int), s));
     for (int64_t b0 = 0; b0 < batch; b0 += kMaxBatchPerLaunch) {
         const int nb = (int)std::min<int64_t>(kMaxBatchPerLaunch, batch - b0);
         if ((rc = launch_factor(h, v + b0 * h->nnz, thresh, s, h->fail_batch + b0, nb)) != GLU_OK) return rc;
+        err_or_kernel<<<1, 1, 0, s>>>(h->err_acc, (const int *)(h->sync + nl8));
     }
     return batch_status(h, batch, fail_cols, s);
 }
 
 extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const double *a_vals,
                                          double *lu_out, double thresh, int64_t *fail_cols) {
+    DeviceGuard dg_(h);
     if (h->nz < 0) { glu::set_error("glu_set_input_pattern not called"); return GLU_EINVAL; }
     if (batch < 0 || (batch > 0 && (!a_vals || !lu_out || !fail_cols))) {
         glu::set_error("bad batch arguments");
@@ -2689,6 +2723,8 @@ extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const dou
         GLU_CUDA(cudaMalloc((void **)&h->d_ab, sizeof(double) * std::max<i64>(h->nz, 1) * chunk));
     }
     double *dv = batched ? h->d_vb : h->d_v, *da = batched ? h->d_ab : h->d_a;
+    const size_t nl8 = (size_t)std::max<i64>(h->n_levels, 1) * 8;
+    GLU_CUDA(cudaMemsetAsync(h->err_acc, 0, sizeof(int), s));
     for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
         const int nb = (int)std::min<int64_t>(chunk, batch - b0);
         GLU_CUDA(cudaMemcpyAsync(da, a_vals + b0 * h->nz, sizeof(double) * h->nz * nb,
@@ -2697,6 +2733,7 @@ extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const dou
             if ((rc = glu_scatter_device(h, da + (size_t)k * h->nz, dv + (size_t)k * h->nnz, s)) != GLU_OK)
                 return rc;
         if ((rc = launch_factor(h, dv, thresh, s, h->fail_batch + b0, nb)) != GLU_OK) return rc;
+        err_or_kernel<<<1, 1, 0, s>>>(h->err_acc, (const int *)(h->sync + nl8));
         GLU_CUDA(cudaMemcpyAsync(lu_out + b0 * h->nnz, dv, sizeof(double) * h->nnz * nb,
                                  cudaMemcpyDeviceToHost, s));
     }
@@ -2935,6 +2972,7 @@ static int64_t check_zero_pivot(glu_handle *h, const double *lu, cudaStream_t s)
 }
 
 extern "C" int64_t glu_lower_solve_device(glu_handle *h, const double *lu, double *x, void *stream) {
+    DeviceGuard dg_(h);
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = run_solves(h, lu, x, 1, s);
     if (rc != GLU_OK) return rc;
@@ -2943,6 +2981,7 @@ extern "C" int64_t glu_lower_solve_device(glu_handle *h, const double *lu, doubl
 }
 
 extern "C" int64_t glu_upper_solve_device(glu_handle *h, const double *lu, double *x, void *stream) {
+    DeviceGuard dg_(h);
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = check_zero_pivot(h, lu, s);
     if (rc != GLU_OK) return rc;
@@ -2953,6 +2992,7 @@ extern "C" int64_t glu_upper_solve_device(glu_handle *h, const double *lu, doubl
 }
 
 extern "C" int64_t glu_solve_device(glu_handle *h, const double *lu, double *x, void *stream) {
+    DeviceGuard dg_(h);
     cudaStream_t s = (cudaStream_t)stream;
     i64 rc = check_zero_pivot(h, lu, s);
     if (rc != GLU_OK) return rc;
@@ -2974,6 +3014,7 @@ static int64_t ensure_staging(glu_handle *h) {
 // order is the reference's, so every column is bitwise the single solve.
 extern "C" int64_t glu_solve_multi_device(glu_handle *h, const double *lu, double *x, int64_t nrhs,
                                           int64_t ldx, int32_t part, void *stream) {
+    DeviceGuard dg_(h);
     if (nrhs < 0 || (nrhs > 0 && ldx < h->n) || part < 0 || part > 2) {
         glu::set_error("bad multi-RHS solve arguments");
         return GLU_EINVAL;
@@ -2993,6 +3034,7 @@ extern "C" int64_t glu_solve_multi_device(glu_handle *h, const double *lu, doubl
 // reference's upper_solve raises for that set (its x is then unspecified).
 extern "C" int64_t glu_solve_batch_device(glu_handle *h, const double *lu, int64_t lu_stride, double *x,
                                           int64_t nb, int64_t ldx, int64_t *status, void *stream) {
+    DeviceGuard dg_(h);
     if (nb < 0 || (nb > 0 && (ldx < h->n || lu_stride < h->nnz))) {
         glu::set_error("bad batch solve arguments");
         return GLU_EINVAL;
@@ -3016,6 +3058,7 @@ extern "C" int64_t glu_solve_batch_device(glu_handle *h, const double *lu, int64
 }
 
 extern "C" int64_t glu_factor_host(glu_handle *h, const double *a_vals, double *lu_out, double thresh) {
+    DeviceGuard dg_(h);
     if (h->nz < 0) { glu::set_error("glu_set_input_pattern not called"); return GLU_EINVAL; }
     i64 rc = ensure_staging(h);
     if (rc != GLU_OK) return rc;
@@ -3046,6 +3089,7 @@ extern "C" int64_t glu_factor_host(glu_handle *h, const double *a_vals, double *
 }
 
 extern "C" int64_t glu_solve_host(glu_handle *h, const double *lu, const double *b, double *x) {
+    DeviceGuard dg_(h);
     i64 rc = ensure_staging(h);
     if (rc != GLU_OK) return rc;
     cudaStream_t s = h->stream;

@@ -246,6 +246,45 @@ extern "C" int64_t glu_detect_upward(int64_t n, const int64_t *col_ptr, const in
     return e;
 }
 
+// depgraph.py:129-156 detect_double_u_exact (the GLU2.0 detector the
+// relaxed rule replaces; a debugging oracle): column t depends on i (L(t,i)
+// != 0) when some j in {t} u L(:,t) has row j sharing a column k > t with
+// row i, plus the upward edges.  Per column t the columns k > t of the rows
+// {t} u L(:,t) are stamped once, then each candidate row i is scanned for a
+// stamped column -- the same union the reference's per-j set intersections
+// test.  dep_idx needs nnz entries.  Returns the edge count.
+extern "C" int64_t glu_detect_double_u_exact(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                                             const int64_t *diag_pos, const int64_t *row_ptr,
+                                             const int64_t *col_idx, int64_t *dep_ptr, int64_t *dep_idx) {
+    std::vector<i64> stamp(n, -1), cand;
+    i64 e = 0;
+    dep_ptr[0] = 0;
+    auto mark_row = [&](i64 j, i64 t) {
+        for (i64 q = row_ptr[j + 1] - 1; q >= row_ptr[j] && col_idx[q] > t; q--) stamp[col_idx[q]] = t;
+    };
+    for (i64 t = 0; t < n; t++) {
+        cand.clear();
+        for (i64 p = col_ptr[t]; p < diag_pos[t]; p++) {  // upward: U(i,t), L(:,i) non-empty
+            const i64 i = row_idx[p];
+            if (col_ptr[i + 1] - diag_pos[i] > 1) cand.push_back(i);
+        }
+        mark_row(t, t);
+        for (i64 p = diag_pos[t] + 1; p < col_ptr[t + 1]; p++) mark_row(row_idx[p], t);
+        for (i64 q = row_ptr[t]; q < row_ptr[t + 1] && col_idx[q] < t; q++) {  // L(t,i) != 0
+            const i64 i = col_idx[q];
+            bool found = false;
+            for (i64 r = row_ptr[i + 1] - 1; r >= row_ptr[i] && col_idx[r] > t && !found; r--)
+                found = stamp[col_idx[r]] == t;
+            if (found) cand.push_back(i);
+        }
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+        for (i64 i : cand) dep_idx[e++] = i;
+        dep_ptr[t + 1] = e;
+    }
+    return e;
+}
+
 extern "C" int64_t glu_levelize(int64_t n, const int64_t *dep_ptr, const int64_t *dep_idx,
                                 int64_t *level_of, int64_t *level_ptr, int64_t *level_cols) {
     i64 nl = 0;

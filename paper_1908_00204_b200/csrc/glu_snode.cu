@@ -711,7 +711,6 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
     cudaError_t e = cudaMemsetAsync(d->done, 0, sizeof(unsigned) * kDoneStride * std::max<i64>(d->n_phases, 1), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d->gdone, 0, sizeof(unsigned) * kGdoneRep * kLine, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d->cmax, 0, sizeof(unsigned long long) * std::max<i64>(d->n, 1), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(err, 0, sizeof(int), s);
     if (e != cudaSuccess) {
         set_error(std::string("sn_launch: ") + cudaGetErrorString(e));
         return GLU_ECUDA;

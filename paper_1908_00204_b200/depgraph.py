@@ -1,12 +1,11 @@
 """Column dependencies and levelization (API of levlu/depgraph.py).
 
-The relaxed detector (paper Alg. 4, levlu/depgraph.py:113-126) and
-``levelize`` (levlu/depgraph.py:159-170) run natively and keep the edge
+The detectors (upward, relaxed = paper Alg. 4, the exact GLU2.0 double-U
+rule; levlu/depgraph.py:96-156), ``levelize`` (:159-170) and
+``simulate_hazards`` (:173-205) run natively on the host and keep edge
 lists in CSR form; ``DependencyGraph.deps`` materializes the reference's
-list-of-arrays view on demand.  ``simulate_hazards`` and the exact
-double-U detector are CPU debugging oracles that the reference keeps for
-itself; schedule safety on the GPU path is
-checked by the plan builder instead (numeric.py, detect_races).
+list-of-arrays view on demand, and ``DependencyGraph(n, deps, method)``
+builds a graph from that view as the reference's dataclass does.
 """
 
 from __future__ import annotations
@@ -27,14 +26,25 @@ class DetectMethod(enum.Enum):
 
 
 class DependencyGraph:
-    """Per-column sorted lists of strictly smaller columns each column needs."""
+    """Per-column sorted lists of strictly smaller columns each column needs
+    (levlu/depgraph.py:27-38: DependencyGraph(n, deps, method))."""
 
-    def __init__(self, n: int, dep_ptr: np.ndarray, dep_idx: np.ndarray, method: DetectMethod):
+    def __init__(self, n: int, deps: list, method: DetectMethod):
         self.n = n
-        self.dep_ptr = dep_ptr
-        self.dep_idx = dep_idx
         self.method = method
-        self._deps = None
+        self._deps = list(deps)
+        if len(self._deps) != n:
+            raise ValueError("one dependency list per column")
+        lens = np.array([len(d) for d in self._deps], dtype=np.int64)
+        self.dep_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        self.dep_idx = (np.concatenate([np.asarray(d, dtype=np.int64) for d in self._deps])
+                        if self.dep_ptr[-1] else np.empty(0, dtype=np.int64))
+
+    @classmethod
+    def from_csr(cls, n: int, dep_ptr: np.ndarray, dep_idx: np.ndarray, method: DetectMethod):
+        g = cls.__new__(cls)
+        g.n, g.method, g.dep_ptr, g.dep_idx, g._deps = n, method, dep_ptr, dep_idx, None
+        return g
 
     @property
     def deps(self) -> list:
@@ -42,6 +52,14 @@ class DependencyGraph:
             p, d = self.dep_ptr, self.dep_idx
             self._deps = [d[p[j]:p[j + 1]] for j in range(self.n)]
         return self._deps
+
+    def __eq__(self, other):
+        if not isinstance(other, DependencyGraph):
+            return NotImplemented
+        return (self.n == other.n and self.method == other.method and
+                np.array_equal(self.dep_ptr, other.dep_ptr) and np.array_equal(self.dep_idx, other.dep_idx))
+
+    __hash__ = None
 
     @property
     def edge_count(self) -> int:
@@ -107,7 +125,7 @@ def detect_relaxed(fp: FilledPattern) -> DependencyGraph:
     e = _lib.check(_lib.lib.glu_detect_relaxed(n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
                                                _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(dep_ptr),
                                                _lib.ptr(dep_idx)), "detect_relaxed")
-    return DependencyGraph(n, dep_ptr, dep_idx[:e].copy(), DetectMethod.RELAXED)
+    return DependencyGraph.from_csr(n, dep_ptr, dep_idx[:e].copy(), DetectMethod.RELAXED)
 
 
 def detect_upward(fp: FilledPattern) -> DependencyGraph:
@@ -119,7 +137,42 @@ def detect_upward(fp: FilledPattern) -> DependencyGraph:
     e = _lib.check(_lib.lib.glu_detect_upward(n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
                                               _lib.ptr(dep_ptr), _lib.ptr(dep_idx)),
                    "detect_upward")
-    return DependencyGraph(n, dep_ptr, dep_idx[:e].copy(), DetectMethod.UPWARD)
+    return DependencyGraph.from_csr(n, dep_ptr, dep_idx[:e].copy(), DetectMethod.UPWARD)
+
+
+def detect_double_u_exact(fp: FilledPattern) -> DependencyGraph:
+    """Exact GLU2.0 detection (levlu/depgraph.py:129-156): upward edges plus
+    the double-U rule -- t depends on i (L(t,i) != 0) when a row j in
+    {t} u L(:,t) shares a column k > t with row i."""
+    cp, ri, dp, rp, ci = _fp_arrays(fp)
+    n = fp.n
+    dep_ptr = np.zeros(n + 1, dtype=np.int64)
+    dep_idx = np.empty(max(int(cp[-1]) if n else 0, 1), dtype=np.int64)
+    e = _lib.check(_lib.lib.glu_detect_double_u_exact(n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),
+                                                      _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(dep_ptr),
+                                                      _lib.ptr(dep_idx)), "detect_double_u_exact")
+    return DependencyGraph.from_csr(n, dep_ptr, dep_idx[:e].copy(), DetectMethod.DOUBLE_U_EXACT)
+
+
+def simulate_hazards(fp: FilledPattern, s: LevelSchedule) -> HazardReport:
+    """Same-level (writer, reader) pairs whose right-looking write set meets
+    the reader's multiplier read set (levlu/depgraph.py:173-205), in the
+    reference's order: level, writer, reader, element.  Evaluated natively
+    in O(MACs) instead of the reference's per-level set products."""
+    seen = np.concatenate(s.levels) if s.levels else np.empty(0, dtype=np.int64)
+    if len(seen) != fp.n or len(np.unique(seen)) != fp.n:
+        raise ValueError("schedule is not a partition of the columns")
+    cp, ri, dp, rp, ci = _fp_arrays(fp)
+    lv = _lib.i64(s.level_of)
+    cap = 1 << 16
+    while True:
+        out = np.zeros((cap, 5), dtype=np.int64)
+        total = int(_lib.lib.glu_find_hazards(fp.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp), _lib.ptr(rp),
+                                              _lib.ptr(ci), _lib.ptr(lv), cap, _lib.ptr(out)))
+        if total <= cap:
+            break
+        cap = 4 * total
+    return HazardReport([Hazard(int(w), int(r), (int(i), int(k)), int(l)) for l, w, r, i, k in out[:total]])
 
 
 def _graph_csr(g) -> tuple[np.ndarray, np.ndarray]:

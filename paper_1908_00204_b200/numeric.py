@@ -324,6 +324,12 @@ def _stream(s):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def _current_device() -> int:
+    import torch
+
+    return torch.cuda.current_device() if torch.cuda.is_available() else -1
+
+
 _CACHE: dict = {}
 # re-entrant: a weakref callback (_drop) can fire from GC while
 # get_factorizer holds the lock and allocates
@@ -366,7 +372,7 @@ def get_factorizer(fp: FilledPattern, level_of: np.ndarray, contract: int,
         engine = pick_engine(fp, contract)
     if engine == "sn":
         tail = True  # one plan serves single and batched launches
-    key = (id(fp), contract, _digest(level_of), tail, engine)
+    key = (id(fp), contract, _digest(level_of), tail, engine, _current_device())
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
         if hit is not None and hit[0]() is fp:

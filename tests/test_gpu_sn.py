@@ -99,6 +99,42 @@ def test_sn_g200_full_size_bitwise():
     assert fz.sn_info["macs"] == numeric.pattern_flops(fp)[0]
 
 
+def test_sn_g400_full_size_bitwise():
+    a = synthetic.make("g400")
+    fp = glu.symbolic_fillin(a.pattern)
+    ref, err = _oracle_a(fp, a)
+    vals, rc, _ = _sn_factor(a, fp)
+    assert err == -1 and rc == -1 and np.array_equal(vals, ref)
+
+
+def test_sn_batch_sets_bitwise():
+    """refactorize_batch through the supernodal engine (one launch per set):
+    every set bitwise, a singular set reported at its own column."""
+    import os
+
+    old = os.environ.get("GLU_ENGINE")
+    os.environ["GLU_ENGINE"] = "sn"
+    try:
+        a = synthetic.grid5(40, seed=3)
+        fp = glu.symbolic_fillin(a.pattern)
+        lu = glu.factor_left_looking(a, fp)
+        sets = np.stack([synthetic.perturb_values(a, 50 + b) for b in range(3)])
+        sets[1] = 0.0
+        vals, st = glu.refactorize_batch(lu, a, sets)
+        pat = orc.Pattern.from_fp(fp)
+        for b in range(3):
+            v, _ = orc.scatter(pat, a.col_ptr, a.row_idx, sets[b])
+            err = orc.factor_left_looking(pat, v)
+            assert st[b] == err
+            if err == -1:
+                assert np.array_equal(vals[b], v)
+    finally:
+        if old is None:
+            os.environ.pop("GLU_ENGINE", None)
+        else:
+            os.environ["GLU_ENGINE"] = old
+
+
 def test_sn_public_api_engine_switch(monkeypatch):
     """GLU_ENGINE=sn routes the reference API (left-looking, factor_parallel
     deterministic, refactorize) through the supernodal engine."""
