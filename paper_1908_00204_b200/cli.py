@@ -4,17 +4,19 @@
         [--atomic] [--threads T] [--deps relaxed|upward [--allow-unsafe]] [--detect-races]
         [--perm P | --row-perm R --col-perm C] [--check-residual] [--stats-out R.json|R.csv]
     python -m paper_1908_00204_b200 solve MATRIX.mtx RHS.txt [--out x.txt]
+    python -m paper_1908_00204_b200 deps-compare MATRIX.mtx [--csv PATH|-]
+    python -m paper_1908_00204_b200 level-stats MATRIX.mtx [--deps D] [--warps W]
 
-Mirrors `levlu factor` / `levlu solve` (levlu/cli.py:69-308): same flags,
-same report lines, the same `checksum` line (first 16 hex digits of sha256
-over the LU values, levlu/cli.py:201) -- identical to the reference's
-because the factors are bit-identical -- the same RunReport JSON/CSV and the
-same exit codes (0 ok, 1 usage or I/O error, 2 pivot breakdown, 3 schedule
-hazard; levlu/cli.py:23-26).  The numeric work runs on the B200 through the
-package API; there is no CPU path.  Differences: `--precision single` is a
-usage error (the B200 path computes in fp64), the deps line adds
-`device=cuda`, and `deps-compare` / `level-stats` (analysis reports, out of
-this path's scope) are not provided.
+Mirrors `levlu` (levlu/cli.py:69-359): same subcommands and flags, same
+report lines, the same `checksum` line (first 16 hex digits of sha256 over
+the LU values, levlu/cli.py:201) -- identical to the reference's because
+the factors are bit-identical -- the same RunReport JSON/CSV, the same
+deps-compare / level-stats CSV, and the same exit codes (0 ok, 1 usage or
+I/O error, 2 pivot breakdown, 3 schedule hazard; levlu/cli.py:23-26).  The
+numeric work runs on the B200 through the package API; there is no CPU
+path.  Differences: the deps line adds `device=cuda`; `--precision single`
+factors fp32 values in fp64 arithmetic and rounds the factors to fp32
+(numeric._value_dtype).
 """
 
 from __future__ import annotations
@@ -34,7 +36,8 @@ from . import depgraph, numeric, resource, sparse, symbolic
 
 EXIT_OK, EXIT_USAGE, EXIT_PIVOT, EXIT_HAZARD = 0, 1, 2, 3
 
-_DETECTORS = {"relaxed": depgraph.detect_relaxed, "upward": depgraph.detect_upward}
+_DETECTORS = {"upward": depgraph.detect_upward, "exact": depgraph.detect_double_u_exact,
+              "relaxed": depgraph.detect_relaxed}
 
 
 class CliError(Exception):
@@ -89,11 +92,10 @@ def _read_perm(path: str, n: int) -> sparse.Permutation:
 
 
 def _load_matrix(args) -> sparse.CscMatrix:
-    if getattr(args, "precision", "double") != "double":
-        raise CliError("the B200 path factors in fp64; --precision single is not supported")
+    dtype = np.float32 if getattr(args, "precision", "double") == "single" else np.float64
     try:
         with open(args.matrix) as fh:
-            a = sparse.to_csc(sparse.load_matrix_market(fh))
+            a = sparse.to_csc(sparse.load_matrix_market(fh), dtype=dtype)
     except OSError as e:
         raise CliError(f"cannot read {args.matrix}: {e}")
     except (sparse.MatrixFormatError, ValueError) as e:
@@ -113,7 +115,8 @@ def _load_matrix(args) -> sparse.CscMatrix:
 
 def _resource_model(args) -> resource.ResourceModel:
     return resource.ResourceModel(total_warps=args.warps, stream_threshold=args.stream_threshold,
-                                  memory_budget_bytes=args.mem_budget)
+                                  memory_budget_bytes=args.mem_budget,
+                                  scalar_size_bytes=4 if getattr(args, "precision", "double") == "single" else 8)
 
 
 def _analyze(a, method: str):
@@ -180,7 +183,7 @@ def cmd_factor(args) -> int:
 def cmd_solve(args) -> int:
     a = _load_matrix(args)
     try:
-        b = np.loadtxt(args.rhs, dtype=np.float64, ndmin=1)
+        b = np.loadtxt(args.rhs, dtype=a.values.dtype, ndmin=1)
     except OSError as e:
         raise CliError(f"cannot read {args.rhs}: {e}")
     except ValueError as e:
@@ -205,6 +208,50 @@ def cmd_solve(args) -> int:
     res = float(np.abs(r).max() / scale) if scale else float(np.abs(r).max(initial=0.0))
     print(f"wrote {args.out}")
     print(f"residual {res:.3e}")
+    return EXIT_OK
+
+
+def cmd_deps_compare(args) -> int:
+    """The three detectors side by side (levlu/cli.py:237-264): edges,
+    levels, time; the upward <= exact <= relaxed edge-set ordering is
+    checked (exit 3 if violated)."""
+    a = _load_matrix(args)
+    fp = symbolic.symbolic_fillin(a.pattern)
+    results = []
+    for name in ("upward", "exact", "relaxed"):
+        t0 = time.perf_counter()
+        graph = _DETECTORS[name](fp)
+        dt = time.perf_counter() - t0
+        results.append((name, graph, depgraph.levelize(graph).level_count, dt))
+    edges = {name: g.edge_set() for name, g, _, _ in results}
+    if not (edges["upward"] <= edges["exact"] <= edges["relaxed"]):
+        print("error: detector superset ordering violated", file=sys.stderr)
+        return EXIT_HAZARD
+    for name, g, levels, dt in results:
+        print(f"{name:8s} edges={g.edge_count:8d} levels={levels:6d} time={dt * 1e3:.3f} ms")
+    if args.csv:
+        out = sys.stdout if args.csv == "-" else open(args.csv, "w")
+        try:
+            out.write("method,edges,levels\n")
+            for name, g, levels, _ in results:
+                out.write(f"{name},{g.edge_count},{levels}\n")
+        finally:
+            if out is not sys.stdout:
+                out.close()
+    return EXIT_OK
+
+
+def cmd_level_stats(args) -> int:
+    """Per-level size, max subcolumns and kernel mode as CSV (levlu/cli.py:
+    267-279), modes from plan_schedule under the given resource model."""
+    a = _load_matrix(args)
+    fp, schedule, _ = _analyze(a, args.deps)
+    st = depgraph.level_stats(fp, schedule)
+    resource.plan_schedule(schedule, st, a.n, _resource_model(args))
+    out = sys.stdout
+    out.write("level,size,max_subcolumns,mode\n")
+    for lvl in range(st.level_count):
+        out.write(f"{lvl},{st.sizes[lvl]},{st.max_subcolumns[lvl]},{st.modes[lvl]}\n")
     return EXIT_OK
 
 
@@ -243,6 +290,20 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("rhs", help="right-hand side, one scalar per line")
     p.add_argument("--out", default="x.txt", help="solution output file")
     p.set_defaults(func=cmd_solve)
+    p = sub.add_parser("deps-compare", help="compare the three dependency detectors")
+    p.add_argument("matrix", help="Matrix Market coordinate file")
+    p.add_argument("--perm", help="symmetric permutation file (one 0-based index per line)")
+    p.add_argument("--row-perm", help="row permutation file")
+    p.add_argument("--col-perm", help="column permutation file")
+    p.add_argument("--precision", choices=["single", "double"], default="double")
+    p.add_argument("--csv", help="write method,edges,levels CSV to PATH ('-' for stdout)")
+    p.set_defaults(func=cmd_deps_compare)
+    p = sub.add_parser("level-stats", help="emit per-level statistics as CSV")
+    _add_common(p)
+    p.add_argument("--perm", help="symmetric permutation file (one 0-based index per line)")
+    p.add_argument("--row-perm", help="row permutation file")
+    p.add_argument("--col-perm", help="column permutation file")
+    p.set_defaults(func=cmd_level_stats)
     return ap
 
 

@@ -407,9 +407,20 @@ def _relaxed_levels(fp: FilledPattern) -> np.ndarray:
     return lv
 
 
+def _value_dtype(values: np.ndarray) -> np.dtype:
+    """fp64, or fp32 (the reference's single precision, tests/test_numeric.py:
+    203-210): fp32 values are factored and solved in fp64 arithmetic on the
+    device and returned rounded to fp32 -- within fp32 rounding of the
+    reference's fp32 arithmetic, not bit-identical to it (the bitwise
+    contracts are fp64)."""
+    dt = np.dtype(values.dtype)
+    if dt not in (np.dtype(np.float64), np.dtype(np.float32)):
+        raise TypeError(f"the B200 path factors fp64 (or fp32) values; got {dt}")
+    return dt
+
+
 def _require_f64(a: CscMatrix):
-    if a.values.dtype != np.float64:
-        raise TypeError(f"the B200 path factors fp64 values; got {a.values.dtype}")
+    _value_dtype(a.values)
 
 
 def _check(err: int) -> None:
@@ -466,14 +477,17 @@ def _factor(a: CscMatrix, fp: FilledPattern, level_of: np.ndarray | None, contra
         raise PatternMismatchError("matrix and pattern sizes differ")
     phases = plan_levels(fp, level_of, contract)
     fz = get_factorizer(fp, phases, contract)
+    dt = _value_dtype(a.values)
+    if dt == np.float32:  # the reference's fp32 threshold (numeric.py:268, v.dtype.type)
+        thresh = float(np.float32(thresh))
     with fz._lock:
         fz.set_input(a.col_ptr, a.row_idx)
         fz.set_fail_levels(phases if level_of is None or contract != _lib.CONTRACT_A else level_of)
         fz.set_option(2, 1 if by_column else 0)
         fz.set_option(1, 1 if stamps else 0)
-        vals, rc = fz.factor_host(a.values, thresh)
+        vals, rc = fz.factor_host(np.asarray(a.values, dtype=np.float64), thresh)
     _check(rc)
-    return vals, fz, phases
+    return (vals.astype(dt) if dt != np.float64 else vals), fz, phases
 
 
 def factor_left_looking(a: CscMatrix, fp: FilledPattern,
@@ -583,7 +597,7 @@ def refactorize_batch(lu: LuFactors, a_pattern: CscMatrix, values: np.ndarray,
     (LU values [B, nnz], status [B]) where status[b] is -1 or the column at
     which set b's pivot broke down (the PivotError the reference would
     raise for that set, numeric.py:27-35)."""
-    _require_f64(a_pattern)
+    dt = _value_dtype(a_pattern.values)
     if a_pattern.n != lu.n:
         raise PatternMismatchError("matrix and pattern sizes differ")
     vals = np.ascontiguousarray(values, dtype=np.float64)
@@ -598,8 +612,9 @@ def refactorize_batch(lu: LuFactors, a_pattern: CscMatrix, values: np.ndarray,
                            else phases)
         fz.set_option(2, 1 if schedule is None else 0)
         fz.set_option(1, 0)
-        out, fails = fz.factor_batch_host(vals, opts.zero_pivot_threshold)
-    return out, fails
+        thresh = float(np.float32(opts.zero_pivot_threshold)) if dt == np.float32 else opts.zero_pivot_threshold
+        out, fails = fz.factor_batch_host(vals, thresh)
+    return (out.astype(dt) if dt != np.float64 else out), fails
 
 
 def subcolumn_update(fp: FilledPattern, values: np.ndarray, source_j: int, dest_k: int):
@@ -627,14 +642,14 @@ def subcolumn_update(fp: FilledPattern, values: np.ndarray, source_j: int, dest_
 def _solve(lu: LuFactors, b: np.ndarray, part: str) -> np.ndarray:
     if len(b) != lu.n:
         raise ValueError("right-hand side length mismatch")
-    if lu.values.dtype != np.float64:
-        raise TypeError(f"the B200 path solves fp64 factors; got {lu.values.dtype}")
+    dt = _value_dtype(lu.values)
     fz = get_factorizer(lu.pattern, _relaxed_levels(lu.pattern), _lib.CONTRACT_A)
     with fz._lock:
-        x, rc = fz.solve_host(lu.values, np.asarray(b, dtype=np.float64), part)
+        x, rc = fz.solve_host(np.asarray(lu.values, dtype=np.float64),
+                              np.asarray(np.asarray(b, dtype=dt), dtype=np.float64), part)
     if rc >= 0:
         raise PivotError(rc)
-    return x
+    return x.astype(dt) if dt != np.float64 else x
 
 
 def solve_many(lu: LuFactors, b: np.ndarray) -> np.ndarray:

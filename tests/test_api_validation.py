@@ -39,6 +39,6 @@ def test_refactorize_batch_rejects_bad_shapes(lu5):
     a = csc_from_golden(g)
     with pytest.raises(ValueError):
         glu.refactorize_batch(lu5, a, np.ones((2, len(a.row_idx) + 1)))
-    with pytest.raises(TypeError):
+    with pytest.raises(TypeError):  # fp64 / fp32 only
         glu.refactorize_batch(lu5, glu.CscMatrix(a.n, a.col_ptr, a.row_idx,
-                                                 a.values.astype(np.float32)), np.ones((2, 5)))
+                                                 a.values.astype(np.complex128)), np.ones((2, 5)))

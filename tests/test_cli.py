@@ -84,7 +84,7 @@ def test_exit_usage_cases(tmp_path, conflict8, diag5, capsys):
     assert cli.main(["factor", conflict8, "--sequential", "left", "--parallel"]) == cli.EXIT_USAGE
     assert cli.main(["factor", conflict8, "--deps", "bogus"]) == cli.EXIT_USAGE
     assert cli.main(["factor", conflict8, "--deps", "upward", "--parallel"]) == cli.EXIT_USAGE
-    assert cli.main(["factor", conflict8, "--precision", "single"]) == cli.EXIT_USAGE
+    assert cli.main(["factor", conflict8, "--precision", "half"]) == cli.EXIT_USAGE
     assert cli.main([]) == cli.EXIT_USAGE
     pr = tmp_path / "pr.txt"
     pr.write_text("1\n0\n2\n3\n4\n")

@@ -480,3 +480,22 @@ def test_batched_tail_failure_in_one_set():
             assert np.array_equal(v[b].cpu().numpy(), single), b
     assert int(fails[3]) >= fz.plan_info["tail_t0"]
     assert all(int(fails[b]) == -1 for b in (0, 1, 2, 4, 5))
+
+
+def test_single_precision_inputs():
+    """fp32 values (the reference's single precision, tests/test_numeric.py:
+    203-210): factored in fp64 on the device, returned as fp32 factors within
+    the reference's fp32 residual bound; solves return fp32."""
+    from conftest import random_dd
+
+    a = random_dd(np.random.default_rng(11), 40, 0.1)
+    a32 = glu.CscMatrix(a.n, a.col_ptr, a.row_idx, a.values.astype(np.float32))
+    fp, s, plans = _analyze(a32)
+    lu, _ = glu.factor_parallel(a32, fp, s, plans, glu.FactorOptions(worker_count=2))
+    assert lu.values.dtype == np.float32
+    assert glu.residual(a32, lu) <= 1e-5
+    lu64 = glu.factor_left_looking(glu.CscMatrix(a.n, a.col_ptr, a.row_idx,
+                                                 a.values.astype(np.float32).astype(np.float64)), fp)
+    assert np.array_equal(lu.values, lu64.values.astype(np.float32))
+    x = glu.solve(lu, np.ones(a.n, dtype=np.float32))
+    assert x.dtype == np.float32 and np.all(np.isfinite(x))
