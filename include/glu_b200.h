@@ -160,7 +160,7 @@ void glu_sn_plan_info(const glu_plan *p, int64_t *info);
 /* Copies a supernodal plan out (sizes from glu_sn_plan_info; int32 x4
    records): sn {s0, s1, |R_S|, first pair}, pan {p0, p1, supernode, rows
    below}, pairs {k, a, base, map}, relmap, push {panel, pair0, pair1,
-   target panel}, tasks (2 records each) {kind << 28 | chunk, phase, p0, p1,
+   target panel}, tasks (2 records each) {kind << 27 | chunk, phase, p0, p1,
    s1, rows below the panel, pair0, pair1}, phase_ptr[phases+1],
    col_a[n].  Any pointer may be NULL. */
 void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *pairs,

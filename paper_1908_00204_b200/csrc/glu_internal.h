@@ -76,11 +76,13 @@ struct alignas(16) I4 {
     int32_t x, y, z, w;
 };
 
+// task kind = record.x >> 27: the kind in bits 1-2, kSnLocal in bit 0
 enum SnTaskKind : int32_t {
-    kSnDiag = 0,  // factor a panel's w x w diagonal block (+ column maxima above it)
-    kSnTrsm = 1,  // 32 rows below a panel: divide, in-panel updates
-    kSnTri = 2,   // U(P, K): forward substitution inside a push's source panel
-    kSnRect = 3,  // 32 rows below the source panel into every column of a push
+    kSnDiag = 0 << 1,  // factor a panel's w x w diagonal block and write it back
+    kSnTrsm = 1 << 1,  // 32 rows below a panel: divide, in-panel updates
+    kSnTri = 2 << 1,   // U(P, K): forward substitution inside a push's source panel
+    kSnRect = 3 << 1,  // 32 rows below the source panel into every column of a push
+    kSnLocal = 1,      // TRSM / TRI: factor the (not yet written back) diagonal block locally
 };
 
 struct SnPlan {
@@ -90,7 +92,7 @@ struct SnPlan {
     std::vector<I4> pairs;   // per (supernode S, target column k): {k, a, base, map}
     std::vector<int32_t> relmap;  // positions of R_S's rows in column k (absolute slots)
     std::vector<I4> push;    // {source panel, first pair, end pair, target panel}
-    std::vector<I4> tasks;   // 2 per task, phase order: {kind << 28 | chunk, phase, p0, p1}, {s1, h, pair0, pair1}
+    std::vector<I4> tasks;   // 2 per task, phase order: {kind << 27 | chunk, phase, p0, p1}, {s1, h, pair0, pair1}
     std::vector<int32_t> phase_ptr;  // tasks of phase p: [phase_ptr[p], phase_ptr[p+1])
     std::vector<int32_t> col_a;      // per column c: first row of c's supernode present in c
     int64_t n_stages = 0;

@@ -28,11 +28,12 @@
 //     order (the kernel's chains), and panel K is factored in the stage after
 //     its last push.
 //
-// Each stage has three phases (the kernel's only synchronisation):
-//   0  DIAG(P)    factor the w x w diagonal block of every panel of the stage
-//   1  TRSM(P,c)  rows below it, 32 at a time: divide and in-panel updates
+// Each stage has two phases (the kernel's only synchronisation):
+//   0  TRSM(P,c)  rows below the panel, 32 at a time: divide and in-panel
+//                 updates (factoring the w x w diagonal block locally)
 //      TRI(push)  U(P, K) = forward substitution inside the source panel
-//   2  RECT(push,c) rows below P, 32 at a time, into every column of K
+//   1  RECT(push,c) rows below P, 32 at a time, into every column of K
+//      DIAG(P)    the factored diagonal block written back
 // Empty phases are dropped.
 #include <algorithm>
 #include <atomic>
@@ -277,55 +278,72 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
     }
     P->macs = macs;
 
-    // 6. tasks in phase order (3 phases per stage, empty phases dropped)
+    // 6. tasks in phase order: two phases per stage, empty phases dropped.
+    //   phase 2s     TRSM(P) of the panels factored in stage s and TRI of the
+    //                stage's pushes; both factor P's w x w diagonal block
+    //                themselves when it is not yet factored (kSnLocal: the
+    //                panel's own stage), from values no task of the phase writes
+    //   phase 2s + 1 RECT of the stage's pushes, and DIAG(P), which writes
+    //                the factored block back (nothing in this phase reads it)
+    // Inside a phase tasks are ordered by estimated cost, largest first, so
+    // the static round-robin deal gives every warp a similar load.
     i64 n_stages = 0;
     for (i64 p = 0; p < np; p++) n_stages = std::max<i64>(n_stages, fstage[p] + 1);
     for (i32 s : push_stage) n_stages = std::max<i64>(n_stages, s + 1);
     P->n_stages = n_stages;
-    const i64 nph = 3 * n_stages;
-    std::vector<i64> cnt(nph + 1, 0);
+    const i64 nph = 2 * n_stages;
     auto chunks = [](i64 h) { return (h + 31) / 32; };
-    for (i64 p = 0; p < np; p++) {
-        cnt[3 * fstage[p]]++;
-        cnt[3 * fstage[p] + 1] += chunks(P->pan[p].w);
-    }
-    const i64 npush = (i64)P->push.size();
-    for (i64 x = 0; x < npush; x++) {
-        const i64 h = P->pan[P->push[x].x].w;
-        if (push_tri[x]) cnt[3 * push_stage[x] + 1]++;
-        cnt[3 * push_stage[x] + 2] += chunks(h);
-    }
-    std::vector<i32> remap(nph, -1);
-    i64 live = 0, total = 0;
-    for (i64 f = 0; f < nph; f++)
-        if (cnt[f] > 0) { remap[f] = (i32)live++; total += cnt[f]; }
-    if (total >= (i64)INT32_MAX) {
-        set_error("supernodal plan: >= 2^31 tasks");
-        return GLU_EINVAL;
-    }
-    P->phase_ptr.assign(live + 1, 0);
-    for (i64 f = 0; f < nph; f++)
-        if (remap[f] >= 0) P->phase_ptr[remap[f] + 1] = (i32)cnt[f];
-    for (i64 f = 0; f < live; f++) P->phase_ptr[f + 1] += P->phase_ptr[f];
-    std::vector<i32> fill(P->phase_ptr.begin(), P->phase_ptr.end() - 1);
-    // two records per task: {kind << 28 | chunk, phase, p0, p1}, {s1, rows below p1, pair0, pair1}
-    P->tasks.resize(2 * total);
-    auto put = [&](i64 f, i32 pi, i32 chunk, i32 kind, i32 r0, i32 r1) {
-        const i32 ph = remap[f];
-        const I4 pn = P->pan[pi];
-        const i64 at = 2 * (i64)fill[ph]++;
-        P->tasks[at] = I4{(kind << 28) | chunk, ph, pn.x, pn.y};
-        P->tasks[at + 1] = I4{(i32)s1_of(pn.z), pn.w, r0, r1};
+    struct T {
+        i64 cost;
+        i32 f, pi, chunk, kind, r0, r1;
     };
+    std::vector<T> all;
+    const i64 npush = (i64)P->push.size();
+    constexpr i64 kTaskCost = 4000;  // ~1 us of latency, in MACs
     for (i64 p = 0; p < np; p++) {
-        put(3 * fstage[p], (i32)p, 0, kSnDiag, 0, 0);
-        for (i64 c = 0; c < chunks(P->pan[p].w); c++) put(3 * fstage[p] + 1, (i32)p, (i32)c, kSnTrsm, 0, 0);
+        const I4 pn = P->pan[p];
+        const i64 w = pn.y - pn.x;
+        all.push_back({kTaskCost + w * w * w / 3, 2 * fstage[p] + 1, (i32)p, 0, kSnDiag, 0, 0});
+        for (i64 c = 0; c < chunks(pn.w); c++) {
+            const i64 rows = std::min<i64>(32, pn.w - 32 * c);
+            all.push_back({kTaskCost + w * w * w / 3 + rows * w * w / 2, 2 * fstage[p], (i32)p, (i32)c,
+                           kSnTrsm | kSnLocal, 0, 0});
+        }
     }
     for (i64 x = 0; x < npush; x++) {
         const I4 ps = P->push[x];
-        if (push_tri[x]) put(3 * push_stage[x] + 1, ps.x, 0, kSnTri, ps.y, ps.z);
-        for (i64 c = 0; c < chunks(P->pan[ps.x].w); c++)
-            put(3 * push_stage[x] + 2, ps.x, (i32)c, kSnRect, ps.y, ps.z);
+        const I4 pn = P->pan[ps.x];
+        const i64 w = pn.y - pn.x, np_ = ps.z - ps.y;
+        const bool local = push_stage[x] == fstage[ps.x];
+        if (push_tri[x])
+            all.push_back({kTaskCost + np_ * w * w / 2 + (local ? w * w * w / 3 : 0), 2 * push_stage[x], ps.x, 0,
+                           kSnTri | (local ? kSnLocal : 0), ps.y, ps.z});
+        for (i64 c = 0; c < chunks(pn.w); c++) {
+            const i64 rows = std::min<i64>(32, pn.w - 32 * c);
+            all.push_back({kTaskCost + rows * np_ * w, 2 * push_stage[x] + 1, ps.x, (i32)c, kSnRect, ps.y, ps.z});
+        }
+    }
+    std::stable_sort(all.begin(), all.end(), [](const T &a, const T &b) {
+        return a.f != b.f ? a.f < b.f : a.cost > b.cost;
+    });
+    if ((i64)all.size() >= (i64)INT32_MAX) {
+        set_error("supernodal plan: >= 2^31 tasks");
+        return GLU_EINVAL;
+    }
+    std::vector<i32> remap(nph, -1);
+    i64 live = 0;
+    for (const T &t : all)
+        if (remap[t.f] < 0) remap[t.f] = (i32)live++;
+    P->phase_ptr.assign(live + 1, 0);
+    for (const T &t : all) P->phase_ptr[remap[t.f] + 1]++;
+    for (i64 f = 0; f < live; f++) P->phase_ptr[f + 1] += P->phase_ptr[f];
+    // two records per task: {kind << 28 | chunk, phase, p0, p1}, {s1, rows below p1, pair0, pair1}
+    P->tasks.resize(2 * all.size());
+    for (size_t i = 0; i < all.size(); i++) {
+        const T &t = all[i];
+        const I4 pn = P->pan[t.pi];
+        P->tasks[2 * i] = I4{(t.kind << 27) | t.chunk, remap[t.f], pn.x, pn.y};
+        P->tasks[2 * i + 1] = I4{(i32)s1_of(pn.z), pn.w, t.r0, t.r1};
     }
     return GLU_OK;
 }

@@ -134,17 +134,14 @@ __device__ __forceinline__ void panel_cols(const SnParams &P, int p0, int w, int
 // check pass), divides it by the pivot and updates its later columns, so
 // every element receives its sources j in ascending order.
 template <int WM>
-__device__ void task_diag(const SnParams &P, int4 ta, int lane) {
-    const int p0 = ta.z, w = ta.w - ta.z;
-    int dcl, clol;
-    panel_cols(P, p0, w, lane, dcl, clol);
-    double x[WM];
+__device__ __forceinline__ void diag_factor(const SnParams &P, int p0, int w, int lane, int dcl, int clol,
+                                            double (&x)[WM], unsigned long long &mymax) {
 #pragma unroll
     for (int c = 0; c < WM; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
         x[c] = (c < w && lane < w && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
     }
-    unsigned long long mymax = 0;
+    mymax = 0;
     static_for<0, WM>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
         const bool below = lane > j && lane < w;
@@ -162,6 +159,16 @@ __device__ void task_diag(const SnParams &P, int4 ta, int lane) {
             x[c] = (below && ((has >> c) & 1u)) ? y : x[c];
         }
     });
+}
+
+template <int WM>
+__device__ void task_diag(const SnParams &P, int4 ta, int lane) {
+    const int p0 = ta.z, w = ta.w - ta.z;
+    int dcl, clol;
+    panel_cols(P, p0, w, lane, dcl, clol);
+    double x[WM];
+    unsigned long long mymax;
+    diag_factor<WM>(P, p0, w, lane, dcl, clol, x, mymax);
 #pragma unroll
     for (int c = 0; c < WM; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
@@ -175,18 +182,30 @@ __device__ void task_diag(const SnParams &P, int4 ta, int lane) {
 // updates the later columns with U(j, c) from the factored block (shared
 // memory, broadcast reads).
 template <int WM>
-__device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
-    const int chunk = ta.x & 0x0fffffff;
+__device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane, bool local) {
+    const int chunk = ta.x & 0x07ffffff;
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     int dcl, clol;
     panel_cols(P, p0, w, lane, dcl, clol);
     const int t = chunk * 32 + lane;
     const bool act = t < h;
+    if (local) {  // the panel's own stage: its diagonal block is factored here
+        double b[WM];
+        unsigned long long unused;
+        diag_factor<WM>(P, p0, w, lane, dcl, clol, b, unused);
+#pragma unroll
+        for (int c = 0; c < WM; c++) S.b[c][lane] = lane <= c ? b[c] : 0.0;
+    } else {
+#pragma unroll
+        for (int c = 0; c < WM; c++) {
+            const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
+            S.b[c][lane] = (c < w && lane <= c && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
+        }
+    }
     double x[WM];
 #pragma unroll
     for (int c = 0; c < WM; c++) {
-        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
-        S.b[c][lane] = (c < w && lane <= c && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
+        const int dc = __shfl_sync(0xffffffffu, dcl, c);
         x[c] = (act && c < w) ? ldv(P.v + dc + (p1 - p0 - c) + t) : 0.0;
     }
     __syncwarp();
@@ -216,21 +235,32 @@ __device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int 
 // TRI: U(P, k) for every target column k of the push (lane = column):
 // forward substitution with the panel's unit-lower block, j ascending.
 template <int WM>
-__device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
+__device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane, bool local) {
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, s1 = tb.x;
-    const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
+    int dcl, clol;
+    panel_cols(P, p0, w, lane, dcl, clol);
     const int q = tb.z + lane;
     int4 pr = make_int4(0, p1, 0, -1);
     if (q < tb.w) pr = __ldg(P.pairs + q);
     const bool act = pr.y < p1;
     const int lo = max(pr.y - p0, 0);
+    if (local) {  // the panel's own stage: its unit-lower block is factored here
+        double b[WM];
+        unsigned long long unused;
+        diag_factor<WM>(P, p0, w, lane, dcl, clol, b, unused);
+        // lane r holds row r: L(r, j) = b[j] for r > j; S.b[j][r] = L(r, j)
+#pragma unroll
+        for (int j = 0; j < WM; j++) S.b[j][lane] = lane > j ? b[j] : 0.0;
+    } else {
+#pragma unroll
+        for (int j = 0; j < WM; j++) {
+            const int dj = __shfl_sync(0xffffffffu, dcl, j);
+            S.b[j][lane] = (j < w && lane > j && lane < w) ? ldv(P.v + dj + (lane - j)) : 0.0;
+        }
+    }
     double u[WM];
 #pragma unroll
-    for (int j = 0; j < WM; j++) {
-        const int dj = __shfl_sync(0xffffffffu, dcl, j);
-        S.b[j][lane] = (j < w && lane > j && lane < w) ? ldv(P.v + dj + (lane - j)) : 0.0;
-        u[j] = (act && j < w && j >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + j))) : 0.0;
-    }
+    for (int j = 0; j < WM; j++) u[j] = (act && j < w && j >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + j))) : 0.0;
     __syncwarp();
     static_for<0, WM>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
@@ -258,7 +288,7 @@ constexpr int kRectB = 4;
 
 template <int WM>
 __device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
-    const int chunk = ta.x & 0x0fffffff;
+    const int chunk = ta.x & 0x07ffffff;
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     const int s1 = tb.x, in_sn = s1 - p1;
     const int t = chunk * 32 + lane;
@@ -323,7 +353,7 @@ struct RectSmem {
 static_assert(sizeof(RectSmem) <= sizeof(WarpSmem), "RectSmem overlays WarpSmem");
 
 __device__ void task_rect_tile(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int lane) {
-    const int chunk = ta.x & 0x0fffffff;
+    const int chunk = ta.x & 0x07ffffff;
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     const int s1 = tb.x, in_sn = s1 - p1;
     const int npair = tb.w - tb.z;
@@ -418,10 +448,11 @@ __device__ void task_rect_tile(const SnParams &P, RectSmem &R, int4 ta, int4 tb,
 // instruction cache, and most panels are one column wide).
 template <int WM>
 __device__ __forceinline__ void run_kind(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
-    switch (ta.x >> 28) {
+    const int code = ta.x >> 27;
+    switch (code & ~kSnLocal) {
         case kSnDiag: task_diag<WM>(P, ta, lane); break;
-        case kSnTrsm: task_trsm<WM>(P, S, ta, tb, lane); break;
-        case kSnTri: task_tri<WM>(P, S, ta, tb, lane); break;
+        case kSnTrsm: task_trsm<WM>(P, S, ta, tb, lane, code & kSnLocal); break;
+        case kSnTri: task_tri<WM>(P, S, ta, tb, lane, code & kSnLocal); break;
         default:
             if (WM > 8) task_rect_tile(P, *reinterpret_cast<RectSmem *>(&S), ta, tb, lane);
             else task_rect<WM>(P, ta, tb, lane);

@@ -78,6 +78,31 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
     col_a = plan["col_a"]
     tasks, pptr = plan["tasks"], plan["phase_ptr"]
 
+    def factor_block(E, p0, p1, clo, record):
+        """The w x w diagonal block factored from the phase-start values
+        (DIAG, or TRSM / TRI with the local flag)."""
+        w = p1 - p0
+        B = {}
+        for c in range(w):
+            dc = int(dp[p0 + c])
+            if record:
+                for q in range(int(cp[p0 + c]), dc - (c - clo[c])):
+                    mx(p0 + c, E.rd(q))
+            for r in range(clo[c], w):
+                B[c, r] = E.rd(dc + r - c)
+        for j in range(w):
+            if record:
+                for r in range(clo[j], w):
+                    mx(p0 + j, B[j, r])
+            piv = B[j, j]
+            for r in range(j + 1, w):
+                B[j, r] = B[j, r] / piv
+            for r in range(j + 1, w):
+                for c in range(j + 1, w):
+                    if j >= clo[c]:
+                        B[c, r] = B[c, r] - B[j, r] * B[c, j]
+        return B
+
     def mx(c, x):
         a = abs(x)
         if a == a and a > cmax[c]:
@@ -87,39 +112,27 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
         E = _Phase(v.copy())
         for ti in range(pptr[ph], pptr[ph + 1]):
             kc, tph, p0, p1, s1, h, r0, r1 = (int(x) for x in tasks[ti])
-            kind, chunk = kc >> 28, kc & ((1 << 28) - 1)
+            code, chunk = kc >> 27, kc & ((1 << 27) - 1)
+            kind, local = code >> 1, code & 1
             assert tph == ph
             E.task = ti
             if kind == 0:  # DIAG
                 w = p1 - p0
                 clo = [max(int(col_a[p0 + c]) - p0, 0) for c in range(w)]
-                B = {}
-                for c in range(w):
-                    dc = int(dp[p0 + c])
-                    for q in range(int(cp[p0 + c]), dc - (c - clo[c])):
-                        mx(p0 + c, E.rd(q))
-                    for r in range(clo[c], w):
-                        B[c, r] = E.rd(dc + r - c)
-                for j in range(w):
-                    for r in range(clo[j], w):
-                        mx(p0 + j, B[j, r])
-                    piv = B[j, j]
-                    for r in range(j + 1, w):
-                        B[j, r] = B[j, r] / piv
-                    for r in range(j + 1, w):
-                        for c in range(j + 1, w):
-                            if j >= clo[c]:
-                                B[c, r] = B[c, r] - B[j, r] * B[c, j]
+                B = factor_block(E, p0, p1, clo, True)
                 for c in range(w):
                     for r in range(clo[c], w):
                         E.wr(int(dp[p0 + c]) + r - c, B[c, r])
             elif kind == 1:  # TRSM
                 w = p1 - p0
                 clo = [max(int(col_a[p0 + c]) - p0, 0) for c in range(w)]
-                U = {}
-                for c in range(w):
-                    for r in range(clo[c], c + 1):
-                        U[c, r] = E.rd(int(dp[p0 + c]) + r - c)
+                if local:
+                    U = factor_block(E, p0, p1, clo, False)
+                else:
+                    U = {}
+                    for c in range(w):
+                        for r in range(clo[c], c + 1):
+                            U[c, r] = E.rd(int(dp[p0 + c]) + r - c)
                 for t in range(chunk * 32, min(h, chunk * 32 + 32)):
                     x = [E.rd(int(dp[p0 + c]) + (p1 - p0 - c) + t) for c in range(w)]
                     for j in range(w):
@@ -133,7 +146,12 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None):
                         E.wr(int(dp[p0 + c]) + (p1 - p0 - c) + t, x[c])
             elif kind == 2:  # TRI
                 w = p1 - p0
-                Lb = {(j, r): E.rd(int(dp[p0 + j]) + r - j) for j in range(w) for r in range(j + 1, w)}
+                if local:
+                    clo = [max(int(col_a[p0 + c]) - p0, 0) for c in range(w)]
+                    B = factor_block(E, p0, p1, clo, False)
+                    Lb = {(j, r): B[j, r] for j in range(w) for r in range(j + 1, w)}
+                else:
+                    Lb = {(j, r): E.rd(int(dp[p0 + j]) + r - j) for j in range(w) for r in range(j + 1, w)}
                 for q in range(r0, r1):
                     k, a, base, mp = (int(x) for x in pairs[q])
                     if a >= p1:

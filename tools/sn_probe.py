@@ -42,8 +42,8 @@ def phase_profile(fz, fp, a_d, v, st):
     fz.set_option(15, 0)
     dur = np.diff(buf).astype(np.float64) * 1e-3  # us
     tasks, pp = plan["tasks"], plan["phase_ptr"]
-    kinds = np.array([int(tasks[pp[p], 0]) >> 28 for p in range(nph)])
-    kinds = np.where(kinds == 2, 1, np.where(kinds == 3, 2, kinds))
+    kinds = np.array([int(tasks[pp[p], 0]) >> 28 for p in range(nph)])  # 0 trsm/tri/diag-ish, 1 rect
+    kinds = np.array([min(int(k), 1) + 1 for k in kinds])  # 1: phase led by TRSM/TRI, 2: RECT/DIAG
     ntask = np.diff(pp)
     out = {"total_us": float(dur.sum()), "phases": nph}
     for k, name in ((0, "diag"), (1, "trsm_tri"), (2, "rect")):
@@ -75,7 +75,7 @@ def phase_profile(fz, fp, a_d, v, st):
             "exec_max_us": exec_max * 1e-3, "flush_us": (buf[1:] - last_done) * 1e-3}
     for k, x in comp.items():
         out[k] = {"sum": float(x.sum()), "median": float(np.median(x)), "p90": float(np.percentile(x, 90))}
-    kinds_t = (tasks[:, 0] >> 28)
+    kinds_t = (tasks[:, 0] >> 28)  # (kind << 27) >> 28 = kind index
     for k, name in ((0, "diag"), (1, "trsm"), (2, "tri"), (3, "rect")):
         m = kinds_t == k
         if m.any():
