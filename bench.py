@@ -523,17 +523,17 @@ def run_ours(args):
                               "frac": macs / (main_ms * 1e-3) / fp64_macs_peak if main_ms else None,
                               "peak_source": f"derived: {info['sms']} SMs x 64 FP64 lanes x {sm_mhz:.0f} MHz "
                                              f"/ 2 instructions per MAC (DMUL + DADD, no FMA)"},
-            "latency_floor": ({"phases": fz.sn_info["phases"], "stages": fz.sn_info["stages"],
-                               "note": "every phase is a device-wide hand-off (~2.5 us measured: "
-                                       "flush 1.0-1.3 us + wake 1.3-1.5 us, tools/sn_probe.py)",
-                               "floor_ms": fz.sn_info["phases"] * 2.5e-3}
+            "latency_floor": ({"model_critical_path_ms": fz.sn_info["crit_ns"] * 1e-6,
+                               "note": "longest dependency chain of the dataflow plan under its latency "
+                                       "model (1 us per hand-off + per-task cost; glu_snode.cpp step 6): "
+                                       "the pushes into one target panel run one after another"}
                               if engine == "sn" else None),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_api": e2e_api,
             "batch": batch,
             "clocks": clk.summary(),
-            "gpu_launches": 4 * args.steps if engine == "sn" else
+            "gpu_launches": (4 + (1 if fz.sn_info["dblk"] > 0 else 0)) * args.steps if engine == "sn" else
             (3 + (1 if t0c < a.n else 0)) * args.steps,
         }
         if engine == "plan" and tail_ms:

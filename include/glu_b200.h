@@ -153,19 +153,25 @@ int64_t glu_plan_build_sn(int64_t n, const int64_t *col_ptr, const int64_t *row_
                           const int64_t *diag_pos, const int64_t *row_ptr, const int64_t *col_idx,
                           const int64_t *csc_pos, const int64_t *level_of, int32_t n_threads,
                           glu_plan **out);
-/* info[0..9] = supernodes, panels, (supernode, column) pairs, relative-map
-   entries, pushes, tasks, phases, stages, MACs, plan bytes (all 0 for a
-   per-MAC plan). */
+/* info[0..13] (16 words) = supernodes, panels, (supernode, column) pairs,
+   relative-map entries, pushes, tasks, diagonal-block scratch doubles,
+   critical path of the plan's latency model (ns), MACs, plan bytes, RG
+   tasks, RG slots, RG MAC indices, RG U indices (all 0 for a per-MAC
+   plan). */
 void glu_sn_plan_info(const glu_plan *p, int64_t *info);
 /* Copies a supernodal plan out (sizes from glu_sn_plan_info; int32 x4
    records): sn {s0, s1, |R_S|, first pair}, pan {p0, p1, supernode, rows
-   below}, pairs {k, a, base, map}, relmap, push {panel, pair0, pair1,
-   target panel}, tasks (2 records each) {kind << 27 | chunk, phase, p0, p1,
-   s1, rows below the panel, pair0, pair1}, phase_ptr[phases+1],
-   col_a[n].  Any pointer may be NULL. */
-void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *pairs,
-                        int32_t *relmap, int32_t *push, int32_t *tasks, int32_t *phase_ptr,
-                        int32_t *col_a);
+   below}, panm {RECT chunks into the panel, TRSM chunks, scratch offset or
+   -1, 0}, pairs {k, a, base, map}, relmap, push {panel, pair0, pair1,
+   target panel}, push_need[pushes], tasks (3 records each) {code << 27 |
+   chunk, source panel, p0, p1, s1, rows below the panel, pair0, pair1,
+   target panel, need, 0, 0}, col_a[n], rg {first slot, slots, first MAC
+   index, first U index}, rg_slot, rg_idx (u16), rg_uidx (u16).  Any
+   pointer may be NULL. */
+void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *panm, int32_t *pairs,
+                        int32_t *relmap, int32_t *push, int32_t *push_need, int32_t *tasks,
+                        int32_t *col_a, int32_t *rg, int32_t *rg_slot, uint16_t *rg_idx,
+                        uint16_t *rg_uidx);
 
 /* Checks a caller's level schedule for factor_parallel (numeric.py:241-351
    accepts any LevelSchedule) and refines it for contract B.  A source
@@ -201,13 +207,10 @@ int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value);
    which may differ from the one the plan was built on (contract A plans
    on the relaxed schedule). */
 int64_t glu_set_fail_levels(glu_handle *h, const int64_t *level_of);
-/* Diagnostics of the supernodal engine: after glu_set_option(h, 15, 1),
-   out[0] = kernel start and out[1 + p] = completion of phase p
-   (%globaltimer ns) of the last factorization.  Returns the words written
-   (0 for a per-MAC handle). */
-int64_t glu_sn_stamps(glu_handle *h, int64_t *out, int64_t max);
-/* glu_set_option(h, 15, 2) also records, per task, {iteration start, wait
-   done, executed, 0} (%globaltimer ns); read with glu_sn_trace. */
+/* Diagnostics of the supernodal engine: glu_set_option(h, 15, 1) records,
+   per task of the next factorization, {start, source ready, target ready,
+   done} (%globaltimer ns; 0 where a task has no such wait); read with
+   glu_sn_trace (returns the tasks written, 0 for a per-MAC handle). */
 int64_t glu_sn_trace(glu_handle *h, int64_t *out, int64_t max_tasks);
 /* Diagnostics: glu_set_option(h, 3, first_phase) and (h, 4, n_phases)
    record, for every item of those phases, 8 words {item | phase << 32,

@@ -50,10 +50,9 @@ SIGNATURES = {
     "glu_tail_capacity": (_i64, []),
     "glu_plan_build_sn": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _p, _i32, _pp]),
     "glu_sn_plan_info": (None, [_p, _p]),
-    "glu_sn_plan_export": (None, [_p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "glu_sn_plan_export": (None, [_p] * 14),
     "glu_schedule_refine": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _i32, _p, _p]),
     "glu_set_fail_levels": (_i64, [_p, _p]),
-    "glu_sn_stamps": (_i64, [_p, _p, _i64]),
     "glu_sn_trace": (_i64, [_p, _p, _i64]),
     "glu_plan_info": (None, [_p, _p]),
     "glu_trace_read": (_i64, [_p, _p, _i64]),

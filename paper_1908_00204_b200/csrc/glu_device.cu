@@ -2362,9 +2362,9 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
         case 10:  // tuning: dataflow-solve tasks per ticket grab (0 = static round-robin)
             h->solve_tblock = (int)std::max<int64_t>(0, std::min<int64_t>(value, 64));
             return GLU_OK;
-        case 15:  // diagnostics: supernodal engine per-phase completion stamps (glu_sn_stamps)
+        case 15:  // diagnostics: supernodal engine per-task timestamps (glu_sn_trace)
             if (!h->sn) { glu::set_error("option 15 needs a supernodal handle"); return GLU_EINVAL; }
-            return glu::sn_set_stamps(h->sn, (int)value);
+            return glu::sn_set_trace(h->sn, (int)value);
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
             return GLU_OK;
@@ -2372,11 +2372,6 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             glu::set_error("unknown option");
             return GLU_EINVAL;
     }
-}
-
-extern "C" int64_t glu_sn_stamps(glu_handle *h, int64_t *out, int64_t max) {
-    if (!h->sn) return 0;
-    return glu::sn_read_stamps(h->sn, out, max);
 }
 
 extern "C" int64_t glu_sn_trace(glu_handle *h, int64_t *out, int64_t max_tasks) {

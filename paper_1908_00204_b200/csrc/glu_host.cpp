@@ -1192,9 +1192,10 @@ extern "C" int64_t glu_plan_build_sn(int64_t n, const int64_t *col_ptr, const in
     return GLU_OK;
 }
 
-extern "C" void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *pairs,
-                                   int32_t *relmap, int32_t *push, int32_t *tasks, int32_t *phase_ptr,
-                                   int32_t *col_a) {
+extern "C" void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan, int32_t *panm,
+                                   int32_t *pairs, int32_t *relmap, int32_t *push, int32_t *push_need,
+                                   int32_t *tasks, int32_t *col_a, int32_t *rg, int32_t *rg_slot,
+                                   uint16_t *rg_idx, uint16_t *rg_uidx) {
     const glu::SnPlan *s = p->sn.get();
     if (!s) return;
     auto cp4 = [](const std::vector<glu::I4> &v, int32_t *dst) {
@@ -1203,12 +1204,15 @@ extern "C" void glu_sn_plan_export(const glu_plan *p, int32_t *sn, int32_t *pan,
     auto cp1 = [](const std::vector<int32_t> &v, int32_t *dst) {
         if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(int32_t));
     };
-    cp4(s->sn, sn); cp4(s->pan, pan); cp4(s->pairs, pairs); cp1(s->relmap, relmap);
-    cp4(s->push, push); cp4(s->tasks, tasks); cp1(s->phase_ptr, phase_ptr); cp1(s->col_a, col_a);
+    cp4(s->sn, sn); cp4(s->pan, pan); cp4(s->panm, panm); cp4(s->pairs, pairs); cp1(s->relmap, relmap);
+    cp4(s->push, push); cp1(s->push_need, push_need); cp4(s->tasks, tasks); cp1(s->col_a, col_a);
+    cp4(s->rg, rg); cp1(s->rg_slot, rg_slot);
+    if (rg_idx && !s->rg_idx.empty()) std::memcpy(rg_idx, s->rg_idx.data(), s->rg_idx.size() * sizeof(uint16_t));
+    if (rg_uidx && !s->rg_uidx.empty()) std::memcpy(rg_uidx, s->rg_uidx.data(), s->rg_uidx.size() * sizeof(uint16_t));
 }
 
 extern "C" void glu_sn_plan_info(const glu_plan *p, int64_t *info) {
-    std::memset(info, 0, sizeof(int64_t) * 12);
+    std::memset(info, 0, sizeof(int64_t) * 16);
     const glu::SnPlan *s = p->sn.get();
     if (!s) return;
     info[0] = (i64)s->sn.size();
@@ -1216,13 +1220,19 @@ extern "C" void glu_sn_plan_info(const glu_plan *p, int64_t *info) {
     info[2] = (i64)s->pairs.size();
     info[3] = (i64)s->relmap.size();
     info[4] = (i64)s->push.size();
-    info[5] = (i64)s->tasks.size() / 2;
-    info[6] = (i64)s->phase_ptr.size() - 1;
-    info[7] = s->n_stages;
+    info[5] = (i64)s->tasks.size() / 3;
+    info[6] = s->n_dblk;
+    info[7] = s->crit_ns;
     info[8] = s->macs;
-    info[9] = (i64)((s->sn.size() + s->pan.size() + s->pairs.size() + s->push.size() + s->tasks.size()) *
-                        sizeof(glu::I4) +
-                    (s->relmap.size() + s->phase_ptr.size()) * sizeof(int32_t));
+    info[9] = (i64)((s->sn.size() + s->pan.size() + s->panm.size() + s->pairs.size() + s->push.size() +
+                     s->tasks.size() + s->rg.size()) * sizeof(glu::I4) +
+                    (s->relmap.size() + s->push_need.size() + s->col_a.size() + s->rg_slot.size()) *
+                        sizeof(int32_t) +
+                    (s->rg_idx.size() + s->rg_uidx.size()) * sizeof(uint16_t));
+    info[10] = (i64)s->rg.size();
+    info[11] = (i64)s->rg_slot.size();
+    info[12] = (i64)s->rg_idx.size();
+    info[13] = (i64)s->rg_uidx.size();
 }
 
 namespace glu {

@@ -71,31 +71,52 @@ static_assert(sizeof(DeepRef) == 16, "DeepRef layout");
 // cut into panels of <= kSnW columns.  Index records are 16-byte vectors.
 // ---------------------------------------------------------------------------
 constexpr int kSnW = 16;  // panel width: one warp lane per panel column / row
+// RG tasks stage their target slots, the pushes' L rows and their MAC
+// indices in a warp's shared memory
+constexpr int kRgPushes = 16;   // pushes per RG task
+constexpr int kRgSlots = 512;   // distinct slots (targets and multipliers U(p0, k))
+constexpr int kRgIdx = 2048;    // MAC indices (u16)
 
 struct alignas(16) I4 {
     int32_t x, y, z, w;
 };
 
-// task kind = record.x >> 27: the kind in bits 1-2, kSnLocal in bit 0
+// task code = record.x >> 27 = kind << 2 | flags
 enum SnTaskKind : int32_t {
-    kSnDiag = 0 << 1,  // factor a panel's w x w diagonal block and write it back
-    kSnTrsm = 1 << 1,  // 32 rows below a panel: divide, in-panel updates
-    kSnTri = 2 << 1,   // U(P, K): forward substitution inside a push's source panel
-    kSnRect = 3 << 1,  // 32 rows below the source panel into every column of a push
-    kSnLocal = 1,      // TRSM / TRI: factor the (not yet written back) diagonal block locally
+    kSnTrsm = 0,  // rows below a panel: factor its diagonal block locally, divide, in-panel updates
+    kSnRect = 1,  // push rows below the source panel into every column of the target panel
+    kSnUw = 2,    // write the solved U(P, K) of a push whose RECT chunks all read it
+    kSnRg = 3,    // a run of one-chunk pushes from one-column panels into one target panel
+};
+enum SnTaskFlags : int32_t {
+    kSnTriF = 1,    // RECT: forward substitution of U(P, K) inside the source block first
+    kSnWriteU = 2,  // RECT: the only reader of U(P, K) -- it writes the solved values
 };
 
 struct SnPlan {
     int64_t n = 0, nnz = 0;
     std::vector<I4> sn;      // {s0, s1, |R_S|, first pair}
     std::vector<I4> pan;     // {p0, p1, supernode, rows below the panel}
+    std::vector<I4> panm;    // per panel {pushes' RECT chunks into it, TRSM chunks, scratch offset | -1, 0}
     std::vector<I4> pairs;   // per (supernode S, target column k): {k, a, base, map}
     std::vector<int32_t> relmap;  // positions of R_S's rows in column k (absolute slots)
-    std::vector<I4> push;    // {source panel, first pair, end pair, target panel}
-    std::vector<I4> tasks;   // 2 per task, phase order: {kind << 27 | chunk, phase, p0, p1}, {s1, h, pair0, pair1}
-    std::vector<int32_t> phase_ptr;  // tasks of phase p: [phase_ptr[p], phase_ptr[p+1])
+    std::vector<I4> push;    // {source panel, first pair, end pair, target panel}, target-major
+    std::vector<int32_t> push_need;  // per push: RECT chunks of earlier pushes into its target
+    // 3 records per task, in a topological (as-soon-as-possible) order:
+    //   {code << 27 | chunk, source panel P, p0, p1}, {s1, rows below p1, pair0, pair1},
+    //   {target panel K, need, 0, 0}; RG: {code << 27 | pushes, first MAC index, first U index, 0},
+    //   {first slot, slots, first push, pushes}, {K, need, 0, 0}
+    std::vector<I4> tasks;
     std::vector<int32_t> col_a;      // per column c: first row of c's supernode present in c
-    int64_t n_stages = 0;
+    // RG tasks: per RG {first slot, slots, first MAC index, first U index}; the
+    // slots it stages in shared memory (targets and multipliers); per MAC
+    // (push, pair q, row t at q * h + t) the index of its target in that
+    // list; per (push, pair) the index of U(p0, k)
+    std::vector<I4> rg;
+    std::vector<int32_t> rg_slot;
+    std::vector<uint16_t> rg_idx, rg_uidx;
+    int64_t n_dblk = 0;              // doubles of factored-diagonal-block scratch (panels w >= 2)
+    int64_t crit_ns = 0;             // critical path of the plan's latency model
     int64_t macs = 0;
 };
 
@@ -134,9 +155,8 @@ struct SnDev;
 int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
 void sn_free(SnDev *d);
 int sn_grid(int sm_count);
-int64_t sn_set_stamps(SnDev *d, int mode);
+int64_t sn_set_trace(SnDev *d, int mode);
 int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks);
-int64_t sn_read_stamps(SnDev *d, int64_t *out, int64_t max);
 // one factorization of v (A_s values after the scatter); pivot failures
 // are min-reduced into *fail as (fail_level << 32 | column) or column
 int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *diag_pos,

@@ -22,19 +22,20 @@
 // push into column k), and orders them per target in ascending j (contract
 // A, the left-looking order, _kernels.py:37-76):
 //
-//   * pushes into a target panel K are applied in ascending source panel,
-//     one per stage (stage(P,K) = max(stage(P factored), previous push + 1));
+//   * pushes into a target panel K are applied one after another in
+//     ascending source panel (a counter per target panel), and panel K is
+//     factored after its last push;
 //   * inside a push, every target receives the panel's columns in ascending
-//     order (the kernel's chains), and panel K is factored in the stage after
-//     its last push.
+//     order (the kernel's chains).
 //
-// Each stage has two phases (the kernel's only synchronisation):
-//   0  TRSM(P,c)  rows below the panel, 32 at a time: divide and in-panel
-//                 updates (factoring the w x w diagonal block locally)
-//      TRI(push)  U(P, K) = forward substitution inside the source panel
-//   1  RECT(push,c) rows below P, 32 at a time, into every column of K
-//      DIAG(P)    the factored diagonal block written back
-// Empty phases are dropped.
+// The kernel is a dataflow walk over three task kinds (no phases, no grid
+// barrier; step 6 below has the counters):
+//   TRSM(P,c)   32 rows below panel P: factor the w x w diagonal block
+//               locally, divide, in-panel updates (chunk 0 also stores the
+//               factored block in a scratch area, written back at the end)
+//   RECT(x,c)   push x = (P, K), 32 rows below P into every column of K,
+//               after the forward substitution U(P, K) inside P's block
+//   UW(x)       writes the solved U(P, K) when several RECT chunks read it
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -219,8 +220,9 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         const i64 S = pan_sn[p];
         P->pan[p] = I4{(i32)pan0[p], (i32)pan0[p + 1], (i32)S, (i32)((s1_of(S) - pan0[p + 1]) + nR[S])};
     }
-    std::vector<i32> fstage(np, 0), seen(np, -1), push_stage;
+    std::vector<i32> seen(np, -1);
     std::vector<char> push_tri;
+    std::vector<i64> push_macs;
     std::vector<i32> srcs;
     i64 macs = 0;
     for (i64 K = 0; K < np; K++) {
@@ -238,7 +240,6 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
             }
         }
         std::sort(srcs.begin(), srcs.end());
-        i64 last = -1;
         for (i32 p : srcs) {
             const I4 pn = P->pan[p];
             const i64 S = pn.z, s1 = s1_of(S);
@@ -257,14 +258,12 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
             }
             if (pm == 0) continue;
             macs += pm;
-            last = std::max<i64>(fstage[p], last + 1);
             P->push.push_back(I4{p, (i32)r0, (i32)r1, (i32)K});
-            push_stage.push_back((i32)last);
             push_tri.push_back(tri > 0);
+            push_macs.push_back(pm);
         }
-        fstage[K] = (i32)(last + 1);
     }
-    // in-panel MACs (DIAG + TRSM): every source j of a column c inside its panel
+    // in-panel MACs (TRSM's diagonal-block factorization and row updates)
     for (i64 p = 0; p < np; p++) {
         const I4 pn = P->pan[p];
         const i64 S = pn.z, s1 = s1_of(S);
@@ -278,73 +277,222 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
     }
     P->macs = macs;
 
-    // 6. tasks in phase order: two phases per stage, empty phases dropped.
-    //   phase 2s     TRSM(P) of the panels factored in stage s and TRI of the
-    //                stage's pushes; both factor P's w x w diagonal block
-    //                themselves when it is not yet factored (kSnLocal: the
-    //                panel's own stage), from values no task of the phase writes
-    //   phase 2s + 1 RECT of the stage's pushes, and DIAG(P), which writes
-    //                the factored block back (nothing in this phase reads it)
-    // Inside a phase tasks are ordered by estimated cost, largest first, so
-    // the static round-robin deal gives every warp a similar load.
-    i64 n_stages = 0;
-    for (i64 p = 0; p < np; p++) n_stages = std::max<i64>(n_stages, fstage[p] + 1);
-    for (i32 s : push_stage) n_stages = std::max<i64>(n_stages, s + 1);
-    P->n_stages = n_stages;
-    const i64 nph = 2 * n_stages;
-    auto chunks = [](i64 h) { return (h + 31) / 32; };
-    struct T {
-        i64 cost;
-        i32 f, pi, chunk, kind, r0, r1;
-    };
-    std::vector<T> all;
+    // 6. dataflow tasks.  Per panel P: nch = max(1, ceil(rows below / 32))
+    // TRSM chunks; per push x = (P, K): nch(P) RECT chunks (rows below P,
+    // 32 each; the forward substitution for U(P, K) folded in) and, when
+    // U(P, K) changes and several chunks read it, one U-writer.  Counters:
+    //   in[K]  RECT chunks of pushes into K done; push x waits for
+    //          in[K] >= need(x) (every earlier push into K), TRSM(K) for
+    //          in[K] >= total_in(K)
+    //   f[P]   TRSM chunks of P done; RECT(x) waits for f[P] >= nch(P)
+    //   U-writer of x waits for in[K] >= need(x) + nch(P)
+    // A run of consecutive one-chunk pushes from one-column panels into K
+    // (most pushes of a nested-dissection order: the small separators'
+    // columns) is one RG task instead: a warp applies them in order, waiting
+    // for each source panel's TRSM as it goes, and counts them all at the
+    // end -- the chain of pushes into K then costs an L2 round trip per push
+    // instead of a cross-SM hand-off.
+    // Tasks are ordered by their start in an as-soon-as-possible schedule
+    // under a latency model (hop + per-task cost); every dependency starts
+    // strictly earlier, so the order is topological and the kernel's static
+    // deal (each warp walks its tasks in order) cannot deadlock.
     const i64 npush = (i64)P->push.size();
-    constexpr i64 kTaskCost = 4000;  // ~1 us of latency, in MACs
+    auto chunks = [](i64 h) { return std::max<i64>(1, (h + 31) / 32); };
+    P->panm.assign(np, I4{0, 0, -1, 0});
+    i64 dbl = 0;
     for (i64 p = 0; p < np; p++) {
         const I4 pn = P->pan[p];
         const i64 w = pn.y - pn.x;
-        all.push_back({kTaskCost + w * w * w / 3, 2 * fstage[p] + 1, (i32)p, 0, kSnDiag, 0, 0});
-        for (i64 c = 0; c < chunks(pn.w); c++) {
-            const i64 rows = std::min<i64>(32, pn.w - 32 * c);
-            all.push_back({kTaskCost + w * w * w / 3 + rows * w * w / 2, 2 * fstage[p], (i32)p, (i32)c,
-                           kSnTrsm | kSnLocal, 0, 0});
+        P->panm[p].y = (i32)chunks(pn.w);
+        if (w >= 2) {
+            P->panm[p].z = (i32)dbl;
+            dbl += w * w;
         }
     }
-    for (i64 x = 0; x < npush; x++) {
-        const I4 ps = P->push[x];
-        const I4 pn = P->pan[ps.x];
-        const i64 w = pn.y - pn.x, np_ = ps.z - ps.y;
-        const bool local = push_stage[x] == fstage[ps.x];
-        if (push_tri[x])
-            all.push_back({kTaskCost + np_ * w * w / 2 + (local ? w * w * w / 3 : 0), 2 * push_stage[x], ps.x, 0,
-                           kSnTri | (local ? kSnLocal : 0), ps.y, ps.z});
-        for (i64 c = 0; c < chunks(pn.w); c++) {
-            const i64 rows = std::min<i64>(32, pn.w - 32 * c);
-            all.push_back({kTaskCost + rows * np_ * w, 2 * push_stage[x] + 1, ps.x, (i32)c, kSnRect, ps.y, ps.z});
+    if (dbl >= (i64)INT32_MAX) {
+        set_error("supernodal plan: diagonal-block scratch >= 2^31 doubles");
+        return GLU_EINVAL;
+    }
+    P->n_dblk = dbl;
+    constexpr double kHop = 1.0;                 // us: release -> observe
+    constexpr double kMacsPerUs = 4000.0;        // one warp's FP64 chain rate
+    constexpr double kGatherSrcUs = 0.3;         // one push inside an RG (shared-memory chains)
+    constexpr i64 kMaxGather = kRgPushes;        // pushes per RG task (one per lane)
+    constexpr i64 kMinGather = 3;                // shorter runs stay RECT tasks (their slots load before the waits)
+    std::vector<double> f_done(np, 0.0), f_start(np, 0.0);
+    struct T {
+        double start, cost;
+        i32 kind, pi, chunk, x;
+    };
+    std::vector<T> all;
+    all.reserve((size_t)(np + 2 * npush));
+    double crit = 0.0;
+    // RG slot bookkeeping: the slots an RG touches all lie in its target
+    // panel's columns; mark[slot - col_ptr[k0]] = (generation, index in T)
+    i64 max_span = 0;
+    for (i64 K = 0; K < np; K++) max_span = std::max<i64>(max_span, col_ptr[pan0[K + 1]] - col_ptr[pan0[K]]);
+    std::vector<i32> mark_gen((size_t)max_span, -1), mark_idx((size_t)max_span, 0);
+    i32 gen = -1;
+    std::vector<i32> cur_slots;
+    i64 x = 0;
+    for (i64 K = 0; K < np; K++) {
+        double t = 0.0;
+        i64 need = 0;
+        const i64 kbase = col_ptr[pan0[K]];
+        // RG: a run of consecutive one-chunk pushes from one-column panels
+        // into K, applied by one warp in order (no hand-off between them)
+        i64 g_first = -1, g_cnt = 0;
+        double g_key = 0.0, g_cost = 0.0, g_t0 = 0.0;
+        size_t g_idx0 = 0, g_uidx0 = 0;
+        auto slot_of = [&](const I4 &pr, i64 tr) -> i64 {  // row tr below a one-column source, pair pr
+            return pr.w >= 0 ? (i64)P->relmap[pr.w + tr] : (i64)pr.z + tr;
+        };
+        auto close_g = [&]() {
+            if (g_cnt >= kMinGather) {
+                const i32 r = (i32)P->rg.size();
+                P->rg.push_back(I4{(i32)P->rg_slot.size(), (i32)cur_slots.size(), (i32)g_idx0, (i32)g_uidx0});
+                P->rg_slot.insert(P->rg_slot.end(), cur_slots.begin(), cur_slots.end());
+                all.push_back({g_key, g_cost, kSnRg << 2, r, (i32)g_cnt, (i32)g_first});
+            } else if (g_cnt > 0) {
+                // too short: one RECT task per push, chained as usual
+                P->rg_idx.resize(g_idx0);
+                P->rg_uidx.resize(g_uidx0);
+                double tt = g_t0;
+                for (i64 y = g_first; y < g_first + g_cnt; y++) {
+                    const i32 src = P->push[y].x;
+                    const double st = std::max(tt, f_done[src]) + kHop;
+                    const double per = 1.5 + (double)push_macs[y] / kMacsPerUs;
+                    all.push_back({st, per, kSnRect << 2, src, 0, (i32)y});
+                    tt = st + per;
+                }
+                t = std::max(t, tt);
+            }
+            g_cnt = 0;
+        };
+        for (; x < npush && P->push[x].w == (i32)K; x++) {
+            const I4 ps = P->push[x];
+            const I4 pn = P->pan[ps.x];
+            const i64 w = pn.y - pn.x, npair = ps.z - ps.y, nc = chunks(pn.w);
+            P->push_need.push_back((i32)need);
+            if (w == 1 && nc == 1) {
+                const double ready = f_done[ps.x];
+                const i64 h = pn.w;
+                // new distinct slots (targets and U(p0, k)) this push would add to the
+                // open RG, and its MAC indices (pair q, row tr at q * h + tr)
+                i64 fresh = 0;
+                if (g_cnt > 0)
+                    for (i64 q = ps.y; q < ps.z; q++) {
+                        const I4 pr = P->pairs[q];
+                        if (pr.y >= pn.y) continue;
+                        if (mark_gen[(i64)pr.z - 1 - kbase] != gen) fresh++;
+                        for (i64 tr = 0; tr < h; tr++)
+                            if (mark_gen[slot_of(pr, tr) - kbase] != gen) fresh++;
+                    }
+                if (!(g_cnt > 0 && g_cnt < kMaxGather && ready <= t + kHop &&
+                      (i64)cur_slots.size() + fresh <= kRgSlots &&
+                      (i64)(P->rg_idx.size() - g_idx0) + npair * h <= kRgIdx &&
+                      (i64)(P->rg_uidx.size() - g_uidx0) + npair <= kRgPushes * kSnW)) {
+                    close_g();
+                    g_first = x;
+                    g_t0 = t;
+                    t = std::max(t, ready) + kHop;
+                    g_key = t;
+                    g_cost = 0.0;
+                    gen++;
+                    cur_slots.clear();
+                    g_idx0 = P->rg_idx.size();
+                    g_uidx0 = P->rg_uidx.size();
+                }
+                // the push's MACs as indices into the RG's slot list (pair q, row tr
+                // at q * h + tr), and per pair the index of U(p0, k)
+                auto index_of = [&](i64 slot) -> uint16_t {
+                    const i64 sl = slot - kbase;
+                    if (mark_gen[sl] != gen) {
+                        mark_gen[sl] = gen;
+                        mark_idx[sl] = (i32)cur_slots.size();
+                        cur_slots.push_back((i32)slot);
+                    }
+                    return (uint16_t)mark_idx[sl];
+                };
+                for (i64 q = ps.y; q < ps.z; q++) {
+                    const I4 pr = P->pairs[q];
+                    const bool ok = pr.y < pn.y;
+                    P->rg_uidx.push_back(ok ? index_of((i64)pr.z - 1) : (uint16_t)0);
+                    for (i64 tr = 0; tr < h; tr++) P->rg_idx.push_back(ok ? index_of(slot_of(pr, tr)) : (uint16_t)0);
+                }
+                // after its sources' TRSM tasks in the list (topological order)
+                g_key = std::max(g_key, f_start[ps.x] + 1e-3);
+                t = std::max(t, ready) + kGatherSrcUs;
+                g_cost += kGatherSrcUs;
+                g_cnt++;
+                need += 1;
+                continue;
+            }
+            close_g();
+            const double st = std::max(t, f_done[ps.x]) + kHop;
+            const double per = 1.5 + (double)push_macs[x] / (double)nc / kMacsPerUs +
+                               (push_tri[x] ? 0.05 * (double)(w * w) : 0.0);
+            const bool uw = push_tri[x] && nc > 1;
+            const i32 flags = (push_tri[x] ? kSnTriF : 0) | (push_tri[x] && !uw ? kSnWriteU : 0);
+            for (i64 c = 0; c < nc; c++) all.push_back({st, per, (kSnRect << 2) | flags, (i32)ps.x, (i32)c, (i32)x});
+            t = st + per;
+            if (uw) all.push_back({t + kHop, 1.0 + 0.05 * (double)(w * w * npair) / 16.0, kSnUw << 2,
+                                   (i32)ps.x, 0, (i32)x});
+            need += nc;
         }
+        close_g();
+        P->panm[K].x = (i32)need;
+        const I4 pn = P->pan[K];
+        const i64 w = pn.y - pn.x, nc = chunks(pn.w);
+        const double st = (need > 0 ? t + kHop : 0.0);
+        const double cost = 2.0 + 0.15 * (double)w + (double)(32 * w * w / 2) / kMacsPerUs;
+        for (i64 c = 0; c < nc; c++) all.push_back({st, cost, kSnTrsm << 2, (i32)K, (i32)c, -1});
+        f_start[K] = st;
+        f_done[K] = st + cost;
+        crit = std::max(crit, f_done[K]);
+    }
+    if ((i64)P->rg_idx.size() >= (i64)INT32_MAX || (i64)P->rg_slot.size() >= (i64)INT32_MAX) {
+        set_error("supernodal plan: RG index arrays >= 2^31 entries");
+        return GLU_EINVAL;
     }
     std::stable_sort(all.begin(), all.end(), [](const T &a, const T &b) {
-        return a.f != b.f ? a.f < b.f : a.cost > b.cost;
+        return a.start != b.start ? a.start < b.start : a.cost > b.cost;
     });
     if ((i64)all.size() >= (i64)INT32_MAX) {
         set_error("supernodal plan: >= 2^31 tasks");
         return GLU_EINVAL;
     }
-    std::vector<i32> remap(nph, -1);
-    i64 live = 0;
-    for (const T &t : all)
-        if (remap[t.f] < 0) remap[t.f] = (i32)live++;
-    P->phase_ptr.assign(live + 1, 0);
-    for (const T &t : all) P->phase_ptr[remap[t.f] + 1]++;
-    for (i64 f = 0; f < live; f++) P->phase_ptr[f + 1] += P->phase_ptr[f];
-    // two records per task: {kind << 28 | chunk, phase, p0, p1}, {s1, rows below p1, pair0, pair1}
-    P->tasks.resize(2 * all.size());
-    for (size_t i = 0; i < all.size(); i++) {
-        const T &t = all[i];
-        const I4 pn = P->pan[t.pi];
-        P->tasks[2 * i] = I4{(t.kind << 27) | t.chunk, remap[t.f], pn.x, pn.y};
-        P->tasks[2 * i + 1] = I4{(i32)s1_of(pn.z), pn.w, t.r0, t.r1};
-    }
+    P->crit_ns = (i64)(crit * 1e3);
+    // three records per task (glu_internal.h SnPlan::tasks)
+    P->tasks.resize(3 * all.size());
+    parallel_for((i64)all.size(), nt, 1 << 16, [&](int, i64 b, i64 e) {
+        for (i64 i = b; i < e; i++) {
+            const T &t = all[i];
+            if (t.kind == (kSnRg << 2)) {
+                // {code << 27 | pushes, first MAC index, first U index, 0}, {first slot, slots,
+                // first push, pushes}, {K, need, 0, 0}
+                const I4 g = P->rg[t.pi];
+                const I4 ps = P->push[t.x];
+                P->tasks[3 * i] = I4{(t.kind << 27) | t.chunk, g.z, g.w, 0};
+                P->tasks[3 * i + 1] = I4{g.x, g.y, t.x, t.chunk};
+                P->tasks[3 * i + 2] = I4{ps.w, P->push_need[t.x], 0, 0};
+                continue;
+            }
+            const I4 pn = P->pan[t.pi];
+            I4 c{0, 0, 0, 0};
+            i32 pr0 = 0, pr1 = 0;
+            if (t.x >= 0) {
+                const I4 ps = P->push[t.x];
+                pr0 = ps.y;
+                pr1 = ps.z;
+                c = I4{ps.w, P->push_need[t.x], 0, 0};
+            }
+
+            P->tasks[3 * i] = I4{(t.kind << 27) | t.chunk, t.pi, pn.x, pn.y};
+            P->tasks[3 * i + 1] = I4{(i32)s1_of(pn.z), pn.w, pr0, pr1};
+            P->tasks[3 * i + 2] = c;
+        }
+    });
     return GLU_OK;
 }
 

@@ -1,21 +1,34 @@
-// glu_snode.cu -- supernodal engine: one persistent kernel over the phase-
-// ordered warp tasks of glu_snode.cpp, then a pivot-check pass.
+// glu_snode.cu -- supernodal engine: one persistent dataflow kernel over the
+// warp tasks of glu_snode.cpp, a write-back of the factored diagonal blocks,
+// then a pivot-check pass.
 //
 // Every task is one warp.  Warps walk the task list with a static stride
 // (task i -> CTA i % grid, warp (i / grid) % 8, so consecutive tasks land on
-// different SMs); a warp entering phase p waits until every task of phase
-// p-1 has been counted, and counts its own tasks of a phase with one fence +
-// one atomic when it leaves that phase.  Tasks of a phase only wait on
-// smaller task indices, each warp runs its tasks in index order and all CTAs
-// are co-resident (cooperative launch), so the walk cannot deadlock.
+// different SMs) and run their tasks in list order.  There is no phase and
+// no grid barrier: a task waits only for the counters of what it reads
+// (glu_snode.cpp step 6) --
+//   TRSM(P)   in[P] == every RECT chunk of every push into P
+//   RECT(x)   f[P] == every TRSM chunk of its source panel, then
+//             in[K] == every RECT chunk of the earlier pushes into K
+//   UW(x)     in[K] == the RECT chunks of x as well
+// -- and counts itself with one fence + one atomic when done.  Every
+// dependency has a smaller task index, each warp runs its tasks in index
+// order and all CTAs are co-resident (cooperative launch), so the walk
+// cannot deadlock: the smallest unfinished task can always run.
+//
+// A RECT task loads everything that is final once its source panel is
+// factored (its L rows, the factored diagonal block, the target positions)
+// BEFORE it waits for its target panel, so the chain of pushes into one
+// target panel -- the engine's critical path -- carries only the target
+// loads, the FP64 chains and the release.
 //
 // Arithmetic is the reference's, bit for bit (levlu/_kernels.py:37-76,
 // contract A): every MAC is __dsub_rn(t, __dmul_rn(Ldiv, U)) with the
 // divided L value and the final U value, every divide __ddiv_rn, and every
-// target receives its sources in ascending column order (panels in
-// ascending order across stages, panel columns in ascending order inside a
-// task's chain).  The pivot test |piv| <= thresh * max|column| runs after
-// the factorization from per-column maxima gathered on the way (the
+// target receives its sources in ascending column order (pushes into a
+// target panel in ascending source panel, panel columns in ascending order
+// inside a task's chain).  The pivot test |piv| <= thresh * max|column| runs
+// after the factorization from per-column maxima gathered on the way (the
 // undivided L values, the final U values), so a failing column is found
 // exactly as the reference finds it; the columns after it are garbage, as
 // the reference never computes them.
@@ -39,23 +52,22 @@ namespace {
 
 constexpr int kSnThreads = 256;
 constexpr int kSnWarps = kSnThreads / 32;
-constexpr int kDoneStride = 8;  // u32 words between phase counters
-constexpr int kGdoneRep = 8;    // replicas of the phases-complete counter (spread the pollers)
-constexpr int kLine = 32;       // u32 words per 128-byte line
 constexpr unsigned long long kSnWatchdogNs = 4000000000ull;
 
 struct SnParams {
     double *v;
-    const i32 *col_ptr, *diag_pos, *col_a, *fail_level;
-    const int4 *pairs, *tasks;  // tasks: 2 records each (glu_internal.h SnPlan::tasks)
-    const i32 *relmap, *phase_ptr;
+    double *dblk;  // factored diagonal blocks of panels with w >= 2, column-major w x w
+    const i32 *diag_pos, *col_a;
+    const int4 *pairs, *tasks, *panm;  // tasks: 3 records each (glu_internal.h SnPlan::tasks)
+    const int4 *push, *pan;            // RG tasks: push {panel, pair0, pair1, K}, panel {p0, p1, S, h}
+    const i32 *rg_slot;
+    const uint16_t *rg_idx, *rg_uidx;
+    const i32 *relmap;
     i32 n_tasks;
-    unsigned *done;   // per phase: counted tasks (kDoneStride apart)
-    unsigned *gdone;  // phases complete, kGdoneRep replicas kLine apart
+    unsigned *cnt;  // per panel P: [2P] RECT chunks into P done, [2P + 1] TRSM chunks of P done
     unsigned long long *cmax;
     int *err;
-    unsigned long long *stamps;  // optional: [0] kernel start, [1 + p] completion of phase p
-    unsigned long long *trace;   // optional: per task {iteration start, wait done, executed, 0}
+    unsigned long long *trace;  // optional: per task {start, source ready, target ready, done}
 };
 
 __device__ __forceinline__ double ldv(const double *p) { return __ldcg(p); }
@@ -85,30 +97,78 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
-constexpr int kB = 32;  // lanes: shared-memory block dimension
-struct WarpSmem {
-    double b[kB][kB + 1];  // panel block, column-major [column][row]
-    int clo[kB];           // per panel column: first panel row present
-    double pad[16 * kB - kB + 8];  // RectSmem (task_rect_tile) overlays this region
-};
+// Wait until *c >= need: lane 0 polls with relaxed loads (an acquire load
+// invalidates the SM's L1 each time), backing off, then one acquire load
+// once the count is reached; the warp barrier orders every lane's later
+// loads after it.  False on the watchdog / error path.
+__device__ __forceinline__ bool wait_ge(const SnParams &P, const unsigned *c, unsigned need, int lane) {
+    int ok = 1;
+    if (lane == 0 && need > 0 && ld_acquire(c) < need) {
+        const unsigned long long t0 = globaltimer();
+        unsigned ns = 16;
+        while (ld_relaxed(c) < need || ld_acquire(c) < need) {
+            if (*(volatile int *)P.err) { ok = 0; break; }
+            if (globaltimer() - t0 > kSnWatchdogNs) {
+                atomicExch(P.err, 1);
+                ok = 0;
+                break;
+            }
+            __nanosleep(ns);
+            ns = ns < 128 ? 2 * ns : ns;
+        }
+    }
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
 
-// Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E).  The
-// FP64 chains below index register arrays with the loop counter, which
-// must be a constant after unrolling (a nest of #pragma unroll loops whose
-// body holds the division's slow-path call is left rolled by nvcc, and the
-// arrays then live in local memory).
-template <int B, int E, class F>
-__device__ __forceinline__ void static_for(F &&f) {
-    if constexpr (B < E) {
-        f(std::integral_constant<int, B>{});
-        static_for<B + 1, E>(f);
+// Count a finished task: every lane's stores, then (lane 0) a device-scope
+// fence and the counter increment.
+__device__ __forceinline__ void release(unsigned *c, int lane) {
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        atomicAdd(c, 1u);
     }
 }
 
+constexpr int kB = 32;  // lanes: shared-memory tile dimension
+
+// Per-warp shared memory.  The task code is kept compact on purpose --
+// runtime loops over shared-memory tiles instead of fully unrolled register
+// chains per panel width: the warps of an SM run different task kinds and
+// widths side by side, and a kernel much larger than the 32 KB L1.5
+// instruction cache stalls them on instruction fetch (a fully unrolled
+// 16-wide TRSM alone is ~40 KB of SASS).
+struct TrsmSmem {
+    double b[kSnW][kB + 1];  // the diagonal block, column-major [column][row]
+    double x[kSnW][kB];      // the chunk's rows below the panel, [column][row = lane]
+};
+struct RectSmem {
+    double l[kSnW][kB];     // [j][row]: divided L rows below the source panel
+    double u[kSnW][kSnW];   // [j][target column]: U(P, K)
+    double lb[kSnW][kSnW];  // [j][r]: L(r, j) of the factored diagonal block
+    int lo[kSnW];           // per target column: first panel row present
+};
+struct RgSmem {
+    double val[kRgSlots];      // the staged slots
+    double L[kRgPushes][kB];   // the pushes' L rows (row = lane)
+    uint16_t idx[kRgIdx];      // MAC -> slot index
+    uint16_t uidx[kRgPushes * kSnW];  // (push, pair) -> index of U(p0, k)
+};
+union WarpSmem {
+    TrsmSmem t;
+    RectSmem r;
+    RgSmem g;
+};
+
 // Panel metadata, lane = panel column: its diagonal slot and the first
 // panel row present in it (a supernode's U rows in a column are a suffix).
-// Loaded lane-parallel so the block loads below issue back to back.
 __device__ __forceinline__ void panel_cols(const SnParams &P, int p0, int w, int lane, int &dc, int &clo) {
     dc = 0;
     clo = kB;
@@ -118,467 +178,439 @@ __device__ __forceinline__ void panel_cols(const SnParams &P, int p0, int w, int
     }
 }
 
-// The unrolled task variants below run every loop to the class width WM
-// without per-width branches: registers of columns / rows >= w hold
-// garbage that is never stored (and never feeds a stored value -- a column
-// only receives updates from lower columns), so the FP64 chains are free
-// of branches and the compiler can interleave them.  Structural
-// predicates that change stored values (a supernode's partial U suffix,
-// col_a) become selects, never a subtraction of a zero product: x - l * 0
+// Structural predicates that change stored values (a supernode's partial U
+// suffix, col_a) are selects, never a subtraction of a zero product: x - l * 0
 // is not always x (x = -0 with l < 0, or l = inf).
 
-// DIAG: the w x w block of the panel, lane = block row r holding its row
-// in registers.  Step j: row j is final for columns >= j (U part), lane j
-// broadcasts it; every lane r > j takes column j's undivided value (the
-// column maximum over the block's L part -- the U rows are taken by the
-// check pass), divides it by the pivot and updates its later columns, so
-// every element receives its sources j in ascending order.
-template <int WM>
-__device__ __forceinline__ void diag_factor(const SnParams &P, int p0, int w, int lane, int dcl, int clol,
-                                            double (&x)[WM], unsigned long long &mymax) {
-#pragma unroll
-    for (int c = 0; c < WM; c++) {
-        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
-        x[c] = (c < w && lane < w && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
-    }
-    mymax = 0;
-    static_for<0, WM>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        const bool below = lane > j && lane < w;
-        // bit c: U(j, c) present (column c's U suffix starts at or above row j)
-        const unsigned has = __ballot_sync(0xffffffffu, clol <= j);
-        const unsigned long long m = warp_max(below ? absbits(x[j]) : 0ull);
-        if (lane == j) mymax = m;
-        const double piv = __shfl_sync(0xffffffffu, x[j], j);
-        const double l = __ddiv_rn(x[j], piv);
-        x[j] = below ? l : x[j];
-#pragma unroll
-        for (int c = j + 1; c < WM; c++) {
-            const double ujc = __shfl_sync(0xffffffffu, x[c], j);
-            const double y = msub(x[c], l, ujc);
-            x[c] = (below && ((has >> c) & 1u)) ? y : x[c];
-        }
-    });
-}
-
-template <int WM>
-__device__ void task_diag(const SnParams &P, int4 ta, int lane) {
-    const int p0 = ta.z, w = ta.w - ta.z;
-    int dcl, clol;
-    panel_cols(P, p0, w, lane, dcl, clol);
-    double x[WM];
-    unsigned long long mymax;
-    diag_factor<WM>(P, p0, w, lane, dcl, clol, x, mymax);
-#pragma unroll
-    for (int c = 0; c < WM; c++) {
-        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
-        if (c < w && lane < w && lane >= clo) stv(P.v + dc + (lane - c), x[c]);
-    }
-    if (lane < w && mymax) atomicMax(P.cmax + p0 + lane, mymax);
-}
-
-// TRSM: 32 rows below the panel; lane = row, the row's w values in
-// registers; step j takes the undivided value's maximum, divides, and
-// updates the later columns with U(j, c) from the factored block (shared
-// memory, broadcast reads).
-template <int WM>
-__device__ void task_trsm(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane, bool local) {
+// TRSM(P, chunk), w >= 2: the w x w diagonal block is factored locally
+// (every push into P is done, and nothing writes the block in place during
+// the kernel: chunk 0 stores the factored block in the scratch area, written
+// back after the kernel, and records the block's L-part column maxima), then
+// the chunk's 32 rows below the panel.  Lane = row.  Block step j: every
+// row r > j takes column j's undivided value (its maximum over the block's
+// L part is column j's), divides it by the pivot and updates its later
+// columns with U(j, c), so every element receives its sources j in
+// ascending order.  Row step j: the same with the factored block.
+__device__ void task_trsm(const SnParams &P, TrsmSmem &S, int4 ta, int4 tb, int4 pm, int lane) {
     const int chunk = ta.x & 0x07ffffff;
     const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     int dcl, clol;
     panel_cols(P, p0, w, lane, dcl, clol);
     const int t = chunk * 32 + lane;
     const bool act = t < h;
-    if (local) {  // the panel's own stage: its diagonal block is factored here
-        double b[WM];
-        unsigned long long unused;
-        diag_factor<WM>(P, p0, w, lane, dcl, clol, b, unused);
-#pragma unroll
-        for (int c = 0; c < WM; c++) S.b[c][lane] = lane <= c ? b[c] : 0.0;
-    } else {
-#pragma unroll
-        for (int c = 0; c < WM; c++) {
-            const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
-            S.b[c][lane] = (c < w && lane <= c && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
-        }
-    }
-    double x[WM];
-#pragma unroll
-    for (int c = 0; c < WM; c++) {
-        const int dc = __shfl_sync(0xffffffffu, dcl, c);
-        x[c] = (act && c < w) ? ldv(P.v + dc + (p1 - p0 - c) + t) : 0.0;
+    for (int c = 0; c < w; c++) {
+        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
+        S.b[c][lane] = (lane < w && lane >= clo) ? ldv(P.v + dc + (lane - c)) : 0.0;
+        S.x[c][lane] = act ? ldv(P.v + dc + (w - c) + t) : 0.0;
     }
     __syncwarp();
+    const bool inb = lane < w;
+    unsigned long long bmax = 0;
+    for (int j = 0; j < w; j++) {
+        const unsigned has = __ballot_sync(0xffffffffu, clol <= j);  // bit c: U(j, c) present
+        const bool below = lane > j && inb;
+        const double xj = S.b[j][lane];
+        const unsigned long long m = warp_max(below ? absbits(xj) : 0ull);
+        if (lane == j) bmax = m;
+        const double l = __ddiv_rn(xj, S.b[j][j]);
+        __syncwarp();
+        if (below) {
+            S.b[j][lane] = l;
+#pragma unroll 4
+            for (int c = j + 1; c < w; c++)
+                if ((has >> c) & 1u) S.b[c][lane] = msub(S.b[c][lane], l, S.b[c][j]);
+        }
+        __syncwarp();
+    }
+    if (chunk == 0) {
+        if (inb && pm.z >= 0)
+            for (int c = 0; c < w; c++) stv(P.dblk + pm.z + c * w + lane, S.b[c][lane]);
+        if (inb && bmax) atomicMax(P.cmax + p0 + lane, bmax);
+    }
     unsigned long long mymax = 0;
-    static_for<0, WM>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
+    for (int j = 0; j < w; j++) {
         const unsigned has = __ballot_sync(0xffffffffu, clol <= j);
-        const unsigned long long m = warp_max(act && j < w ? absbits(x[j]) : 0ull);
+        const double xj = S.x[j][lane];
+        const unsigned long long m = warp_max(act ? absbits(xj) : 0ull);
         if (lane == j) mymax = m;
-        const double d = __ddiv_rn(x[j], S.b[j][j]);
-        x[j] = d;
-#pragma unroll
-        for (int c = j + 1; c < WM; c++) {
-            const double y = msub(x[c], d, S.b[c][j]);
-            x[c] = ((has >> c) & 1u) ? y : x[c];
-        }
-    });
-#pragma unroll
-    for (int c = 0; c < WM; c++) {
+        const double d = __ddiv_rn(xj, S.b[j][j]);
+        S.x[j][lane] = d;
+#pragma unroll 4
+        for (int c = j + 1; c < w; c++)
+            if ((has >> c) & 1u) S.x[c][lane] = msub(S.x[c][lane], d, S.b[c][j]);
+    }
+    for (int c = 0; c < w; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c);
-        if (act && c < w) stv(P.v + dc + (p1 - p0 - c) + t, x[c]);
+        if (act) stv(P.v + dc + (w - c) + t, S.x[c][lane]);
     }
-    if (lane < w && mymax) atomicMax(P.cmax + p0 + lane, mymax);
+    if (inb && mymax) atomicMax(P.cmax + p0 + lane, mymax);
     __syncwarp();
 }
 
-// TRI: U(P, k) for every target column k of the push (lane = column):
-// forward substitution with the panel's unit-lower block, j ascending.
-template <int WM>
-__device__ void task_tri(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane, bool local) {
-    const int p0 = ta.z, p1 = ta.w, w = p1 - p0, s1 = tb.x;
-    int dcl, clol;
-    panel_cols(P, p0, w, lane, dcl, clol);
-    const int q = tb.z + lane;
-    int4 pr = make_int4(0, p1, 0, -1);
-    if (q < tb.w) pr = __ldg(P.pairs + q);
-    const bool act = pr.y < p1;
-    const int lo = max(pr.y - p0, 0);
-    if (local) {  // the panel's own stage: its unit-lower block is factored here
-        double b[WM];
-        unsigned long long unused;
-        diag_factor<WM>(P, p0, w, lane, dcl, clol, b, unused);
-        // lane r holds row r: L(r, j) = b[j] for r > j; S.b[j][r] = L(r, j)
-#pragma unroll
-        for (int j = 0; j < WM; j++) S.b[j][lane] = lane > j ? b[j] : 0.0;
-    } else {
-#pragma unroll
-        for (int j = 0; j < WM; j++) {
-            const int dj = __shfl_sync(0xffffffffu, dcl, j);
-            S.b[j][lane] = (j < w && lane > j && lane < w) ? ldv(P.v + dj + (lane - j)) : 0.0;
-        }
-    }
-    double u[WM];
-#pragma unroll
-    for (int j = 0; j < WM; j++) u[j] = (act && j < w && j >= lo) ? ldv(P.v + pr.z - (s1 - (p0 + j))) : 0.0;
-    __syncwarp();
-    static_for<0, WM>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        const double uj = u[j];
-        const bool on = j >= lo;
-#pragma unroll
-        for (int r = j + 1; r < WM; r++) {
-            const double y = msub(u[r], S.b[j][r], uj);
-            u[r] = on ? y : u[r];
-        }
-    });
-    if (act) {
-#pragma unroll
-        for (int r = 0; r < WM; r++)
-            if (r < w && r > lo) stv(P.v + pr.z - (s1 - (p0 + r)), u[r]);
-    }
-    __syncwarp();
-}
-
-// RECT for narrow panels (WM <= 8): lane = row, its divided L row in
-// registers; target columns in batches of kRectB (their U(j, k), target
-// slots and values loaded together, kRectB independent chains per lane),
-// U(j, k) broadcast by shuffle, each chain over j ascending.
-constexpr int kRectB = 4;
-
-template <int WM>
-__device__ void task_rect(const SnParams &P, int4 ta, int4 tb, int lane) {
+// TRSM for a one-column panel: divide the rows below by the pivot.
+__device__ void task_trsm1(const SnParams &P, int4 ta, int4 tb, int lane) {
     const int chunk = ta.x & 0x07ffffff;
-    const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
+    const int p0 = ta.z, h = tb.y;
+    const int t = chunk * 32 + lane;
+    const int dc = __ldg(P.diag_pos + p0);
+    const double x = t < h ? ldv(P.v + dc + 1 + t) : 0.0;
+    const double piv = ldv(P.v + dc);
+    const unsigned long long m = warp_max(t < h ? absbits(x) : 0ull);
+    if (t < h) stv(P.v + dc + 1 + t, __ddiv_rn(x, piv));
+    if (lane == 0 && m) atomicMax(P.cmax + p0, m);
+}
+
+// Target slot of source-panel row t (rows below p1, in_sn of them inside
+// the supernode) in the column of pair {k, a, base, map}.
+__device__ __forceinline__ int target_pos(const SnParams &P, int t, int in_sn, int base, int map) {
+    return t < in_sn ? base - (in_sn - t) : (map >= 0 ? __ldg(P.relmap + map + (t - in_sn)) : base + (t - in_sn));
+}
+
+// RECT for a one-column source panel (most pushes): lane = row t, the
+// target slots of every column of the push found before the target wait,
+// then every target loaded at once, one MAC each with U(p0, k) (held by
+// lane q, broadcast by shuffle).
+__device__ bool task_rect1(const SnParams &P, int4 ta, int4 tb, int4 tc, int lane, unsigned long long *tr) {
+    const int chunk = ta.x & 0x07ffffff;
+    const int Pi = ta.y, p0 = ta.z, p1 = ta.w, h = tb.y;
     const int s1 = tb.x, in_sn = s1 - p1;
     const int t = chunk * 32 + lane;
     const bool act = t < h;
     const int npair = tb.w - tb.z;
+    const int4 pm = __ldg(P.panm + Pi);
     int4 myp = make_int4(0, p1, 0, -1);
     if (lane < npair) myp = __ldg(P.pairs + tb.z + lane);
-    const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
-    double L[WM];
+    const bool colok = lane < npair && myp.y < p1;
+    const int dc = __ldg(P.diag_pos + p0);
+    int pos[kSnW];
 #pragma unroll
-    for (int j = 0; j < WM; j++) {
-        const int dj = __shfl_sync(0xffffffffu, dcl, j);
-        L[j] = (act && j < w) ? ldv(P.v + dj + (p1 - p0 - j) + t) : 0.0;
+    for (int q = 0; q < kSnW; q++) {
+        const int base = __shfl_sync(0xffffffffu, myp.z, q);
+        const int map = __shfl_sync(0xffffffffu, myp.w, q);
+        const bool ok = __shfl_sync(0xffffffffu, (int)colok, q) != 0;
+        pos[q] = (ok && act) ? target_pos(P, t, in_sn, base, map) : -1;
     }
-    for (int q0 = 0; q0 < npair; q0 += kRectB) {
-        double uv[kRectB], x[kRectB];
-        int pos[kRectB], lo[kRectB];
+    if (!wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
+    if (tr && lane == 0) tr[1] = globaltimer();
+    const double L = act ? ldv(P.v + dc + 1 + t) : 0.0;
+    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
+    if (tr && lane == 0) tr[2] = globaltimer();
+    const double u = colok ? ldv(P.v + myp.z - (s1 - p0)) : 0.0;  // U(p0, k_lane)
+    double x[kSnW];
 #pragma unroll
-        for (int b = 0; b < kRectB; b++) {
-            const int q = q0 + b;
-            const int a = __shfl_sync(0xffffffffu, myp.y, q & 31);
-            const int base = __shfl_sync(0xffffffffu, myp.z, q & 31);
-            const int map = __shfl_sync(0xffffffffu, myp.w, q & 31);
-            const bool ok = q < npair && a < p1;
-            lo[b] = ok ? max(a - p0, 0) : WM;
-            uv[b] = (ok && lane < w && lane >= lo[b]) ? ldv(P.v + base - (s1 - (p0 + lane))) : 0.0;
-            pos[b] = -1;
-            if (ok && act)
-                pos[b] = t < in_sn ? base - (in_sn - t)
-                                   : (map >= 0 ? __ldg(P.relmap + map + (t - in_sn)) : base + (t - in_sn));
+    for (int q = 0; q < kSnW; q++) x[q] = pos[q] >= 0 ? ldv(P.v + pos[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < kSnW; q++) {
+        const double uq = __shfl_sync(0xffffffffu, u, q);
+        if (pos[q] >= 0) stv(P.v + pos[q], msub(x[q], L, uq));
+    }
+    return true;
+}
+
+// U(P, K) of a push in shared memory: lane q < 16 holds target column q.
+__device__ __forceinline__ void load_u_tile(const SnParams &P, RectSmem &R, int4 myp, bool colok, int mylo,
+                                            int p0, int w, int s1, int lane) {
+    if (lane < kSnW) {
+        R.lo[lane] = mylo;
+        for (int j = 0; j < w; j++)
+            R.u[j][lane] = (colok && j >= mylo) ? ldv(P.v + myp.z - (s1 - (p0 + j))) : 0.0;
+    }
+}
+// The forward substitution U(r, k) -= L(r, j) * U(j, k), j ascending.
+__device__ __forceinline__ void solve_u_tile(RectSmem &R, bool colok, int mylo, int w, int lane) {
+    if (lane < kSnW && colok) {
+        for (int j = mylo; j < w - 1; j++) {
+            const double uj = R.u[j][lane];
+            for (int r = j + 1; r < w; r++) R.u[r][lane] = msub(R.u[r][lane], R.lb[j][r], uj);
         }
-#pragma unroll
-        for (int b = 0; b < kRectB; b++) x[b] = pos[b] >= 0 ? ldv(P.v + pos[b]) : 0.0;
-#pragma unroll
-        for (int j = 0; j < WM; j++) {
-#pragma unroll
-            for (int b = 0; b < kRectB; b++) {
-                const double uj = __shfl_sync(0xffffffffu, uv[b], j);
-                const double y = msub(x[b], L[j], uj);
-                x[b] = (j >= lo[b] && j < w) ? y : x[b];
-            }
-        }
-#pragma unroll
-        for (int b = 0; b < kRectB; b++)
-            if (pos[b] >= 0) stv(P.v + pos[b], x[b]);
+    }
+}
+__device__ __forceinline__ void load_lb(const SnParams &P, RectSmem &R, int off, int w, int lane) {
+    for (int e = lane; e < w * w; e += 32) {
+        const int j = e / w, r = e - j * w;
+        R.lb[j][r] = ldv(P.dblk + off + e);
     }
 }
 
-// RECT for wide panels (w > 8): register-tiled blocks C[32 rows x 16
-// target columns] -= L[32 x w] * U[w x 16] (two halves for > 16 target
-// columns), every element's chain over j ascending.  Lane (ry, cx) =
-// (lane / 4, lane % 4) holds rows ry + 8 i and columns cx + 4 k (i, k < 4);
-// per j it reads 4 L and 4 U values from shared memory (conflict-free
-// broadcasts) for 16 MACs.  Columns whose U suffix starts inside the panel
-// (lo > 0, only in structurally unsymmetric patterns) take the select path.
-struct RectSmem {
-    double l[kB][kB];  // [j][row]
-    double u[kB][16];  // [j][column of the half]
-    int lo[16];
-};
-
-static_assert(sizeof(RectSmem) <= sizeof(WarpSmem), "RectSmem overlays WarpSmem");
-
-__device__ void task_rect_tile(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int lane) {
+// RECT for source panels with w >= 2: register-tiled block C[32 rows x 16
+// target columns] -= L[32 x w] * U[w x 16], every element's chain over j
+// ascending, after the forward substitution of U(P, K) inside the source
+// block when the push changes it.  Lane (ry, cx) = (lane / 4, lane % 4)
+// holds rows ry + 8 i and columns cx + 4 k (i, k < 4); per j it reads 4 L and
+// 4 U values from shared memory (conflict-free broadcasts) for 16 MACs.
+// Columns whose U suffix starts inside the panel (lo > 0, only in
+// structurally unsymmetric patterns) take the select path.
+__device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4 tc, int lane,
+                          unsigned long long *tr) {
+    const int code = ta.x >> 27;
     const int chunk = ta.x & 0x07ffffff;
-    const int p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
+    const int Pi = ta.y, p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     const int s1 = tb.x, in_sn = s1 - p1;
     const int npair = tb.w - tb.z;
     const int t = chunk * 32 + lane;
+    const int4 pm = __ldg(P.panm + Pi);
     int4 myp = make_int4(0, p1, 0, -1);
     if (lane < npair) myp = __ldg(P.pairs + tb.z + lane);
     const bool colok = lane < npair && myp.y < p1;
     const int mylo = colok ? max(myp.y - p0, 0) : kB;
     const int dcl = lane < w ? __ldg(P.diag_pos + p0 + lane) : 0;
-#pragma unroll 8
-    for (int j = 0; j < kSnW; j++) {
-        const int dj = __shfl_sync(0xffffffffu, dcl, j);
-        R.l[j][lane] = (t < h && j < w) ? ldv(P.v + dj + (p1 - p0 - j) + t) : 0.0;
-    }
     const int ry = lane >> 2, cx = lane & 3;
-    for (int half = 0; half * 16 < npair; half++) {
-        const int qh = lane - 16 * half;  // this lane's column in the half (lanes 16h .. 16h+15)
-        __syncwarp();
-        if (qh >= 0 && qh < 16) {
-            R.lo[qh] = mylo;
-#pragma unroll 8
-            for (int j = 0; j < kSnW; j++)
-                R.u[j][qh] = (colok && j < w && j >= mylo) ? ldv(P.v + myp.z - (s1 - (p0 + j))) : 0.0;
+    int pos[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int q = cx + 4 * k;
+        const int base = __shfl_sync(0xffffffffu, myp.z, q), map = __shfl_sync(0xffffffffu, myp.w, q);
+        const bool cok = __shfl_sync(0xffffffffu, (int)colok, q) != 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int tt = chunk * 32 + ry + 8 * i;
+            pos[i][k] = (cok && tt < h) ? target_pos(P, tt, in_sn, base, map) : -1;
         }
-        const bool anylo = __any_sync(0xffffffffu, qh >= 0 && qh < 16 && colok && mylo > 0);
-        double c[4][4];
-        int pos[4][4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int q = 16 * half + cx + 4 * k;
-            const int base = __shfl_sync(0xffffffffu, myp.z, q & 31), map = __shfl_sync(0xffffffffu, myp.w, q & 31);
-            const bool cok = __shfl_sync(0xffffffffu, (int)colok, q & 31) != 0 && q < 32;
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int tt = chunk * 32 + ry + 8 * i;
-                int ps = -1;
-                if (cok && tt < h)
-                    ps = tt < in_sn ? base - (in_sn - tt)
-                                    : (map >= 0 ? __ldg(P.relmap + map + (tt - in_sn)) : base + (tt - in_sn));
-                pos[i][k] = ps;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-#pragma unroll
-            for (int i = 0; i < 4; i++) c[i][k] = pos[i][k] >= 0 ? ldv(P.v + pos[i][k]) : 0.0;
-        __syncwarp();
-        if (!anylo) {
-#pragma unroll 4
-            for (int j = 0; j < w; j++) {
-                double l[4], u[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
-#pragma unroll
-                for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
-#pragma unroll
-                for (int i = 0; i < 4; i++)
-#pragma unroll
-                    for (int k = 0; k < 4; k++) c[i][k] = msub(c[i][k], l[i], u[k]);
-            }
-        } else {
-            int clo[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) clo[k] = R.lo[cx + 4 * k];
-            for (int j = 0; j < w; j++) {
-                double l[4], u[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
-#pragma unroll
-                for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
-#pragma unroll
-                for (int i = 0; i < 4; i++)
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const double y = msub(c[i][k], l[i], u[k]);
-                        c[i][k] = j >= clo[k] ? y : c[i][k];
-                    }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-#pragma unroll
-            for (int i = 0; i < 4; i++)
-                if (pos[i][k] >= 0) stv(P.v + pos[i][k], c[i][k]);
     }
+    if (!wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
+    if (tr && lane == 0) tr[1] = globaltimer();
+    for (int j = 0; j < w; j++) {
+        const int dj = __shfl_sync(0xffffffffu, dcl, j);
+        R.l[j][lane] = t < h ? ldv(P.v + dj + (w - j) + t) : 0.0;
+    }
+    const bool tri = (code & kSnTriF) != 0;
+    if (tri) load_lb(P, R, pm.z, w, lane);
+    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
+    if (tr && lane == 0) tr[2] = globaltimer();
+    load_u_tile(P, R, myp, colok, mylo, p0, w, s1, lane);
+    const bool anylo = __any_sync(0xffffffffu, colok && mylo > 0);
+    double c[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) c[i][k] = pos[i][k] >= 0 ? ldv(P.v + pos[i][k]) : 0.0;
     __syncwarp();
-}
-
-// Panel widths in classes 1, 2, 4, 8, 16, 32: every task runs the variant
-// unrolled for its class, so the code a phase executes stays small (one
-// fully unrolled 32-wide kernel is ~700 KB of SASS, far beyond the
-// instruction cache, and most panels are one column wide).
-template <int WM>
-__device__ __forceinline__ void run_kind(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
-    const int code = ta.x >> 27;
-    switch (code & ~kSnLocal) {
-        case kSnDiag: task_diag<WM>(P, ta, lane); break;
-        case kSnTrsm: task_trsm<WM>(P, S, ta, tb, lane, code & kSnLocal); break;
-        case kSnTri: task_tri<WM>(P, S, ta, tb, lane, code & kSnLocal); break;
-        default:
-            if (WM > 8) task_rect_tile(P, *reinterpret_cast<RectSmem *>(&S), ta, tb, lane);
-            else task_rect<WM>(P, ta, tb, lane);
-            break;
+    if (tri) {
+        solve_u_tile(R, colok, mylo, w, lane);
+        __syncwarp();
     }
-}
-
-__device__ __forceinline__ void run_task(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int lane) {
-    const int w = ta.w - ta.z;
-    if (w <= 1) run_kind<1>(P, S, ta, tb, lane);
-    else if (w <= 2) run_kind<2>(P, S, ta, tb, lane);
-    else if (w <= 4) run_kind<4>(P, S, ta, tb, lane);
-    else if (w <= 8) run_kind<8>(P, S, ta, tb, lane);
-    else if (kSnW <= 16 || w <= 16) run_kind<16>(P, S, ta, tb, lane);
-    else run_kind<(kSnW > 16 ? 32 : 16)>(P, S, ta, tb, lane);
-}
-
-// A warp leaving phase p counts its tasks of p (release: fence, then add);
-// the warp that completes p advances the phases-complete counter.  Phases
-// complete in order (a phase's tasks start after the previous one
-// completed), and atomicMax keeps the counter monotone.
-__device__ __forceinline__ void flush_phase(const SnParams &P, int p, unsigned mine) {
-    __threadfence();
-    const unsigned old = atomicAdd(P.done + (size_t)p * kDoneStride, mine);
-    if (old + mine == (unsigned)(__ldg(P.phase_ptr + p + 1) - __ldg(P.phase_ptr + p))) {
-        if (P.stamps) P.stamps[1 + p] = globaltimer();
+    int clo[4];
 #pragma unroll
-        for (int r = 0; r < kGdoneRep; r++) atomicMax(P.gdone + r * kLine, (unsigned)(p + 1));
+    for (int k = 0; k < 4; k++) clo[k] = anylo ? R.lo[cx + 4 * k] : 0;
+#pragma unroll 2
+    for (int j = 0; j < w; j++) {
+        double l[4], u[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
+#pragma unroll
+        for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const double y = msub(c[i][k], l[i], u[k]);
+                c[i][k] = j >= clo[k] ? y : c[i][k];
+            }
     }
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            if (pos[i][k] >= 0) stv(P.v + pos[i][k], c[i][k]);
+    if ((code & kSnWriteU) && lane < kSnW && colok)
+        for (int r = mylo + 1; r < w; r++) stv(P.v + myp.z - (s1 - (p0 + r)), R.u[r][lane]);
+    __syncwarp();
+    return true;
 }
 
-struct CtaSync {
-    int known;  // phases known complete (from the last poll of this CTA)
-    int lock;   // one polling warp per CTA at a time
-};
+// UW(x): after every RECT chunk of push x has read U(P, K), solve it once
+// more (the same chains, so the same bits) and write it.
+__device__ bool task_uw(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4 tc, int lane,
+                        unsigned long long *tr) {
+    const int Pi = ta.y, p0 = ta.z, p1 = ta.w, w = p1 - p0, s1 = tb.x;
+    const int npair = tb.w - tb.z;
+    const int4 pm = __ldg(P.panm + Pi);
+    int4 myp = make_int4(0, p1, 0, -1);
+    if (lane < npair) myp = __ldg(P.pairs + tb.z + lane);
+    const bool colok = lane < npair && myp.y < p1;
+    const int mylo = colok ? max(myp.y - p0, 0) : kB;
+    // the RECT chunks waited for P's TRSM chunks (which wrote the block)
+    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)(tc.y + pm.y), lane)) return false;
+    if (tr && lane == 0) tr[1] = tr[2] = globaltimer();
+    load_lb(P, R, pm.z, w, lane);
+    load_u_tile(P, R, myp, colok, mylo, p0, w, s1, lane);
+    __syncwarp();
+    solve_u_tile(R, colok, mylo, w, lane);
+    __syncwarp();
+    if (lane < kSnW && colok)
+        for (int r = mylo + 1; r < w; r++) stv(P.v + myp.z - (s1 - (p0 + r)), R.u[r][lane]);
+    __syncwarp();
+    return true;
+}
 
-// Wait until phases [0, p) are complete.  Warps of a CTA share one poller:
-// the others read the CTA's last observation from shared memory, so an
-// SM sends at most one poll at a time to the (replicated) global counter
-// instead of one per waiting warp.  False on the watchdog / error path.
-__device__ bool wait_phase(const SnParams &P, CtaSync *cs, int p, int lane) {
-    bool ok = true;
-    if (lane == 0) {
-        volatile int *known = &cs->known;
-        if (*known < p) {
-            const unsigned *g = P.gdone + (blockIdx.x % kGdoneRep) * kLine;
-            const unsigned long long t0 = globaltimer();
-            while (*known < p) {
-                if (atomicCAS(&cs->lock, 0, 1) == 0) {
-                    const int seen = (int)ld_acquire(g);
-                    atomicMax(&cs->known, seen);
-                    atomicExch(&cs->lock, 0);
-                    if (seen >= p) break;
-                }
-                if (*(volatile int *)P.err) { ok = false; break; }
-                if (globaltimer() - t0 > kSnWatchdogNs) {
-                    atomicExch(P.err, 1);
-                    ok = false;
-                    break;
-                }
-                __nanosleep(32);
-            }
-        }
-        __threadfence_block();
+// RG: consecutive one-chunk pushes from one-column source panels into K
+// (at most kRgPushes), applied in order by this warp on a shared-memory
+// image of the slots they touch.  A one-column panel is a one-column
+// supernode: its rows below (lane = row) all sit in R_S.  Lane i holds push
+// i's records.  Before the target wait the warp stages the MAC indices (u16,
+// pair q and row t of push i at its offset + q * h + t) and the multiplier
+// indices; after it, the slot values.  The source panels' TRSM counters are
+// acquired lane-parallel; the pushes whose sources are factored get their L
+// rows loaded together, then run back to back from shared memory (a warp
+// barrier between pushes), so the chain into K costs ~0.1 us per push.  The
+// slots are stored back and every push counted at the end.
+__device__ bool task_rg(const SnParams &P, RgSmem &G, int4 ta, int4 tb, int4 tc, int lane,
+                        unsigned long long *tr) {
+    const int idx0 = ta.y, uidx0 = ta.z;
+    const int slot0 = tb.x, nslot = tb.y, x0 = tb.z, m = tb.w;
+    int4 ps = make_int4(0, 0, 0, 0), pn = make_int4(0, 1, 0, 0);
+    int dcl = 0;
+    if (lane < m) {
+        ps = __ldg(P.push + x0 + lane);
+        pn = __ldg(P.pan + ps.x);
+        dcl = __ldg(P.diag_pos + pn.x);
     }
-    return __shfl_sync(0xffffffffu, (int)ok, 0) != 0;
+    // per push: MAC indices and multiplier indices (exclusive scans over the lanes)
+    const int npl = ps.z - ps.y, nmac = npl * pn.w;
+    int ioff = nmac, uoff = npl;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, ioff, d), b = __shfl_up_sync(0xffffffffu, uoff, d);
+        if (lane >= d) {
+            ioff += a;
+            uoff += b;
+        }
+    }
+    ioff -= nmac;
+    uoff -= npl;
+    const int nidx = __shfl_sync(0xffffffffu, ioff + nmac, 31), nuidx = __shfl_sync(0xffffffffu, uoff + npl, 31);
+    for (int e = lane; e < nidx; e += 32) G.idx[e] = __ldg(P.rg_idx + idx0 + e);
+    for (int e = lane; e < nuidx; e += 32) G.uidx[e] = __ldg(P.rg_uidx + uidx0 + e);
+    int slot[kRgSlots / 32];
+#pragma unroll
+    for (int j = 0; j < kRgSlots / 32; j++) slot[j] = lane + 32 * j < nslot ? __ldg(P.rg_slot + slot0 + lane + 32 * j) : -1;
+    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
+    if (tr && lane == 0) tr[1] = tr[2] = globaltimer();
+#pragma unroll
+    for (int j = 0; j < kRgSlots / 32; j++)
+        if (slot[j] >= 0) G.val[lane + 32 * j] = ldv(P.v + slot[j]);
+    const unsigned long long t0 = globaltimer();
+    int done = 0;
+    while (done < m) {
+        // pushes [done, e) have factored sources (lane i acquires push i's)
+        const bool rdy = lane < done || lane >= m || ld_acquire(P.cnt + 2 * ps.x + 1) >= 1u;
+        const unsigned nr = __ballot_sync(0xffffffffu, rdy) | (m < 32 ? ~0u << m : 0u);
+        const int e = nr == ~0u ? m : min(m, __ffs(~nr) - 1);
+        if (e == done) {
+            if (*(volatile int *)P.err) return false;
+            if (globaltimer() - t0 > kSnWatchdogNs) {
+                if (lane == 0) atomicExch(P.err, 1);
+                return false;
+            }
+            __nanosleep(64);
+            continue;
+        }
+        __syncwarp();
+        {  // their L rows, loaded together
+            double Lr[kRgPushes];
+#pragma unroll
+            for (int k = 0; k < kRgPushes; k++) {
+                const int h = __shfl_sync(0xffffffffu, pn.w, k), dc = __shfl_sync(0xffffffffu, dcl, k);
+                Lr[k] = (k >= done && k < e && lane < h) ? ldv(P.v + dc + 1 + lane) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < kRgPushes; k++)
+                if (k >= done && k < e) G.L[k][lane] = Lr[k];
+        }
+        __syncwarp();
+        for (int k = done; k < e; k++) {
+            const int h = __shfl_sync(0xffffffffu, pn.w, k), np_ = __shfl_sync(0xffffffffu, npl, k);
+            const int io = __shfl_sync(0xffffffffu, ioff, k), uo = __shfl_sync(0xffffffffu, uoff, k);
+            const double L = G.L[k][lane];
+            if (lane < h) {
+                for (int q = 0; q < np_; q++) {
+                    const double u = G.val[G.uidx[uo + q]];
+                    const int ix = G.idx[io + q * h + lane];
+                    G.val[ix] = msub(G.val[ix], L, u);
+                }
+            }
+            __syncwarp();  // the next push sees these updates
+        }
+        done = e;
+    }
+#pragma unroll
+    for (int j = 0; j < kRgSlots / 32; j++)
+        if (slot[j] >= 0) stv(P.v + slot[j], G.val[lane + 32 * j]);
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        atomicAdd(P.cnt + 2 * tc.x, (unsigned)m);
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool run_task(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int4 tc, int lane,
+                                         unsigned long long *tr) {
+    const int kind = (ta.x >> 27) >> 2;
+    if (kind == kSnRg) return task_rg(P, S.g, ta, tb, tc, lane, tr);
+    const int w = ta.w - ta.z;
+    if (kind == kSnTrsm) {
+        const int4 pm = __ldg(P.panm + ta.y);
+        if (!wait_ge(P, P.cnt + 2 * ta.y, (unsigned)pm.x, lane)) return false;
+        if (tr && lane == 0) tr[1] = tr[2] = globaltimer();
+        if (w == 1) task_trsm1(P, ta, tb, lane);
+        else task_trsm(P, S.t, ta, tb, pm, lane);
+        release(P.cnt + 2 * ta.y + 1, lane);
+        return true;
+    }
+    if (kind == kSnUw) return task_uw(P, S.r, ta, tb, tc, lane, tr);
+    const bool ok = w == 1 ? task_rect1(P, ta, tb, tc, lane, tr) : task_rect(P, S.r, ta, tb, tc, lane, tr);
+    if (ok) release(P.cnt + 2 * tc.x, lane);
+    return ok;
 }
 
 __global__ void __launch_bounds__(kSnThreads, 2) sn_kernel(SnParams P) {
     extern __shared__ __align__(16) unsigned char sn_smem_raw[];
     WarpSmem *smem = reinterpret_cast<WarpSmem *>(sn_smem_raw);
-    __shared__ CtaSync cs;
-    if (threadIdx.x == 0) {
-        cs.known = 0;
-        cs.lock = 0;
-        if (P.stamps && blockIdx.x == 0) P.stamps[0] = globaltimer();
-    }
-    __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem &S = smem[wib];
     const int nw = gridDim.x * kSnWarps;
-    int cur = -1;
-    unsigned mine = 0;
     int i = wib * gridDim.x + blockIdx.x;
-    int4 ta = make_int4(0, 0, 0, 0), tb = ta;
+    int4 ta = make_int4(0, 0, 0, 0), tb = ta, tc = ta;
     if (i < P.n_tasks) {
-        ta = __ldg(P.tasks + 2 * (size_t)i);
-        tb = __ldg(P.tasks + 2 * (size_t)i + 1);
+        ta = __ldg(P.tasks + 3 * (size_t)i);
+        tb = __ldg(P.tasks + 3 * (size_t)i + 1);
+        tc = __ldg(P.tasks + 3 * (size_t)i + 2);
     }
     while (i < P.n_tasks) {
         // the next task's records load while this one runs
         const int inext = i + nw;
-        int4 na = ta, nb = tb;
+        int4 na = ta, nb = tb, nc = tc;
         if (inext < P.n_tasks) {
-            na = __ldg(P.tasks + 2 * (size_t)inext);
-            nb = __ldg(P.tasks + 2 * (size_t)inext + 1);
+            na = __ldg(P.tasks + 3 * (size_t)inext);
+            nb = __ldg(P.tasks + 3 * (size_t)inext + 1);
+            nc = __ldg(P.tasks + 3 * (size_t)inext + 2);
         }
-        unsigned long long t_start = 0;
-        if (P.trace) t_start = globaltimer();
-        if (ta.y != cur) {
-            if (mine) {
-                __syncwarp();
-                if (lane == 0) flush_phase(P, cur, mine);
-            }
-            mine = 0;
-            cur = ta.y;
-            if (cur > 0 && !wait_phase(P, &cs, cur, lane)) return;
-        }
-        unsigned long long t_wait = 0;
-        if (P.trace) t_wait = globaltimer();
-        run_task(P, S, ta, tb, lane);
-        if (P.trace && lane == 0) {
-            __syncwarp(1u);
-            unsigned long long *tr = P.trace + 4 * (size_t)i;
-            tr[0] = t_start;
-            tr[1] = t_wait;
-            tr[2] = globaltimer();
-        }
-        mine++;
+        unsigned long long *tr = P.trace ? P.trace + 4 * (size_t)i : nullptr;
+        if (tr && lane == 0) tr[0] = globaltimer();
+        if (!run_task(P, S, ta, tb, tc, lane, tr)) return;
+        if (tr && lane == 0) tr[3] = globaltimer();
         i = inext;
         ta = na;
         tb = nb;
+        tc = nc;
     }
-    if (mine) {
-        __syncwarp();
-        if (lane == 0) flush_phase(P, cur, mine);
+}
+
+// The factored diagonal blocks (scratch, column-major w x w) written back
+// into the values: one warp per wide panel, lane = block row.
+__global__ void sn_writeback_kernel(double *v, const double *dblk, const int4 *wb, i32 nwb, const i32 *diag_pos,
+                                    const i32 *col_a) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (i32 k = gw; k < nwb; k += nw) {
+        const int4 e = __ldg(wb + k);  // {p0, p1, scratch offset, 0}
+        const int p0 = e.x, w = e.y - e.x;
+        if (lane >= w) continue;
+        for (int c = 0; c < w; c++) {
+            const int clo = max(__ldg(col_a + p0 + c) - p0, 0);
+            if (lane >= clo) v[__ldg(diag_pos + p0 + c) + (lane - c)] = __ldcg(dblk + e.z + c * w + lane);
+        }
     }
 }
 
@@ -625,13 +657,14 @@ cudaError_t up(T **dst, const std::vector<T> &src, i64 *bytes) {
 }  // namespace
 
 struct SnDev {
-    int4 *pairs = nullptr, *tasks = nullptr;
-    i32 *relmap = nullptr, *phase_ptr = nullptr, *col_a = nullptr;
-    i64 n = 0, n_tasks = 0, n_phases = 0;
-    unsigned *done = nullptr, *gdone = nullptr;
+    int4 *pairs = nullptr, *tasks = nullptr, *panm = nullptr, *wb = nullptr, *push = nullptr, *pan = nullptr;
+    i32 *relmap = nullptr, *col_a = nullptr, *rg_slot = nullptr;
+    uint16_t *rg_idx = nullptr, *rg_uidx = nullptr;
+    double *dblk = nullptr;
+    i64 n = 0, n_tasks = 0, n_pan = 0, n_wb = 0;
+    unsigned *cnt = nullptr;
     unsigned long long *cmax = nullptr;
-    unsigned long long *stamps = nullptr;  // per-phase completion times (diagnostics)
-    unsigned long long *trace = nullptr;   // per-task timestamps (diagnostics)
+    unsigned long long *trace = nullptr;  // per-task timestamps (diagnostics)
     int grid = 0;
 };
 
@@ -648,8 +681,8 @@ int sn_grid(int sm_count) {
 
 void sn_free(SnDev *d) {
     if (!d) return;
-    void *ptrs[] = {d->pairs, d->tasks, d->relmap, d->phase_ptr, d->col_a, d->done, d->gdone, d->cmax,
-                    d->stamps, d->trace};
+    void *ptrs[] = {d->pairs, d->tasks, d->panm, d->wb,   d->push, d->pan,  d->relmap, d->col_a,
+                    d->dblk,  d->cnt,   d->cmax, d->trace, d->rg_slot, d->rg_idx, d->rg_uidx};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete d;
@@ -662,24 +695,37 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
         return reinterpret_cast<const std::vector<int4> &>(v);
     };
     static_assert(sizeof(I4) == sizeof(int4), "I4 layout");
+    std::vector<int4> wb;  // {p0, p1, scratch offset, 0} of the panels with w >= 2
+    for (size_t q = 0; q < p->pan.size(); q++)
+        if (p->panm[q].z >= 0) wb.push_back(make_int4(p->pan[q].x, p->pan[q].y, p->panm[q].z, 0));
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = up(&d->pairs, cast(p->pairs), bytes);
     if (e == cudaSuccess) e = up(&d->tasks, cast(p->tasks), bytes);
+    if (e == cudaSuccess) e = up(&d->panm, cast(p->panm), bytes);
+    if (e == cudaSuccess) e = up(&d->wb, wb, bytes);
+    if (e == cudaSuccess) e = up(&d->push, cast(p->push), bytes);
+    if (e == cudaSuccess) e = up(&d->pan, cast(p->pan), bytes);
+    if (e == cudaSuccess) e = up(&d->rg_slot, p->rg_slot, bytes);
+    if (e == cudaSuccess) e = up(&d->rg_idx, p->rg_idx, bytes);
+    if (e == cudaSuccess) e = up(&d->rg_uidx, p->rg_uidx, bytes);
     if (e == cudaSuccess) e = up(&d->relmap, p->relmap, bytes);
-    if (e == cudaSuccess) e = up(&d->phase_ptr, p->phase_ptr, bytes);
     if (e == cudaSuccess) e = up(&d->col_a, p->col_a, bytes);
     d->n = p->n;
-    d->n_tasks = (i64)p->tasks.size() / 2;
-    d->n_phases = (i64)p->phase_ptr.size() - 1;
-    if (e == cudaSuccess)
-        e = cudaMalloc((void **)&d->done, sizeof(unsigned) * kDoneStride * std::max<i64>(d->n_phases, 1));
-    if (e == cudaSuccess) e = cudaMalloc((void **)&d->gdone, sizeof(unsigned) * kGdoneRep * kLine);
+    d->n_tasks = (i64)p->tasks.size() / 3;
+    d->n_pan = (i64)p->pan.size();
+    d->n_wb = (i64)wb.size();
+    if (e == cudaSuccess && p->n_dblk > 0) {
+        e = cudaMalloc((void **)&d->dblk, sizeof(double) * p->n_dblk);
+        *bytes += (i64)sizeof(double) * p->n_dblk;
+    }
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->cnt, sizeof(unsigned) * 2 * std::max<i64>(d->n_pan, 1));
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->cmax, sizeof(unsigned long long) * std::max<i64>(d->n, 1));
     if (e != cudaSuccess) {
         set_error(std::string("supernodal plan upload: ") + cudaGetErrorString(e));
         sn_free(d);
         return GLU_ECUDA;
     }
+    *bytes += (i64)(sizeof(unsigned) * 2 * d->n_pan + sizeof(unsigned long long) * d->n);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -693,24 +739,15 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
     return GLU_OK;
 }
 
-int64_t sn_set_stamps(SnDev *d, int mode) {
-    // 1: per-phase stamps, 2: + per-task trace, 0: off
-    if (mode && !d->stamps) {
-        if (cudaMalloc((void **)&d->stamps, sizeof(unsigned long long) * (d->n_phases + 1)) != cudaSuccess) {
-            set_error("cudaMalloc(phase stamps)");
-            return GLU_ECUDA;
-        }
-    } else if (!mode && d->stamps) {
-        cudaFree(d->stamps);
-        d->stamps = nullptr;
-    }
-    if (mode == 2 && !d->trace) {
+int64_t sn_set_trace(SnDev *d, int mode) {
+    // 1: per-task trace, 0: off
+    if (mode && !d->trace) {
         if (cudaMalloc((void **)&d->trace, sizeof(unsigned long long) * 4 * std::max<i64>(d->n_tasks, 1)) !=
             cudaSuccess) {
             set_error("cudaMalloc(task trace)");
             return GLU_ECUDA;
         }
-    } else if (mode != 2 && d->trace) {
+    } else if (!mode && d->trace) {
         cudaFree(d->trace);
         d->trace = nullptr;
     }
@@ -725,23 +762,14 @@ int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks) {
     return m;
 }
 
-int64_t sn_read_stamps(SnDev *d, int64_t *out, int64_t max) {
-    if (!d->stamps) return 0;
-    const i64 m = std::min<i64>(max, d->n_phases + 1);
-    std::vector<unsigned long long> h((size_t)m);
-    if (cudaMemcpy(h.data(), d->stamps, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
-        return GLU_ECUDA;
-    for (i64 i = 0; i < m; i++) out[i] = (int64_t)h[i];
-    return m;
-}
-
 int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *diag_pos,
                   const int32_t *fail_level, int32_t n, double thresh, bool by_column,
                   unsigned long long *fail, int *err, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(d->done, 0, sizeof(unsigned) * kDoneStride * std::max<i64>(d->n_phases, 1), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(d->gdone, 0, sizeof(unsigned) * kGdoneRep * kLine, s);
+    cudaError_t e = cudaMemsetAsync(d->cnt, 0, sizeof(unsigned) * 2 * std::max<i64>(d->n_pan, 1), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d->cmax, 0, sizeof(unsigned long long) * std::max<i64>(d->n, 1), s);
+    if (d->trace && e == cudaSuccess)
+        e = cudaMemsetAsync(d->trace, 0, sizeof(unsigned long long) * 4 * std::max<i64>(d->n_tasks, 1), s);
     if (e != cudaSuccess) {
         set_error(std::string("sn_launch: ") + cudaGetErrorString(e));
         return GLU_ECUDA;
@@ -749,25 +777,36 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
     if (d->n_tasks > 0) {
         SnParams P;
         P.v = v;
-        P.col_ptr = col_ptr;
+        P.dblk = d->dblk;
         P.diag_pos = diag_pos;
         P.col_a = d->col_a;
-        P.fail_level = fail_level;
         P.pairs = d->pairs;
         P.tasks = d->tasks;
-        P.gdone = d->gdone;
+        P.panm = d->panm;
+        P.push = d->push;
+        P.pan = d->pan;
+        P.rg_slot = d->rg_slot;
+        P.rg_idx = d->rg_idx;
+        P.rg_uidx = d->rg_uidx;
         P.relmap = d->relmap;
-        P.phase_ptr = d->phase_ptr;
         P.n_tasks = (i32)d->n_tasks;
-        P.done = d->done;
+        P.cnt = d->cnt;
         P.cmax = d->cmax;
         P.err = err;
-        P.stamps = d->stamps;
         P.trace = d->trace;
         void *args[] = {&P};
         e = cudaLaunchCooperativeKernel((const void *)sn_kernel, dim3(d->grid), dim3(kSnThreads), args, kSnSmem, s);
         if (e != cudaSuccess) {
             set_error(std::string("sn_kernel: ") + cudaGetErrorString(e));
+            return GLU_ECUDA;
+        }
+    }
+    if (d->n_wb > 0) {
+        sn_writeback_kernel<<<(unsigned)std::min<i64>((d->n_wb + 7) / 8, 4736), 256, 0, s>>>(
+            v, d->dblk, d->wb, (i32)d->n_wb, diag_pos, d->col_a);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            set_error(std::string("sn_writeback_kernel: ") + cudaGetErrorString(e));
             return GLU_ECUDA;
         }
     }

@@ -164,10 +164,11 @@ class Factorizer:
                                        "tail_macs", "express_items"),
                                       info.tolist()))
             if engine == "sn":
-                sinfo = np.zeros(12, dtype=np.int64)
+                sinfo = np.zeros(16, dtype=np.int64)
                 _lib.lib.glu_sn_plan_info(plan, _lib.ptr(sinfo))
                 self.sn_info = dict(zip(("supernodes", "panels", "pairs", "map", "pushes", "tasks",
-                                         "phases", "stages", "macs", "plan_bytes"), sinfo[:10].tolist()))
+                                         "dblk", "crit_ns", "macs", "plan_bytes", "rg_tasks", "rg_slots",
+                                         "rg_macs", "rg_pairs"), sinfo[:14].tolist()))
                 self.plan_info.update(macs=self.sn_info["macs"], plan_bytes=self.sn_info["plan_bytes"])
             h = ctypes.c_void_p()
             rc = _lib.check(_lib.lib.glu_create(self.n, _lib.ptr(cp), _lib.ptr(ri), _lib.ptr(dp),

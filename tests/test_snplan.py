@@ -48,17 +48,19 @@ def _oracle_a(fp, a):
     return v, orc.factor_left_looking(pat, v, 1e-14)
 
 
-@pytest.mark.parametrize("k,drop", [(12, 0.0), (17, 0.1), (24, 0.0)])
-def test_sn_plan_grid_bitwise(k, drop):
+@pytest.mark.parametrize("k,drop,schedule", [(12, 0.0, "all"), (17, 0.1, "all"), (24, 0.0, "all"),
+                                             (12, 0.0, "serial"), (17, 0.1, "random"), (20, 0.0, "random")])
+def test_sn_plan_grid_bitwise(k, drop, schedule):
     """G3-like grids in nested-dissection order: wide supernodes, panels
-    split inside them, relative maps into outside columns."""
+    split inside them, relative maps into outside columns.  Every task
+    schedule the counters allow gives the reference's bits."""
     a = synthetic.grid5(k, drop=drop, seed=k)
     fp = glu.symbolic_fillin(a.pattern)
     plan = sn_emul.build(fp)
     assert plan["info"]["macs"] == glu.numeric.pattern_flops(fp)[0]
     ref, err = _oracle_a(fp, a)
     assert err == -1
-    v, fail = sn_emul.emulate(plan, fp, _scatter(fp, a))
+    v, fail = sn_emul.emulate(plan, fp, _scatter(fp, a), schedule=schedule, seed=k)
     assert fail == -1 and np.array_equal(v, ref)
 
 
@@ -85,6 +87,8 @@ def test_sn_plan_wide_supernode_panels():
     ref, err = _oracle_a(fp, a)
     out, fail = sn_emul.emulate(plan, fp, _scatter(fp, a))
     assert err == -1 and fail == -1 and np.array_equal(out, ref)
+    out, fail = sn_emul.emulate(plan, fp, _scatter(fp, a), schedule="random", seed=5)
+    assert fail == -1 and np.array_equal(out, ref)
 
 
 @pytest.mark.parametrize("seed,n,dens", [(21, 60, 0.05), (22, 150, 0.02)])

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import pathlib
 import sys
 import time
@@ -19,9 +20,11 @@ ROOT = pathlib.Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
-def phase_profile(fz, fp, a_d, v, st):
-    """Per-phase durations from the kernel's completion stamps, grouped by
-    the kind of tasks the phase holds (0 DIAG, 1 TRSM/TRI, 2 RECT)."""
+def task_profile(fz, fp, a_d, v, st):
+    """Per-task timestamps of one factorization ({start, source ready, target
+    ready, done}, glu_sn_trace): kernel span, the plan model's critical
+    path, and per kind / width class the execution time after the last wait
+    and the wait times."""
     import torch
 
     sys.path.insert(0, str(ROOT / "tests"))
@@ -29,74 +32,38 @@ def phase_profile(fz, fp, a_d, v, st):
     from paper_1908_00204_b200 import _lib
 
     plan = sn_emul.build(fp)
-    fz.set_option(15, 2)
+    tasks = plan["tasks"]
+    ntasks = len(tasks)
+    fz.set_option(15, 1)
     fz.scatter_device(a_d, v, st)
     fz.factor_device_async(v, 1e-14, st)
     torch.cuda.synchronize()
-    nph = len(plan["phase_ptr"]) - 1
-    buf = np.zeros(nph + 1, dtype=np.int64)
-    _lib.lib.glu_sn_stamps(fz.handle, _lib.ptr(buf), nph + 1)
-    ntasks = len(plan["tasks"])
     tr = np.zeros((ntasks, 4), dtype=np.int64)
     _lib.lib.glu_sn_trace(fz.handle, _lib.ptr(tr), ntasks)
     fz.set_option(15, 0)
-    dur = np.diff(buf).astype(np.float64) * 1e-3  # us
-    tasks, pp = plan["tasks"], plan["phase_ptr"]
-    kinds = np.array([int(tasks[pp[p], 0]) >> 28 for p in range(nph)])  # 0 trsm/tri/diag-ish, 1 rect
-    kinds = np.array([min(int(k), 1) + 1 for k in kinds])  # 1: phase led by TRSM/TRI, 2: RECT/DIAG
-    ntask = np.diff(pp)
-    out = {"total_us": float(dur.sum()), "phases": nph}
-    for k, name in ((0, "diag"), (1, "trsm_tri"), (2, "rect")):
-        d = dur[kinds == k]
-        if len(d):
-            out[name] = {"n": int(len(d)), "sum_us": float(d.sum()), "median_us": float(np.median(d)),
-                         "p90_us": float(np.percentile(d, 90)), "max_us": float(d.max()),
-                         "tasks_median": float(np.median(ntask[kinds == k]))}
-    # phases by task count
-    for lo, hi in ((1, 1), (2, 8), (9, 64), (65, 512), (513, 1 << 30)):
-        m = (ntask >= lo) & (ntask <= hi)
-        if m.any():
-            out[f"tasks_{lo}_{hi}"] = {"n": int(m.sum()), "sum_us": float(dur[m].sum()),
-                                       "median_us": float(np.median(dur[m]))}
-    # per phase: wake (previous phase complete -> first / last task past its
-    # wait), execution (longest task), flush (last task done -> phase complete)
-    ph_of = np.repeat(np.arange(nph), ntask)
-    t1, t2 = tr[:, 1].astype(np.float64), tr[:, 2].astype(np.float64)
-    first_wait = np.full(nph, np.inf)
-    last_wait = np.zeros(nph)
-    last_done = np.zeros(nph)
-    exec_max = np.zeros(nph)
-    np.minimum.at(first_wait, ph_of, t1)
-    np.maximum.at(last_wait, ph_of, t1)
-    np.maximum.at(last_done, ph_of, t2)
-    np.maximum.at(exec_max, ph_of, t2 - t1)
-    prev = buf[:-1].astype(np.float64)
-    comp = {"wake_first_us": (first_wait - prev) * 1e-3, "wake_last_us": (last_wait - prev) * 1e-3,
-            "exec_max_us": exec_max * 1e-3, "flush_us": (buf[1:] - last_done) * 1e-3}
-    for k, x in comp.items():
-        out[k] = {"sum": float(x.sum()), "median": float(np.median(x)), "p90": float(np.percentile(x, 90))}
-    kinds_t = (tasks[:, 0] >> 28)  # (kind << 27) >> 28 = kind index
-    for k, name in ((0, "diag"), (1, "trsm"), (2, "tri"), (3, "rect")):
-        m = kinds_t == k
-        if m.any():
-            d = (t2[m] - t1[m]) * 1e-3
-            out[f"task_{name}_us"] = {"n": int(m.sum()), "median": float(np.median(d)),
-                                     "p90": float(np.percentile(d, 90)), "max": float(d.max())}
-    wd = tasks[:, 3] - tasks[:, 2]
-    wcls = np.select([wd <= 1, wd <= 2, wd <= 4, wd <= 8, wd <= 16], [1, 2, 4, 8, 16], 32)
-    npair = tasks[:, 7] - tasks[:, 6]
+    t0 = tr[:, 0].min()
+    if os.environ.get("SN_TRACE_DUMP"):
+        np.savez_compressed(os.environ["SN_TRACE_DUMP"], trace=((tr - t0) // 10).astype(np.int32))
+    tr = (tr - t0).astype(np.float64) * 1e-3  # us from kernel start
+    kind = (tasks[:, 0] >> 27) >> 2
+    w = tasks[:, 3] - tasks[:, 2]
+    wcls = np.select([w <= 1, w <= 2, w <= 4, w <= 8], [1, 2, 4, 8], 16)
+    out = {"span_us": float(tr[:, 3].max()), "model_crit_us": plan["info"]["crit_ns"] * 1e-3, "tasks": ntasks}
+    execd = tr[:, 3] - tr[:, 2]
+    wait_src = tr[:, 1] - tr[:, 0]
+    wait_tgt = tr[:, 2] - tr[:, 1]
     by = {}
-    for k, name in ((0, "diag"), (1, "trsm"), (2, "tri"), (3, "rect")):
-        for wc in (1, 2, 4, 8, 16, 32):
-            m = (kinds_t == k) & (wcls == wc)
+    for k, name in ((0, "trsm"), (1, "rect"), (2, "uw")):
+        for wc in (1, 2, 4, 8, 16):
+            m = (kind == k) & (wcls == wc)
             if m.any():
-                d = (t2[m] - t1[m]) * 1e-3
-                by[f"{name}{wc}"] = [int(m.sum()), round(float(np.median(d)), 2),
-                                     round(float(np.percentile(d, 90)), 2), round(float(d.max()), 2),
-                                     round(float(npair[m].mean()), 1)]
-    out["by_kind_width[n,med,p90,max,npair]"] = by
-    top = np.argsort(dur)[::-1][:8]
-    out["top"] = [(int(p), int(kinds[p]), int(ntask[p]), round(float(dur[p]), 1)) for p in top]
+                by[f"{name}{wc}"] = [int(m.sum()), round(float(np.median(execd[m])), 2),
+                                     round(float(np.percentile(execd[m], 90)), 2),
+                                     round(float(np.median(wait_src[m])), 2), round(float(np.median(wait_tgt[m])), 2)]
+    out["by_kind_width[n,exec_med,exec_p90,wait_src_med,wait_tgt_med]"] = by
+    # busy fraction: sum of (done - start) over all warps / (warps x span)
+    out["sum_exec_ms"] = float(execd.sum() * 1e-3)
+    out["sum_wait_ms"] = float((tr[:, 2] - tr[:, 0]).sum() * 1e-3)
     return out
 
 
@@ -106,7 +73,7 @@ def main():
     p.add_argument("--engines", default="sn,plan")
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--no-parity", action="store_true")
-    p.add_argument("--stamps", action="store_true", help="per-phase completion profile (sn)")
+    p.add_argument("--stamps", action="store_true", help="per-task trace profile (sn)")
     args = p.parse_args()
     import torch
 
@@ -161,7 +128,7 @@ def main():
             out = v.cpu().numpy()
             prof = None
             if args.stamps and eng == "sn":
-                prof = phase_profile(fz, fp, a_d, v, st)
+                prof = task_profile(fz, fp, a_d, v, st)
             par = None
             if ref is not None:
                 par = "bitwise" if np.array_equal(out, ref) else \
@@ -170,7 +137,7 @@ def main():
                        setup_s=round(t_setup, 2), ms=min(ts), ms_all=[round(x, 3) for x in ts],
                        parity=par, plan=fz.plan_info.get("plan_bytes"),
                        sn=getattr(fz, "sn_info", None), device_bytes=fz.handle_info["device_bytes"],
-                       ref_s=round(t_ref, 2) if ref is not None else None, phases=prof)
+                       ref_s=round(t_ref, 2) if ref is not None else None, profile=prof)
             print(json.dumps(rec), flush=True)
             fz.close()
             del v, a_d
