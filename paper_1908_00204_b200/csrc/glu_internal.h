@@ -76,6 +76,7 @@ constexpr int kSnW = 16;  // panel width: one warp lane per panel column / row
 constexpr int kRgPushes = 16;   // pushes per RG task
 constexpr int kRgSlots = 512;   // distinct slots (targets and multipliers U(p0, k))
 constexpr int kRgIdx = 2048;    // MAC indices (u16)
+constexpr int kRgRows = 512;    // L rows (a push has at most kRgRows / 4 rows below its column)
 
 struct alignas(16) I4 {
     int32_t x, y, z, w;
@@ -104,7 +105,7 @@ struct SnPlan {
     std::vector<int32_t> push_need;  // per push: RECT chunks of earlier pushes into its target
     // 3 records per task, in a topological (as-soon-as-possible) order:
     //   {code << 27 | chunk, source panel P, p0, p1}, {s1, rows below p1, pair0, pair1},
-    //   {target panel K, need, 0, 0}; RG: {code << 27 | pushes, first MAC index, first U index, 0},
+    //   {target panel K, need, 0, 0}; RG: {code << 27 | pushes, first MAC index, first U index, chunks},
     //   {first slot, slots, first push, pushes}, {K, need, 0, 0}
     std::vector<I4> tasks;
     std::vector<int32_t> col_a;      // per column c: first row of c's supernode present in c
@@ -113,6 +114,7 @@ struct SnPlan {
     // (push, pair q, row t at q * h + t) the index of its target in that
     // list; per (push, pair) the index of U(p0, k)
     std::vector<I4> rg;
+    std::vector<int32_t> rg_chunks;  // per RG: RECT chunks its pushes count for
     std::vector<int32_t> rg_slot;
     std::vector<uint16_t> rg_idx, rg_uidx;
     int64_t n_dblk = 0;              // doubles of factored-diagonal-block scratch (panels w >= 2)
@@ -156,6 +158,7 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
 void sn_free(SnDev *d);
 int sn_grid(int sm_count);
 int64_t sn_set_trace(SnDev *d, int mode);
+int64_t sn_set_assign(SnDev *d, int dynamic);  // task assignment: 1 ticket counter (default), 0 static
 int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks);
 // one factorization of v (A_s values after the scatter); pivot failures
 // are min-reduced into *fail as (fail_level << 32 | column) or column

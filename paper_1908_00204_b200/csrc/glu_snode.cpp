@@ -314,9 +314,11 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         return GLU_EINVAL;
     }
     P->n_dblk = dbl;
-    constexpr double kHop = 1.0;                 // us: release -> observe
+    // latency model (us), calibrated on the B200 traces (tools/sn_critpath.py)
+    constexpr double kHop = 2.5;                 // release -> observe
     constexpr double kMacsPerUs = 4000.0;        // one warp's FP64 chain rate
-    constexpr double kGatherSrcUs = 0.3;         // one push inside an RG (shared-memory chains)
+    constexpr double kGatherSrcUs = 0.15;        // one push inside an RG (shared-memory chains)
+    constexpr double kGatherUs = 3.0;            // an RG's staging loads
     constexpr i64 kMaxGather = kRgPushes;        // pushes per RG task (one per lane)
     constexpr i64 kMinGather = 3;                // shorter runs stay RECT tasks (their slots load before the waits)
     std::vector<double> f_done(np, 0.0), f_start(np, 0.0);
@@ -344,6 +346,7 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         i64 g_first = -1, g_cnt = 0;
         double g_key = 0.0, g_cost = 0.0, g_t0 = 0.0;
         size_t g_idx0 = 0, g_uidx0 = 0;
+        i64 g_rows = 0, g_chunks = 0;  // the open RG's L rows and RECT chunks
         auto slot_of = [&](const I4 &pr, i64 tr) -> i64 {  // row tr below a one-column source, pair pr
             return pr.w >= 0 ? (i64)P->relmap[pr.w + tr] : (i64)pr.z + tr;
         };
@@ -352,6 +355,7 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
                 const i32 r = (i32)P->rg.size();
                 P->rg.push_back(I4{(i32)P->rg_slot.size(), (i32)cur_slots.size(), (i32)g_idx0, (i32)g_uidx0});
                 P->rg_slot.insert(P->rg_slot.end(), cur_slots.begin(), cur_slots.end());
+                P->rg_chunks.push_back((i32)g_chunks);
                 all.push_back({g_key, g_cost, kSnRg << 2, r, (i32)g_cnt, (i32)g_first});
             } else if (g_cnt > 0) {
                 // too short: one RECT task per push, chained as usual
@@ -360,9 +364,10 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
                 double tt = g_t0;
                 for (i64 y = g_first; y < g_first + g_cnt; y++) {
                     const i32 src = P->push[y].x;
+                    const i64 nch = chunks(P->pan[src].w);
                     const double st = std::max(tt, f_done[src]) + kHop;
-                    const double per = 1.5 + (double)push_macs[y] / kMacsPerUs;
-                    all.push_back({st, per, kSnRect << 2, src, 0, (i32)y});
+                    const double per = 2.5 + (double)push_macs[y] / (double)nch / kMacsPerUs;
+                    for (i64 c = 0; c < nch; c++) all.push_back({st, per, kSnRect << 2, src, (i32)c, (i32)y});
                     tt = st + per;
                 }
                 t = std::max(t, tt);
@@ -374,9 +379,10 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
             const I4 pn = P->pan[ps.x];
             const i64 w = pn.y - pn.x, npair = ps.z - ps.y, nc = chunks(pn.w);
             P->push_need.push_back((i32)need);
-            if (w == 1 && nc == 1) {
+            const i64 hh = pn.w;
+            if (w == 1 && hh <= kRgRows / 4 && npair * hh <= kRgIdx && npair * (hh + 1) <= kRgSlots) {
                 const double ready = f_done[ps.x];
-                const i64 h = pn.w;
+                const i64 h = hh;
                 // new distinct slots (targets and U(p0, k)) this push would add to the
                 // open RG, and its MAC indices (pair q, row tr at q * h + tr)
                 i64 fresh = 0;
@@ -388,20 +394,23 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
                         for (i64 tr = 0; tr < h; tr++)
                             if (mark_gen[slot_of(pr, tr) - kbase] != gen) fresh++;
                     }
-                if (!(g_cnt > 0 && g_cnt < kMaxGather && ready <= t + kHop &&
+                // (a late source does not split the run: the pushes into K run in
+                // order anyway, so the ones after it wait for it either way)
+                if (!(g_cnt > 0 && g_cnt < kMaxGather && g_rows + h <= kRgRows &&
                       (i64)cur_slots.size() + fresh <= kRgSlots &&
                       (i64)(P->rg_idx.size() - g_idx0) + npair * h <= kRgIdx &&
                       (i64)(P->rg_uidx.size() - g_uidx0) + npair <= kRgPushes * kSnW)) {
                     close_g();
                     g_first = x;
                     g_t0 = t;
-                    t = std::max(t, ready) + kHop;
-                    g_key = t;
-                    g_cost = 0.0;
+                    t = std::max(t, ready) + kHop + kGatherUs;
+                    g_key = t - kGatherUs;
+                    g_cost = kGatherUs;
                     gen++;
                     cur_slots.clear();
                     g_idx0 = P->rg_idx.size();
                     g_uidx0 = P->rg_uidx.size();
+                    g_rows = g_chunks = 0;
                 }
                 // the push's MACs as indices into the RG's slot list (pair q, row tr
                 // at q * h + tr), and per pair the index of U(p0, k)
@@ -425,12 +434,14 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
                 t = std::max(t, ready) + kGatherSrcUs;
                 g_cost += kGatherSrcUs;
                 g_cnt++;
-                need += 1;
+                g_rows += h;
+                g_chunks += nc;
+                need += nc;
                 continue;
             }
             close_g();
             const double st = std::max(t, f_done[ps.x]) + kHop;
-            const double per = 1.5 + (double)push_macs[x] / (double)nc / kMacsPerUs +
+            const double per = 2.5 + (double)push_macs[x] / (double)nc / kMacsPerUs +
                                (push_tri[x] ? 0.05 * (double)(w * w) : 0.0);
             const bool uw = push_tri[x] && nc > 1;
             const i32 flags = (push_tri[x] ? kSnTriF : 0) | (push_tri[x] && !uw ? kSnWriteU : 0);
@@ -445,7 +456,7 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         const I4 pn = P->pan[K];
         const i64 w = pn.y - pn.x, nc = chunks(pn.w);
         const double st = (need > 0 ? t + kHop : 0.0);
-        const double cost = 2.0 + 0.15 * (double)w + (double)(32 * w * w / 2) / kMacsPerUs;
+        const double cost = 0.5 + 1.2 * (double)w + (double)(32 * w * w / 2) / kMacsPerUs;
         for (i64 c = 0; c < nc; c++) all.push_back({st, cost, kSnTrsm << 2, (i32)K, (i32)c, -1});
         f_start[K] = st;
         f_done[K] = st + cost;
@@ -469,11 +480,11 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         for (i64 i = b; i < e; i++) {
             const T &t = all[i];
             if (t.kind == (kSnRg << 2)) {
-                // {code << 27 | pushes, first MAC index, first U index, 0}, {first slot, slots,
+                // {code << 27 | pushes, first MAC index, first U index, RECT chunks}, {first slot, slots,
                 // first push, pushes}, {K, need, 0, 0}
                 const I4 g = P->rg[t.pi];
                 const I4 ps = P->push[t.x];
-                P->tasks[3 * i] = I4{(t.kind << 27) | t.chunk, g.z, g.w, 0};
+                P->tasks[3 * i] = I4{(t.kind << 27) | t.chunk, g.z, g.w, P->rg_chunks[t.pi]};
                 P->tasks[3 * i + 1] = I4{g.x, g.y, t.x, t.chunk};
                 P->tasks[3 * i + 2] = I4{ps.w, P->push_need[t.x], 0, 0};
                 continue;

@@ -142,7 +142,7 @@ def _signal(d, i):
     if k == RECT:
         return (0, int(d["K"][i]), 1)
     if k == RG:
-        return (0, int(d["K"][i]), int(d["r1"][i]))
+        return (0, int(d["K"][i]), int(d["p1"][i]))  # ta.w: the RECT chunks of its pushes
     return None
 
 
@@ -221,6 +221,7 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None, schedule="all", seed=0):
             P, r0, r1, _K = (int(y) for y in plan["push"][x])
             p0, p1, _S, h = (int(y) for y in plan["pan"][P])
             s1 = p1  # a one-column panel is a one-column supernode
+            assert h <= 128
             L = [E.rd(int(dp[p0]) + 1 + t) for t in range(h)]
             for q in range(r0, r1):
                 k, a, base, mp = (int(y) for y in pairs[q])

@@ -50,7 +50,7 @@ def main():
     for cnt, sel, key in ((0, kind == 1, K), (1, kind == 0, P)):
         idx = np.flatnonzero(sel)
         if cnt == 0 and len(rgi):
-            idx = np.concatenate([idx, np.repeat(rgi, d["r1"][rgi])])
+            idx = np.concatenate([idx, np.repeat(rgi, d["p1"][rgi])])  # ta.w = RECT chunks
         order = np.lexsort((done[idx], key[idx]))
         idx = idx[order]
         keys = key[idx]
@@ -62,15 +62,17 @@ def main():
         idx, starts = comp[cnt]
         return int(idx[starts[panel] + k - 1])
 
-    nw = args.grid * 8
-    warp_of = (np.arange(n) % args.grid) * 8 + (np.arange(n) // args.grid) % 8
+    z = np.load(args.trace)
+    if "warp" in z:
+        warp_of = z["warp"]
+    else:  # static deal
+        warp_of = (np.arange(n) % args.grid) * 8 + (np.arange(n) // args.grid) % 8
     prev_on_warp = np.full(n, -1)
     last = {}
-    for i in range(n):
-        wv = warp_of[i]
+    for i in np.argsort(tr[:, 0], kind="stable"):  # each warp's tasks in the order it ran them
+        wv = int(warp_of[i])
         prev_on_warp[i] = last.get(wv, -1)
         last[wv] = i
-    del nw
 
     def deps(i):
         k = int(kind[i])
@@ -80,27 +82,31 @@ def main():
             return [(1, int(P[i]), int(panm[P[i], 1])), (0, int(K[i]), int(need[i]))]
         if k == 3:  # RG: the target, then each push's source panel
             x0, c = int(d["r0"][i]), int(d["r1"][i])
-            return [(0, int(K[i]), int(need[i]))] + [(1, int(plan["push"][x, 0]), 1) for x in range(x0, x0 + c)]
+            return [(0, int(K[i]), int(need[i]))] + [(1, int(plan["push"][x, 0]), int(panm[plan["push"][x, 0], 1]))
+                                                     for x in range(x0, x0 + c)]
         return [(0, int(K[i]), int(need[i]) + int(panm[P[i], 1]))]
 
     i = int(np.argmax(done))
     path = []
     ex = hop = busy = 0.0
     kinds = np.zeros(4)
+    links = {}
     while i >= 0:
-        best, bt = -1, -1.0
+        best, bt, bc = -1, -1.0, -1
         for c, p_, k in deps(i):
             if k <= 0:
                 continue
             j = nth(c, p_, k)
             if done[j] > bt:
-                best, bt = j, done[j]
+                best, bt, bc = j, done[j], c
         pw = int(prev_on_warp[i])
         pw_done = done[pw] if pw >= 0 else 0.0
         ready = tr[i, 2]
         ex += done[i] - ready
         kinds[int(kind[i])] += done[i] - ready
         if best >= 0 and bt >= pw_done:
+            lk = ("tgt" if bc == 0 else "src", int(kind[i]), int(kind[best]))
+            links[lk] = links.get(lk, 0) + 1
             hop += ready - bt
             path.append((i, "dep", ready - bt))
             i = best
@@ -123,10 +129,13 @@ def main():
     print(f"  execution per task on the path: median {np.median(exs):.2f} us, p90 {np.percentile(exs, 90):.2f}")
     nb = sum(1 for x in path if x[1] == "warp")
     print(f"  warp-busy links: {nb}")
+    names = {0: "TRSM", 1: "RECT", 2: "UW", 3: "RG"}
+    print("  dependency links (waited on, task <- predecessor):",
+          ", ".join(f"{a} {names[b]}<-{names[c]}: {v}" for (a, b, c), v in sorted(links.items(), key=lambda z: -z[1])))
     for kk, nm in ((0, "TRSM"), (1, "RECT"), (2, "UW"), (3, "RG")):
         m = [x for x in path if kind[x[0]] == kk]
         if m:
-            ww = np.array([w[x[0]] for x in m])
+            ww = np.array([max(int(w[x[0]]), 1) for x in m])
             print(f"  {nm}: {len(m)} on the path, widths {np.bincount(np.minimum(ww, 16))[1:].tolist()}")
 
 

@@ -38,12 +38,16 @@ def task_profile(fz, fp, a_d, v, st):
     fz.scatter_device(a_d, v, st)
     fz.factor_device_async(v, 1e-14, st)
     torch.cuda.synchronize()
-    tr = np.zeros((ntasks, 4), dtype=np.int64)
+    tr = np.zeros((ntasks, 6), dtype=np.int64)
     _lib.lib.glu_sn_trace(fz.handle, _lib.ptr(tr), ntasks)
     fz.set_option(15, 0)
+    warp = tr[:, 4].copy()
+    clk = tr[:, 5].copy()
+    tr = tr[:, :4]
     t0 = tr[:, 0].min()
     if os.environ.get("SN_TRACE_DUMP"):
-        np.savez_compressed(os.environ["SN_TRACE_DUMP"], trace=((tr - t0) // 10).astype(np.int32))
+        np.savez_compressed(os.environ["SN_TRACE_DUMP"], trace=((tr - t0) // 10).astype(np.int32),
+                            warp=warp.astype(np.int32), clk=clk)
     tr = (tr - t0).astype(np.float64) * 1e-3  # us from kernel start
     kind = (tasks[:, 0] >> 27) >> 2
     w = tasks[:, 3] - tasks[:, 2]
@@ -61,6 +65,10 @@ def task_profile(fz, fp, a_d, v, st):
                                      round(float(np.percentile(execd[m], 90)), 2),
                                      round(float(np.median(wait_src[m])), 2), round(float(np.median(wait_tgt[m])), 2)]
     out["by_kind_width[n,exec_med,exec_p90,wait_src_med,wait_tgt_med]"] = by
+    m = (kind == 0) & (w >= 9)
+    if m.any():  # TRSM phase cycles (loads, block, rows)
+        c = clk[m]
+        out["trsm_wide_cycles_med[loads,block,rows]"] = [int(np.median((c >> s) & ((1 << 21) - 1))) for s in (0, 21, 42)]
     # busy fraction: sum of (done - start) over all warps / (warps x span)
     out["sum_exec_ms"] = float(execd.sum() * 1e-3)
     out["sum_wait_ms"] = float((tr[:, 2] - tr[:, 0]).sum() * 1e-3)
@@ -110,6 +118,8 @@ def main():
             fz.set_input(a.col_ptr, a.row_idx)
             fz.set_option(1, 0)
             fz.set_option(2, 1)
+            if eng == "sn" and "SN_ASSIGN" in os.environ:
+                fz.set_option(16, int(os.environ["SN_ASSIGN"]))
             a_d = torch.from_numpy(a.values).to(dev)
             v = torch.empty(fp.nnz, dtype=torch.float64, device=dev)
             st = torch.cuda.current_stream()
