@@ -158,7 +158,7 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
 void sn_free(SnDev *d);
 int sn_grid(int sm_count);
 int64_t sn_set_trace(SnDev *d, int mode);
-int64_t sn_set_assign(SnDev *d, int dynamic);  // task assignment: 1 ticket counter (default), 0 static
+int64_t sn_set_assign(SnDev *d, int mode);  // task assignment: 0 static, 1 tickets two ahead, 2 greedy tickets
 int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks);
 // one factorization of v (A_s values after the scatter); pivot failures
 // are min-reduced into *fail as (fail_level << 32 | column) or column

@@ -72,6 +72,7 @@ struct SnParams {
     int *err;
     unsigned long long *trace;  // optional: per task kTraceWords words
     unsigned *ticket;           // dynamic task assignment (null: static)
+    int greedy;                 // dynamic: hold no ticket beyond the one taken during a task
 };
 
 __device__ __forceinline__ double ldv(const double *p) { return __ldcg(p); }
@@ -227,6 +228,7 @@ __device__ void task_trsm(const SnParams &P, TrsmSmem &S, int4 ta, int4 tb, int4
     const int t = chunk * 32 + lane;
     const bool act = t < h;
     // the block and the rows, copied straight to shared memory (all in flight at once)
+#pragma unroll 1
     for (int c = 0; c < w; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
         cp_async8(&S.b[c][lane], P.v + dc + (lane - c), lane < w && lane >= clo, P.v);
@@ -269,6 +271,8 @@ __device__ void task_trsm(const SnParams &P, TrsmSmem &S, int4 ta, int4 tb, int4
             for (int c = 0; c < w; c++) stv(P.dblk + pm.z + c * w + lane, S.b[c][lane]);
         if (inb && bmax) atomicMax(P.cmax + p0 + lane, bmax);
     }
+    // the rows (a register version, steps unrolled over the class width,
+    // measured 4x slower: 16 inlined divisions with their slow-path calls)
     unsigned long long mymax = 0;
     for (int j = 0; j < w; j++) {
         const unsigned has = __ballot_sync(0xffffffffu, clol <= j);
@@ -370,20 +374,40 @@ __device__ __forceinline__ void load_u_tile(const SnParams &P, RectSmem &R, int4
                                             int p0, int w, int s1, int lane) {
     if (lane < kSnW) {
         R.lo[lane] = mylo;
+#pragma unroll 1
         for (int j = 0; j < w; j++)
             cp_async8(&R.u[j][lane], P.v + myp.z - (s1 - (p0 + j)), colok && j >= mylo, P.v);
     }
 }
 // The forward substitution U(r, k) -= L(r, j) * U(j, k), j ascending.
 __device__ __forceinline__ void solve_u_tile(RectSmem &R, bool colok, int mylo, int w, int lane) {
-    if (lane < kSnW && colok) {
-        for (int j = mylo; j < w - 1; j++) {
-            const double uj = R.u[j][lane];
-            for (int r = j + 1; r < w; r++) R.u[r][lane] = msub(R.u[r][lane], R.lb[j][r], uj);
+    // lane q < 16 holds column q in registers (a shared-memory chain would
+    // serialize every step behind the previous store: ~10k cycles for w = 16);
+    // the steps are unrolled over the class width, selects keep absent
+    // U(j, k) (j < lo) out and rows >= w are never stored
+    const int q = lane & (kSnW - 1);  // lanes 16-31 shadow lanes 0-15 and store nothing
+    const bool act = lane < kSnW && colok;
+    double u[kSnW];
+#pragma unroll
+    for (int r = 0; r < kSnW; r++) u[r] = R.u[r][q];
+#pragma unroll
+    for (int j = 0; j < kSnW - 1; j++) {
+        const double uj = u[j];
+        const bool on = j >= mylo && j < w - 1;
+#pragma unroll
+        for (int r = j + 1; r < kSnW; r++) {
+            const double y = msub(u[r], R.lb[j][r], uj);
+            u[r] = on ? y : u[r];
         }
+    }
+    __syncwarp();
+    if (act) {
+#pragma unroll
+        for (int r = 0; r < kSnW; r++) R.u[r][q] = u[r];
     }
 }
 __device__ __forceinline__ void load_lb(const SnParams &P, RectSmem &R, int off, int w, int lane) {
+#pragma unroll 1
     for (int e = lane; e < w * w; e += 32) {
         const int j = e / w, r = e - j * w;
         cp_async8(&R.lb[j][r], P.dblk + off + e, true, P.v);
@@ -427,6 +451,7 @@ __device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4
     }
     if (!wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
     if (tr && lane == 0) tr[1] = globaltimer();
+#pragma unroll 1
     for (int j = 0; j < w; j++) {
         const int dj = __shfl_sync(0xffffffffu, dcl, j);
         cp_async8(&R.l[j][lane], P.v + dj + (w - j) + t, t < h, P.v);
@@ -435,6 +460,7 @@ __device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4
     if (tri) load_lb(P, R, pm.z, w, lane);
     if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
     if (tr && lane == 0) tr[2] = globaltimer();
+    const long long c0 = clock64();
     load_u_tile(P, R, myp, colok, mylo, p0, w, s1, lane);
     const bool anylo = __any_sync(0xffffffffu, colok && mylo > 0);
     double c[4][4];
@@ -444,27 +470,44 @@ __device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4
         for (int i = 0; i < 4; i++) c[i][k] = pos[i][k] >= 0 ? ldv(P.v + pos[i][k]) : 0.0;
     cp_async_wait();  // L rows, the factored block, U(P, K)
     __syncwarp();
+    const long long c1 = clock64();
     if (tri) {
         solve_u_tile(R, colok, mylo, w, lane);
         __syncwarp();
     }
-    int clo[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) clo[k] = anylo ? R.lo[cx + 4 * k] : 0;
+    const long long c2 = clock64();
+    if (!anylo) {  // every column's U suffix starts at the panel: no selects
 #pragma unroll 2
-    for (int j = 0; j < w; j++) {
-        double l[4], u[4];
+        for (int j = 0; j < w; j++) {
+            double l[4], u[4];
 #pragma unroll
-        for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
+            for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
 #pragma unroll
-        for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
+            for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
 #pragma unroll
-        for (int i = 0; i < 4; i++)
+            for (int i = 0; i < 4; i++)
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const double y = msub(c[i][k], l[i], u[k]);
-                c[i][k] = j >= clo[k] ? y : c[i][k];
-            }
+                for (int k = 0; k < 4; k++) c[i][k] = msub(c[i][k], l[i], u[k]);
+        }
+    } else {
+        int clo[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) clo[k] = R.lo[cx + 4 * k];
+#pragma unroll 1
+        for (int j = 0; j < w; j++) {
+            double l[4], u[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) l[i] = R.l[j][ry + 8 * i];
+#pragma unroll
+            for (int k = 0; k < 4; k++) u[k] = R.u[j][cx + 4 * k];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const double y = msub(c[i][k], l[i], u[k]);
+                    c[i][k] = j >= clo[k] ? y : c[i][k];
+                }
+        }
     }
 #pragma unroll
     for (int k = 0; k < 4; k++)
@@ -474,6 +517,11 @@ __device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4
     if ((code & kSnWriteU) && lane < kSnW && colok)
         for (int r = mylo + 1; r < w; r++) stv(P.v + myp.z - (s1 - (p0 + r)), R.u[r][lane]);
     __syncwarp();
+    if (tr && lane == 0) {  // diagnostics: SM cycles of the loads, the U solve, the MACs + stores
+        const long long c3 = clock64();
+        auto f = [](long long x) { return (unsigned long long)min(max(x, 0ll), (1ll << 21) - 1); };
+        tr[5] = f(c1 - c0) | f(c2 - c1) << 21 | f(c3 - c2) << 42;
+    }
     return true;
 }
 
@@ -573,13 +621,13 @@ __device__ bool task_rg(const SnParams &P, RgSmem &G, int4 ta, int4 tb, int4 tc,
             continue;
         }
         __syncwarp();
-        {  // their L rows, loaded together: flat rows [loff(done), loff(e))
+        {  // their L rows, copied together: flat rows [loff(done), loff(e))
             const int r0 = __shfl_sync(0xffffffffu, loff, done);
             const int r1 = __shfl_sync(0xffffffffu, loff + hl, e - 1);
-            double Lr[kRgRows / 32];
-#pragma unroll
-            for (int j = 0; j < kRgRows / 32; j++) {
-                const int r = r0 + lane + 32 * j;
+            const int nit = (r1 - r0 + 31) >> 5;  // the same trip count on every lane (shuffles inside)
+#pragma unroll 1
+            for (int it = 0; it < nit; it++) {
+                const int r = r0 + lane + 32 * it;
                 // the push holding flat row r: the last push k < e with loff(k) <= r
                 int k = done;
 #pragma unroll
@@ -589,11 +637,9 @@ __device__ bool task_rg(const SnParams &P, RgSmem &G, int4 ta, int4 tb, int4 tc,
                     if (c < e && lc <= r) k = c;
                 }
                 const int lk = __shfl_sync(0xffffffffu, loff, k), dk = __shfl_sync(0xffffffffu, dcl, k);
-                Lr[j] = r < r1 ? ldv(P.v + dk + 1 + (r - lk)) : 0.0;
+                if (r < r1) cp_async8(&G.L[r], P.v + dk + 1 + (r - lk), true, P.v);
             }
-#pragma unroll
-            for (int j = 0; j < kRgRows / 32; j++)
-                if (r0 + lane + 32 * j < r1) G.L[r0 + lane + 32 * j] = Lr[j];
+            cp_async_wait();
         }
         __syncwarp();
         for (int k = done; k < e; k++) {
@@ -662,6 +708,26 @@ __global__ void __launch_bounds__(kSnThreads, 2) sn_kernel(SnParams P) {
         if (lane == 0) t = (int)atomicAdd(P.ticket, 1u);
         return __shfl_sync(0xffffffffu, t, 0);
     };
+    if (P.greedy) {
+        // greedy list scheduling: the next ticket is taken while this task runs
+        // and nothing else is reserved -- a ready task waits only for a free warp
+        int i = take();
+        while (i < P.n_tasks) {
+            const int4 ta = __ldg(P.tasks + 3 * (size_t)i), tb = __ldg(P.tasks + 3 * (size_t)i + 1),
+                       tc = __ldg(P.tasks + 3 * (size_t)i + 2);
+            int k = 0;
+            if (lane == 0) k = (int)atomicAdd(P.ticket, 1u);
+            unsigned long long *tr = P.trace ? P.trace + kTraceWords * (size_t)i : nullptr;
+            if (tr && lane == 0) {
+                tr[0] = globaltimer();
+                tr[4] = blockIdx.x * kSnWarps + wib;
+            }
+            if (!run_task(P, S, ta, tb, tc, lane, tr)) return;
+            if (tr && lane == 0) tr[3] = globaltimer();
+            i = __shfl_sync(0xffffffffu, k, 0);
+        }
+        return;
+    }
     int i = dyn ? take() : wib * gridDim.x + blockIdx.x;
     int j = dyn ? take() : i + nw;  // the next task
     int4 ta = make_int4(0, 0, 0, 0), tb = ta, tc = ta;
@@ -766,7 +832,7 @@ struct SnDev {
     unsigned long long *cmax = nullptr;
     unsigned long long *trace = nullptr;  // per-task timestamps (diagnostics)
     int grid = 0;
-    bool dynamic = false;  // task assignment (sn_set_assign): static measured faster (g400 8.8 vs 11.0 ms)
+    int assign = 0;  // task assignment (sn_set_assign): 0 static, 1 dynamic two ahead, 2 greedy
 };
 
 constexpr size_t kSnSmem = sizeof(WarpSmem) * kSnWarps;
@@ -855,8 +921,8 @@ int64_t sn_set_trace(SnDev *d, int mode) {
     return GLU_OK;
 }
 
-int64_t sn_set_assign(SnDev *d, int dynamic) {
-    d->dynamic = dynamic != 0;
+int64_t sn_set_assign(SnDev *d, int mode) {
+    d->assign = std::max(0, std::min(mode, 2));
     return GLU_OK;
 }
 
@@ -900,7 +966,8 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         P.cmax = d->cmax;
         P.err = err;
         P.trace = d->trace;
-        P.ticket = d->dynamic ? d->cnt + 2 * d->n_pan : nullptr;
+        P.ticket = d->assign ? d->cnt + 2 * d->n_pan : nullptr;
+        P.greedy = d->assign == 2;
         void *args[] = {&P};
         e = cudaLaunchCooperativeKernel((const void *)sn_kernel, dim3(d->grid), dim3(kSnThreads), args, kSnSmem, s);
         if (e != cudaSuccess) {

@@ -69,6 +69,10 @@ def task_profile(fz, fp, a_d, v, st):
     if m.any():  # TRSM phase cycles (loads, block, rows)
         c = clk[m]
         out["trsm_wide_cycles_med[loads,block,rows]"] = [int(np.median((c >> s) & ((1 << 21) - 1))) for s in (0, 21, 42)]
+    m = (kind == 1) & (w >= 9)
+    if m.any():  # RECT phase cycles after the target wait (loads, U solve, MACs + stores)
+        c = clk[m]
+        out["rect_wide_cycles_med[loads,usolve,macs]"] = [int(np.median((c >> s) & ((1 << 21) - 1))) for s in (0, 21, 42)]
     # busy fraction: sum of (done - start) over all warps / (warps x span)
     out["sum_exec_ms"] = float(execd.sum() * 1e-3)
     out["sum_wait_ms"] = float((tr[:, 2] - tr[:, 0]).sum() * 1e-3)
