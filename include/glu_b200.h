@@ -210,8 +210,7 @@ int64_t glu_set_fail_levels(glu_handle *h, const int64_t *level_of);
 /* Diagnostics of the supernodal engine: glu_set_option(h, 15, 1) records,
    per task of the next factorization, 6 words {start, source ready, target
    ready, done (%globaltimer ns), warp, 0}; read with glu_sn_trace (returns
-   the tasks written, 0 for a per-MAC handle).  glu_set_option(h, 16, 0|1):
-   static (default) / dynamic task assignment. */
+   the tasks written, 0 for a per-MAC handle). */
 int64_t glu_sn_trace(glu_handle *h, int64_t *out, int64_t max_tasks);
 /* Diagnostics: glu_set_option(h, 3, first_phase) and (h, 4, n_phases)
    record, for every item of those phases, 8 words {item | phase << 32,

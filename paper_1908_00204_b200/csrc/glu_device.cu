@@ -2365,9 +2365,6 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
         case 15:  // diagnostics: supernodal engine per-task timestamps (glu_sn_trace)
             if (!h->sn) { glu::set_error("option 15 needs a supernodal handle"); return GLU_EINVAL; }
             return glu::sn_set_trace(h->sn, (int)value);
-        case 16:  // tuning: supernodal task assignment, 0 static (default), 1 tickets two ahead, 2 greedy tickets
-            if (!h->sn) { glu::set_error("option 16 needs a supernodal handle"); return GLU_EINVAL; }
-            return glu::sn_set_assign(h->sn, (int)value);
         case 2:  // failing-pivot order: 0 level-major (factor_parallel), 1 column (sequential paths)
             h->fail_by_column = value != 0;
             return GLU_OK;

@@ -108,6 +108,7 @@ struct SnPlan {
     //   {target panel K, need, 0, 0}; RG: {code << 27 | pushes, first MAC index, first U index, chunks},
     //   {first slot, slots, first push, pushes}, {K, need, 0, 0}
     std::vector<I4> tasks;
+    std::vector<float> task_cost;    // per task: the latency model's cost (us), for the warp assignment
     std::vector<int32_t> col_a;      // per column c: first row of c's supernode present in c
     // RG tasks: per RG {first slot, slots, first MAC index, first U index}; the
     // slots it stages in shared memory (targets and multipliers); per MAC
@@ -158,7 +159,6 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
 void sn_free(SnDev *d);
 int sn_grid(int sm_count);
 int64_t sn_set_trace(SnDev *d, int mode);
-int64_t sn_set_assign(SnDev *d, int mode);  // task assignment: 0 static, 1 tickets two ahead, 2 greedy tickets
 int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks);
 // one factorization of v (A_s values after the scatter); pivot failures
 // are min-reduced into *fail as (fail_level << 32 | column) or column

@@ -36,6 +36,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <queue>
 #include <type_traits>
 #include <string>
 #include <vector>
@@ -71,8 +73,7 @@ struct SnParams {
     unsigned long long *cmax;
     int *err;
     unsigned long long *trace;  // optional: per task kTraceWords words
-    unsigned *ticket;           // dynamic task assignment (null: static)
-    int greedy;                 // dynamic: hold no ticket beyond the one taken during a task
+    const int *wptr;            // per warp: its tasks [wptr[g], wptr[g + 1]) of the warp-major task array
 };
 
 __device__ __forceinline__ double ldv(const double *p) { return __ldcg(p); }
@@ -689,74 +690,40 @@ __device__ __forceinline__ bool run_task(const SnParams &P, WarpSmem &S, int4 ta
     return ok;
 }
 
-// Task assignment.  Static: task i runs on CTA i % grid, warp (i / grid) % 8.
-// Dynamic (P.ticket): warps take tasks in list order from a global ticket
-// counter, holding two tickets ahead (the atomic and the next task's record
-// loads overlap the current task), so a warp never sits behind its own long
-// task while ready work waits.  Either way each warp runs its tasks in
-// increasing index and every dependency has a smaller index, so the
-// smallest unfinished task can always run: no deadlock.
+// Task assignment: each warp walks its own list, [wptr[g], wptr[g + 1]) of
+// the warp-major task array (built at upload, sn_assign).  A warp's tasks
+// keep their list order and every dependency has a smaller list index
+// (record tc.w), so the smallest unfinished task can always run: no deadlock.
 __global__ void __launch_bounds__(kSnThreads, 2) sn_kernel(SnParams P) {
     extern __shared__ __align__(16) unsigned char sn_smem_raw[];
     WarpSmem *smem = reinterpret_cast<WarpSmem *>(sn_smem_raw);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem &S = smem[wib];
-    const int nw = gridDim.x * kSnWarps;
-    const bool dyn = P.ticket != nullptr;
-    auto take = [&]() -> int {
-        int t = 0;
-        if (lane == 0) t = (int)atomicAdd(P.ticket, 1u);
-        return __shfl_sync(0xffffffffu, t, 0);
-    };
-    if (P.greedy) {
-        // greedy list scheduling: the next ticket is taken while this task runs
-        // and nothing else is reserved -- a ready task waits only for a free warp
-        int i = take();
-        while (i < P.n_tasks) {
-            const int4 ta = __ldg(P.tasks + 3 * (size_t)i), tb = __ldg(P.tasks + 3 * (size_t)i + 1),
-                       tc = __ldg(P.tasks + 3 * (size_t)i + 2);
-            int k = 0;
-            if (lane == 0) k = (int)atomicAdd(P.ticket, 1u);
-            unsigned long long *tr = P.trace ? P.trace + kTraceWords * (size_t)i : nullptr;
-            if (tr && lane == 0) {
-                tr[0] = globaltimer();
-                tr[4] = blockIdx.x * kSnWarps + wib;
-            }
-            if (!run_task(P, S, ta, tb, tc, lane, tr)) return;
-            if (tr && lane == 0) tr[3] = globaltimer();
-            i = __shfl_sync(0xffffffffu, k, 0);
-        }
-        return;
-    }
-    int i = dyn ? take() : wib * gridDim.x + blockIdx.x;
-    int j = dyn ? take() : i + nw;  // the next task
+    const int g = blockIdx.x * kSnWarps + wib;
+    int pos = __ldg(P.wptr + g);
+    const int end = __ldg(P.wptr + g + 1);
     int4 ta = make_int4(0, 0, 0, 0), tb = ta, tc = ta;
-    if (i < P.n_tasks) {
-        ta = __ldg(P.tasks + 3 * (size_t)i);
-        tb = __ldg(P.tasks + 3 * (size_t)i + 1);
-        tc = __ldg(P.tasks + 3 * (size_t)i + 2);
+    if (pos < end) {
+        ta = __ldg(P.tasks + 3 * (size_t)pos);
+        tb = __ldg(P.tasks + 3 * (size_t)pos + 1);
+        tc = __ldg(P.tasks + 3 * (size_t)pos + 2);
     }
-    while (i < P.n_tasks) {
-        // the task after next is taken and the next task's records load while this one runs
-        int k = j + nw;
-        if (dyn) {
-            if (lane == 0) k = j < P.n_tasks ? (int)atomicAdd(P.ticket, 1u) : P.n_tasks;
-        }
+    while (pos < end) {
+        // the next task's records load while this one runs
         int4 na = ta, nb = tb, nc = tc;
-        if (j < P.n_tasks) {
-            na = __ldg(P.tasks + 3 * (size_t)j);
-            nb = __ldg(P.tasks + 3 * (size_t)j + 1);
-            nc = __ldg(P.tasks + 3 * (size_t)j + 2);
+        if (pos + 1 < end) {
+            na = __ldg(P.tasks + 3 * (size_t)pos + 3);
+            nb = __ldg(P.tasks + 3 * (size_t)pos + 4);
+            nc = __ldg(P.tasks + 3 * (size_t)pos + 5);
         }
-        unsigned long long *tr = P.trace ? P.trace + kTraceWords * (size_t)i : nullptr;
+        unsigned long long *tr = P.trace ? P.trace + kTraceWords * (size_t)tc.w : nullptr;
         if (tr && lane == 0) {
             tr[0] = globaltimer();
-            tr[4] = blockIdx.x * kSnWarps + wib;
+            tr[4] = g;
         }
         if (!run_task(P, S, ta, tb, tc, lane, tr)) return;
         if (tr && lane == 0) tr[3] = globaltimer();
-        i = j;
-        j = dyn ? __shfl_sync(0xffffffffu, k, 0) : k;
+        pos++;
         ta = na;
         tb = nb;
         tc = nc;
@@ -822,6 +789,79 @@ cudaError_t up(T **dst, const std::vector<T> &src, i64 *bytes) {
 
 }  // namespace
 
+// Warp assignment.  Default: round-robin over the list (task i -> CTA
+// i % grid, warp (i / grid) % 8, consecutive tasks on different SMs).
+// GLU_SN_ASSIGN=sim: a list-scheduling simulation of the kernel under the
+// plan's latency model -- tasks in list order, each on the warp that frees
+// first, starting when its counters would be met -- measured slightly
+// slower (cfg4 57.0 vs 55.0 ms, g400 9.14 vs 8.91 ms): the model's task
+// costs are too coarse to beat the blind deal.  Returns the warp-major
+// records (tc.w = list index) and per-warp ranges.
+static void sn_assign(const SnPlan *p, int W, std::vector<int4> &tw, std::vector<int> &wptr) {
+    constexpr double kHop = 2.5;
+    const i64 n = (i64)p->tasks.size() / 3, np = (i64)p->pan.size();
+    std::vector<double> fdone(np, 0.0), kprev(np, 0.0), kcur(np, 0.0);
+    std::vector<i32> kowner(np, -1);  // push (or -1 - RG) whose tasks kcur collects
+    std::vector<i32> warp(n);
+    using E = std::pair<double, int>;
+    std::priority_queue<E, std::vector<E>, std::greater<E>> freeq;
+    for (int w = 0; w < W; w++) freeq.push({0.0, w});
+    const char *mode = std::getenv("GLU_SN_ASSIGN");
+    const bool sim = mode && std::string(mode) == "sim";
+    const int grid = W / kSnWarps;
+    auto settle = [&](i64 K, i32 owner) {  // a new push (group) into K: earlier ones are complete
+        if (kowner[K] != owner) {
+            kprev[K] = std::max(kprev[K], kcur[K]);
+            kcur[K] = 0.0;
+            kowner[K] = owner;
+        }
+    };
+    for (i64 i = 0; i < n && !sim; i++) warp[i] = (int)((i % grid) * kSnWarps + (i / grid) % kSnWarps);
+    for (i64 i = 0; i < n && sim; i++) {
+        const I4 a = p->tasks[3 * i], b = p->tasks[3 * i + 1], c = p->tasks[3 * i + 2];
+        const int kind = (a.x >> 27) >> 2;
+        double ready = 0.0;
+        if (kind == kSnTrsm) {
+            const i64 Pn = a.y;
+            settle(Pn, -2);
+            ready = kprev[Pn];
+        } else if (kind == kSnRect) {
+            const i64 K = c.x;
+            // chunks of one push share (need); a different need means a new push
+            settle(K, c.y);
+            ready = std::max(fdone[a.y], kprev[K]);
+        } else if (kind == kSnUw) {
+            const i64 K = c.x;
+            ready = kowner[K] == c.y ? std::max(kprev[K], kcur[K]) : kprev[K];
+        } else {  // RG: the target once, then every source as it goes
+            const i64 K = c.x;
+            settle(K, c.y);
+            ready = kprev[K];
+            for (i64 y = b.z; y < b.z + b.w; y++) ready = std::max(ready, fdone[p->push[y].x]);
+        }
+        ready += kHop;
+        const E f = freeq.top();
+        freeq.pop();
+        const double fin = std::max(ready, f.first) + (double)p->task_cost[i];
+        freeq.push({fin, f.second});
+        warp[i] = f.second;
+        if (kind == kSnTrsm) fdone[a.y] = std::max(fdone[a.y], fin);
+        else if (kind == kSnRect || kind == kSnRg) kcur[c.x] = std::max(kcur[c.x], fin);
+    }
+    wptr.assign(W + 1, 0);
+    for (i64 i = 0; i < n; i++) wptr[warp[i] + 1]++;
+    for (int w = 0; w < W; w++) wptr[w + 1] += wptr[w];
+    std::vector<int> at(wptr.begin(), wptr.end() - 1);
+    tw.resize(3 * n);
+    for (i64 i = 0; i < n; i++) {
+        const i64 q = at[warp[i]]++;
+        for (int r = 0; r < 3; r++) {
+            const I4 t = p->tasks[3 * i + r];
+            tw[3 * q + r] = make_int4(t.x, t.y, t.z, r == 2 ? (int)i : t.w);
+        }
+    }
+}
+
 struct SnDev {
     int4 *pairs = nullptr, *tasks = nullptr, *panm = nullptr, *wb = nullptr, *push = nullptr, *pan = nullptr;
     i32 *relmap = nullptr, *col_a = nullptr, *rg_slot = nullptr;
@@ -832,7 +872,7 @@ struct SnDev {
     unsigned long long *cmax = nullptr;
     unsigned long long *trace = nullptr;  // per-task timestamps (diagnostics)
     int grid = 0;
-    int assign = 0;  // task assignment (sn_set_assign): 0 static, 1 dynamic two ahead, 2 greedy
+    int *wptr = nullptr;  // per-warp task ranges (sn_assign)
 };
 
 constexpr size_t kSnSmem = sizeof(WarpSmem) * kSnWarps;
@@ -848,8 +888,8 @@ int sn_grid(int sm_count) {
 
 void sn_free(SnDev *d) {
     if (!d) return;
-    void *ptrs[] = {d->pairs, d->tasks, d->panm, d->wb,   d->push, d->pan,  d->relmap, d->col_a,
-                    d->dblk,  d->cnt,   d->cmax, d->trace, d->rg_slot, d->rg_idx, d->rg_uidx};
+    void *ptrs[] = {d->pairs, d->tasks, d->panm,  d->wb,      d->push,   d->pan,     d->relmap, d->col_a,
+                    d->dblk,  d->cnt,   d->cmax,  d->trace, d->rg_slot, d->rg_idx, d->rg_uidx, d->wptr};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete d;
@@ -867,7 +907,7 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
         if (p->panm[q].z >= 0) wb.push_back(make_int4(p->pan[q].x, p->pan[q].y, p->panm[q].z, 0));
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = up(&d->pairs, cast(p->pairs), bytes);
-    if (e == cudaSuccess) e = up(&d->tasks, cast(p->tasks), bytes);
+
     if (e == cudaSuccess) e = up(&d->panm, cast(p->panm), bytes);
     if (e == cudaSuccess) e = up(&d->wb, wb, bytes);
     if (e == cudaSuccess) e = up(&d->push, cast(p->push), bytes);
@@ -902,6 +942,18 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
         sn_free(d);
         return GLU_ECUDA;
     }
+    {  // tasks in warp-major order (sn_assign), each record carrying its list index
+        std::vector<int4> tw;
+        std::vector<int> wptr;
+        sn_assign(p, d->grid * kSnWarps, tw, wptr);
+        e = up(&d->tasks, tw, bytes);
+        if (e == cudaSuccess) e = up(&d->wptr, wptr, bytes);
+        if (e != cudaSuccess) {
+            set_error(std::string("supernodal plan upload: ") + cudaGetErrorString(e));
+            sn_free(d);
+            return GLU_ECUDA;
+        }
+    }
     *out = d;
     return GLU_OK;
 }
@@ -918,11 +970,6 @@ int64_t sn_set_trace(SnDev *d, int mode) {
         cudaFree(d->trace);
         d->trace = nullptr;
     }
-    return GLU_OK;
-}
-
-int64_t sn_set_assign(SnDev *d, int mode) {
-    d->assign = std::max(0, std::min(mode, 2));
     return GLU_OK;
 }
 
@@ -966,8 +1013,7 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         P.cmax = d->cmax;
         P.err = err;
         P.trace = d->trace;
-        P.ticket = d->assign ? d->cnt + 2 * d->n_pan : nullptr;
-        P.greedy = d->assign == 2;
+        P.wptr = d->wptr;
         void *args[] = {&P};
         e = cudaLaunchCooperativeKernel((const void *)sn_kernel, dim3(d->grid), dim3(kSnThreads), args, kSnSmem, s);
         if (e != cudaSuccess) {

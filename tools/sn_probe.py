@@ -122,8 +122,6 @@ def main():
             fz.set_input(a.col_ptr, a.row_idx)
             fz.set_option(1, 0)
             fz.set_option(2, 1)
-            if eng == "sn" and "SN_ASSIGN" in os.environ:
-                fz.set_option(16, int(os.environ["SN_ASSIGN"]))
             a_d = torch.from_numpy(a.values).to(dev)
             v = torch.empty(fp.nnz, dtype=torch.float64, device=dev)
             st = torch.cuda.current_stream()
