@@ -391,14 +391,26 @@ __device__ __forceinline__ void solve_u_tile(RectSmem &R, bool colok, int mylo, 
     double u[kSnW];
 #pragma unroll
     for (int r = 0; r < kSnW; r++) u[r] = R.u[r][q];
+    // Rows r >= w hold garbage: they only ever feed rows above them, which are
+    // never stored, so the steps need no width test.  Columns whose U suffix
+    // starts inside the panel (lo > 0) need a select per step.
+    if (__all_sync(0xffffffffu, !act || mylo == 0)) {
 #pragma unroll
-    for (int j = 0; j < kSnW - 1; j++) {
-        const double uj = u[j];
-        const bool on = j >= mylo && j < w - 1;
+        for (int j = 0; j < kSnW - 1; j++) {
+            const double uj = u[j];
 #pragma unroll
-        for (int r = j + 1; r < kSnW; r++) {
-            const double y = msub(u[r], R.lb[j][r], uj);
-            u[r] = on ? y : u[r];
+            for (int r = j + 1; r < kSnW; r++) u[r] = msub(u[r], R.lb[j][r], uj);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kSnW - 1; j++) {
+            const double uj = u[j];
+            const bool on = j >= mylo;
+#pragma unroll
+            for (int r = j + 1; r < kSnW; r++) {
+                const double y = msub(u[r], R.lb[j][r], uj);
+                u[r] = on ? y : u[r];
+            }
         }
     }
     __syncwarp();
