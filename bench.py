@@ -333,6 +333,23 @@ def profiled_traffic(config, kernel):
         return None
 
 
+def l2_roof(traffic, kernel_ms):
+    """L2 traffic of the kernel (ncu lts__t_sectors x 32 B, profiles/traffic.json)
+    against the measured L2 read bandwidth (tools/ubench/l2bw.cu,
+    profiles/l2_peak.json)."""
+    try:
+        peak = json.loads((ROOT / "profiles" / "l2_peak.json").read_text())["l2_read_gbs"]
+    except (OSError, ValueError, KeyError):
+        return None
+    b = traffic.get("l2_bytes_per_launch")
+    if not b or not kernel_ms:
+        return {"peak_gbs": peak, "achieved_gbs": None, "frac": None}
+    a = b / (kernel_ms * 1e-3) / 1e9
+    return {"bytes": b, "achieved_gbs": a, "peak_gbs": peak, "frac": a / peak,
+            "source": "ncu lts__t_sectors.sum x 32 B (one --set full capture) / this run's kernel time; "
+                      "peak: tools/ubench/l2bw.cu"}
+
+
 def max_over_ranks(x, dev, world):
     import torch
 
@@ -533,7 +550,8 @@ def run_ours(args):
                                             "effective_gbs": bytes_survey / (main_ms * 1e-3) / 1e9
                                             if main_ms else None},
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
-                         "traffic_source": traffic.get("source")},
+                         "traffic_source": traffic.get("source"),
+                         "l2": l2_roof(traffic, main_ms)},
             "roofline_fp64": {"achieved_macs_per_s": macs / (main_ms * 1e-3) if main_ms else None,
                               "peak_macs_per_s": fp64_macs_peak,
                               "frac": macs / (main_ms * 1e-3) / fp64_macs_peak if main_ms else None,
