@@ -216,14 +216,15 @@ class Factorizer:
     def set_input(self, a_col_ptr: np.ndarray, a_row_idx: np.ndarray):
         """Install the A -> A_s slot map (device scatter); cached per A pattern."""
         cp, ri = _lib.i64(a_col_ptr), _lib.i64(a_row_idx)
-        key = (len(cp), len(ri), hashlib.sha1(cp.tobytes() + ri.tobytes()).digest())
-        if key == self._input_key:
-            return
+        last = self._input_key
+        if (last is not None and last[0].shape == cp.shape and last[1].shape == ri.shape
+                and np.array_equal(last[0], cp) and np.array_equal(last[1], ri)):
+            return  # same A pattern as the installed map (compared, not hashed: cfg4 23 vs 215 ms)
         rc = _lib.check(_lib.lib.glu_set_input_pattern(self._h, len(ri), _lib.ptr(cp), _lib.ptr(ri)),
                         "glu_set_input_pattern")
         if rc >= 0:
             raise PatternMismatchError(f"column {rc} of A has entries outside the filled pattern")
-        self._input_key = key
+        self._input_key = (cp.copy(), ri.copy())
 
     def factor_host(self, a_values: np.ndarray, thresh: float) -> tuple[np.ndarray, int]:
         """H2D A values -> device scatter -> factor -> D2H LU values."""
@@ -337,8 +338,22 @@ _CACHE: dict = {}
 _CACHE_LOCK = threading.RLock()
 
 
+_DIGESTS: dict = {}
+
+
 def _digest(a: np.ndarray) -> bytes:
-    return hashlib.sha1(np.ascontiguousarray(a, dtype=np.int64).tobytes()).digest()
+    """sha1 of an int64 array, remembered per array object: a repeated call
+    with the same (unchanged) array costs one comparison instead of a hash
+    (cfg4: 3 vs 23 ms per level schedule)."""
+    a64 = np.ascontiguousarray(a, dtype=np.int64)
+    hit = _DIGESTS.get(id(a))
+    if hit is not None and hit[0].shape == a64.shape and np.array_equal(hit[0], a64):
+        return hit[1]
+    d = hashlib.sha1(a64.tobytes()).digest()
+    if len(_DIGESTS) > 16:
+        _DIGESTS.clear()
+    _DIGESTS[id(a)] = (a64.copy(), d)
+    return d
 
 
 # Per-MAC plans cost ~3.3 B per MAC on the device (and ~2x that on the host
