@@ -239,29 +239,32 @@ __device__ void task_trsm(const SnParams &P, TrsmSmem &S, int4 ta, int4 tb, int4
     __syncwarp();
     const long long c1 = clock64();
     const bool inb = lane < w;
+    // two lanes per block row r = lane % 16: each takes every other column
+    const int br = lane & (kSnW - 1), hf = lane >> 4;
     unsigned long long bmax = 0;
     for (int j = 0; j < w; j++) {
         const unsigned has = __ballot_sync(0xffffffffu, clol <= j);  // bit c: U(j, c) present
-        const bool below = lane > j && inb;
-        const double xj = S.b[j][lane];
+        const bool below = br > j && br < w;
+        const double xj = S.b[j][br];
         const unsigned long long m = warp_max(below ? absbits(xj) : 0ull);
         if (lane == j) bmax = m;
         const double l = div_rn(xj, S.b[j][j], below);
         __syncwarp();
         if (below) {
-            S.b[j][lane] = l;
-            // 4 columns at a time: loads, chains, stores (row j is never written in step j)
-            for (int c = j + 1; c < w; c += 4) {
+            if (hf == 0) S.b[j][br] = l;
+            // 4 of this lane's columns at a time: loads, chains, stores (row j is
+            // never written in step j)
+            for (int c = j + 1 + hf; c < w; c += 8) {
                 double a[4], u[4];
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
-                    const int ck = min(c + k, kSnW - 1);
-                    a[k] = S.b[ck][lane];
+                    const int ck = min(c + 2 * k, kSnW - 1);
+                    a[k] = S.b[ck][br];
                     u[k] = S.b[ck][j];
                 }
 #pragma unroll
                 for (int k = 0; k < 4; k++)
-                    if (c + k < w && ((has >> (c + k)) & 1u)) S.b[c + k][lane] = msub(a[k], l, u[k]);
+                    if (c + 2 * k < w && ((has >> (c + 2 * k)) & 1u)) S.b[c + 2 * k][br] = msub(a[k], l, u[k]);
             }
         }
         __syncwarp();
@@ -612,50 +615,59 @@ __device__ bool task_rg(const SnParams &P, RgSmem &G, int4 ta, int4 tb, int4 tc,
     int slot[kRgSlots / 32];
 #pragma unroll
     for (int j = 0; j < kRgSlots / 32; j++) slot[j] = lane + 32 * j < nslot ? __ldg(P.rg_slot + slot0 + lane + 32 * j) : -1;
-    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
-    if (tr && lane == 0) tr[1] = tr[2] = globaltimer();
-#pragma unroll
-    for (int j = 0; j < kRgSlots / 32; j++)
-        if (slot[j] >= 0) G.val[lane + 32 * j] = ldv(P.v + slot[j]);
+    // Stage the L rows of the pushes whose sources are factored (lane i
+    // acquires push i's TRSM counter): [staged, e) -> flat rows of G.L,
+    // asynchronously.  Returns false on the error path.
+    int staged = 0;
     const unsigned long long t0 = globaltimer();
-    int done = 0;
-    while (done < m) {
-        // pushes [done, e) have factored sources (lane i acquires push i's)
-        const bool rdy = lane < done || lane >= m || ld_acquire(P.cnt + 2 * ps.x + 1) >= (unsigned)fneed;
-        const unsigned nr = __ballot_sync(0xffffffffu, rdy) | (m < 32 ? ~0u << m : 0u);
-        const int e = nr == ~0u ? m : min(m, __ffs(~nr) - 1);
-        if (e == done) {
+    auto stage = [&](bool block) -> bool {
+        while (true) {
+            const bool rdy = lane < staged || lane >= m || ld_acquire(P.cnt + 2 * ps.x + 1) >= (unsigned)fneed;
+            const unsigned nr = __ballot_sync(0xffffffffu, rdy) | (m < 32 ? ~0u << m : 0u);
+            const int e = nr == ~0u ? m : min(m, __ffs(~nr) - 1);
+            if (e > staged) {
+                __syncwarp();
+                const int r0 = __shfl_sync(0xffffffffu, loff, staged);
+                const int r1 = __shfl_sync(0xffffffffu, loff + hl, e - 1);
+                const int nit = (r1 - r0 + 31) >> 5;  // the same trip count on every lane (shuffles inside)
+#pragma unroll 1
+                for (int it = 0; it < nit; it++) {
+                    const int r = r0 + lane + 32 * it;
+                    // the push holding flat row r: the last push k < e with loff(k) <= r
+                    int k = staged;
+#pragma unroll
+                    for (int step = kRgPushes / 2; step; step >>= 1) {
+                        const int c = k + step;
+                        const int lc = __shfl_sync(0xffffffffu, loff, c & 31);
+                        if (c < e && lc <= r) k = c;
+                    }
+                    const int lk = __shfl_sync(0xffffffffu, loff, k), dk = __shfl_sync(0xffffffffu, dcl, k);
+                    if (r < r1) cp_async8(&G.L[r], P.v + dk + 1 + (r - lk), true, P.v);
+                }
+                staged = e;
+                return true;
+            }
+            if (!block) return true;
             if (*(volatile int *)P.err) return false;
             if (globaltimer() - t0 > kSnWatchdogNs) {
                 if (lane == 0) atomicExch(P.err, 1);
                 return false;
             }
             __nanosleep(64);
-            continue;
         }
-        __syncwarp();
-        {  // their L rows, copied together: flat rows [loff(done), loff(e))
-            const int r0 = __shfl_sync(0xffffffffu, loff, done);
-            const int r1 = __shfl_sync(0xffffffffu, loff + hl, e - 1);
-            const int nit = (r1 - r0 + 31) >> 5;  // the same trip count on every lane (shuffles inside)
-#pragma unroll 1
-            for (int it = 0; it < nit; it++) {
-                const int r = r0 + lane + 32 * it;
-                // the push holding flat row r: the last push k < e with loff(k) <= r
-                int k = done;
+    };
+    stage(false);  // sources are usually factored long before the target is ready
+    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
+    if (tr && lane == 0) tr[1] = tr[2] = globaltimer();
 #pragma unroll
-                for (int step = kRgPushes / 2; step; step >>= 1) {
-                    const int c = k + step;
-                    const int lc = __shfl_sync(0xffffffffu, loff, c & 31);
-                    if (c < e && lc <= r) k = c;
-                }
-                const int lk = __shfl_sync(0xffffffffu, loff, k), dk = __shfl_sync(0xffffffffu, dcl, k);
-                if (r < r1) cp_async8(&G.L[r], P.v + dk + 1 + (r - lk), true, P.v);
-            }
-            cp_async_wait();
-        }
+    for (int j = 0; j < kRgSlots / 32; j++)
+        if (slot[j] >= 0) G.val[lane + 32 * j] = ldv(P.v + slot[j]);
+    int done = 0;
+    while (done < m) {
+        if (staged == done && !stage(true)) return false;
+        cp_async_wait();
         __syncwarp();
-        for (int k = done; k < e; k++) {
+        for (int k = done; k < staged; k++) {
             const int h = __shfl_sync(0xffffffffu, pn.w, k), np_ = __shfl_sync(0xffffffffu, npl, k);
             const int io = __shfl_sync(0xffffffffu, ioff, k), uo = __shfl_sync(0xffffffffu, uoff, k);
             const int lo = __shfl_sync(0xffffffffu, loff, k);
@@ -669,7 +681,8 @@ __device__ bool task_rg(const SnParams &P, RgSmem &G, int4 ta, int4 tb, int4 tc,
             }
             __syncwarp();  // the next push sees these updates
         }
-        done = e;
+        done = staged;
+        if (done < m) stage(false);
     }
 #pragma unroll
     for (int j = 0; j < kRgSlots / 32; j++)
