@@ -523,7 +523,7 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
                 // first push, pushes}, {K, need, 0, 0}
                 const I4 g = P->rg[t.pi];
                 const I4 ps = P->push[t.x];
-                P->tasks[3 * i] = I4{(t.kind << 27) | t.chunk, g.z, g.w, P->rg_chunks[t.pi]};
+                P->tasks[3 * i] = I4{(i32)((uint32_t)t.kind << 27 | (uint32_t)t.chunk), g.z, g.w, P->rg_chunks[t.pi]};
                 P->tasks[3 * i + 1] = I4{g.x, g.y, t.x, t.chunk};
                 P->tasks[3 * i + 2] = I4{ps.w, P->push_need[t.x], 0, 0};
                 continue;
@@ -538,7 +538,7 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
                 c = I4{ps.w, P->push_need[t.x], 0, 0};
             }
 
-            P->tasks[3 * i] = I4{(t.kind << 27) | t.chunk, t.pi, pn.x, pn.y};
+            P->tasks[3 * i] = I4{(i32)((uint32_t)t.kind << 27 | (uint32_t)t.chunk), t.pi, pn.x, pn.y};
             P->tasks[3 * i + 1] = I4{(i32)s1_of(pn.z), pn.w, pr0, pr1};
             P->tasks[3 * i + 2] = c;
         }

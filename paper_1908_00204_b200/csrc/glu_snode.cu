@@ -440,7 +440,7 @@ __device__ __forceinline__ void load_lb(const SnParams &P, RectSmem &R, int off,
 // structurally unsymmetric patterns) take the select path.
 __device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4 tc, int lane,
                           unsigned long long *tr) {
-    const int code = ta.x >> 27;
+    const int code = (int)((unsigned)ta.x >> 27);
     const int chunk = ta.x & 0x07ffffff;
     const int Pi = ta.y, p0 = ta.z, p1 = ta.w, w = p1 - p0, h = tb.y;
     const int s1 = tb.x, in_sn = s1 - p1;
@@ -697,7 +697,7 @@ __device__ bool task_rg(const SnParams &P, RgSmem &G, int4 ta, int4 tb, int4 tc,
 
 __device__ __forceinline__ bool run_task(const SnParams &P, WarpSmem &S, int4 ta, int4 tb, int4 tc, int lane,
                                          unsigned long long *tr) {
-    const int kind = (ta.x >> 27) >> 2;
+    const int kind = (int)((unsigned)ta.x >> 29);  // code = kind << 2 | flags in bits 27-31
     if (kind == kSnRg) return task_rg(P, S.g, ta, tb, tc, lane, tr);
     const int w = ta.w - ta.z;
     if (kind == kSnTrsm) {

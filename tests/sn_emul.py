@@ -110,7 +110,7 @@ class _Round:
 
 
 def _decode(tasks):
-    code = tasks[:, 0] >> 27
+    code = (tasks[:, 0].view(np.uint32) >> 27).astype(np.int64)
     return dict(kind=code >> 2, flags=code & 3, chunk=tasks[:, 0] & ((1 << 27) - 1), P=tasks[:, 1],
                 p0=tasks[:, 2], p1=tasks[:, 3], s1=tasks[:, 4], h=tasks[:, 5], r0=tasks[:, 6],
                 r1=tasks[:, 7], K=tasks[:, 8], need=tasks[:, 9])

@@ -49,7 +49,7 @@ def task_profile(fz, fp, a_d, v, st):
         np.savez_compressed(os.environ["SN_TRACE_DUMP"], trace=((tr - t0) // 10).astype(np.int32),
                             warp=warp.astype(np.int32), clk=clk)
     tr = (tr - t0).astype(np.float64) * 1e-3  # us from kernel start
-    kind = (tasks[:, 0] >> 27) >> 2
+    kind = (tasks[:, 0].view(np.uint32) >> 29).astype(np.int64)
     w = tasks[:, 3] - tasks[:, 2]
     wcls = np.select([w <= 1, w <= 2, w <= 4, w <= 8], [1, 2, 4, 8], 16)
     out = {"span_us": float(tr[:, 3].max()), "model_crit_us": plan["info"]["crit_ns"] * 1e-3, "tasks": ntasks}
