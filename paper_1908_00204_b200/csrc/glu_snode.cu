@@ -176,6 +176,7 @@ constexpr int kB = 32;  // lanes: shared-memory tile dimension
 struct TrsmSmem {
     double b[kSnW][kB + 1];  // the diagonal block, column-major [column][row]
     double x[kSnW][kB];      // the chunk's rows below the panel, [column][row = lane]
+    double u[kSnW][kB];      // their undivided values (the column maxima)
 };
 struct RectSmem {
     double l[kSnW][kB];     // [j][row]: divided L rows below the source panel
@@ -241,17 +242,17 @@ __device__ void task_trsm(const SnParams &P, TrsmSmem &S, int4 ta, int4 tb, int4
     const bool inb = lane < w;
     // two lanes per block row r = lane % 16: each takes every other column
     const int br = lane & (kSnW - 1), hf = lane >> 4;
-    unsigned long long bmax = 0;
     for (int j = 0; j < w; j++) {
         const unsigned has = __ballot_sync(0xffffffffu, clol <= j);  // bit c: U(j, c) present
         const bool below = br > j && br < w;
         const double xj = S.b[j][br];
-        const unsigned long long m = warp_max(below ? absbits(xj) : 0ull);
-        if (lane == j) bmax = m;
         const double l = div_rn(xj, S.b[j][j], below);
         __syncwarp();
         if (below) {
-            if (hf == 0) S.b[j][br] = l;
+            if (hf == 0) {
+                S.b[j][br] = l;
+                S.u[j][br] = xj;  // undivided, for the column maximum (taken after the loop)
+            }
             // 4 of this lane's columns at a time: loads, chains, stores (row j is
             // never written in step j)
             for (int c = j + 1 + hf; c < w; c += 8) {
@@ -271,21 +272,32 @@ __device__ void task_trsm(const SnParams &P, TrsmSmem &S, int4 ta, int4 tb, int4
     }
     const long long c2 = clock64();
     if (chunk == 0) {
+        // the block's L-part column maxima (rows below the diagonal, undivided)
+        unsigned long long bmax = 0;
+        for (int c = 0; c < w - 1; c++) {
+            const unsigned long long m = warp_max(lane > c && lane < w ? absbits(S.u[c][lane]) : 0ull);
+            if (lane == c) bmax = m;
+        }
         if (inb && pm.z >= 0)
             for (int c = 0; c < w; c++) stv(P.dblk + pm.z + c * w + lane, S.b[c][lane]);
         if (inb && bmax) atomicMax(P.cmax + p0 + lane, bmax);
+        __syncwarp();  // S.u is reused by the rows below
     }
     // the rows (a register version, steps unrolled over the class width,
-    // measured 4x slower: 16 inlined divisions with their slow-path calls)
-    unsigned long long mymax = 0;
+    // measured 4x slower: 16 inlined divisions with their slow-path calls).
+    // The next column's value is carried in a register from the step that
+    // updates it, and the column maxima (of the undivided values) are taken
+    // after the loop, off the step-to-step chain.
+    double xn = S.x[0][lane];
     for (int j = 0; j < w; j++) {
         const unsigned has = __ballot_sync(0xffffffffu, clol <= j);
-        const double xj = S.x[j][lane];
-        const unsigned long long m = warp_max(act ? absbits(xj) : 0ull);
-        if (lane == j) mymax = m;
+        const double xj = xn;
+        S.u[j][lane] = xj;  // undivided, for the column maximum
         const double d = div_rn(xj, S.b[j][j], act);
         S.x[j][lane] = d;
-        for (int c = j + 1; c < w; c += 4) {
+        xn = j + 1 < w ? S.x[j + 1][lane] : 0.0;
+        if (j + 1 < w && ((has >> (j + 1)) & 1u)) xn = msub(xn, d, S.b[j + 1][j]);
+        for (int c = j + 2; c < w; c += 4) {
             double a[4], u[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -301,6 +313,12 @@ __device__ void task_trsm(const SnParams &P, TrsmSmem &S, int4 ta, int4 tb, int4
     for (int c = 0; c < w; c++) {
         const int dc = __shfl_sync(0xffffffffu, dcl, c);
         if (act) stv(P.v + dc + (w - c) + t, S.x[c][lane]);
+    }
+    __syncwarp();
+    unsigned long long mymax = 0;
+    for (int c = 0; c < w; c++) {
+        const unsigned long long m = warp_max(act ? absbits(S.u[c][lane]) : 0ull);
+        if (lane == c) mymax = m;
     }
     if (inb && mymax) atomicMax(P.cmax + p0 + lane, mymax);
     __syncwarp();
