@@ -3067,7 +3067,11 @@ extern "C" int64_t glu_factor_host(glu_handle *h, const double *a_vals, double *
         GLU_CUDA(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
     }
     if ((rc = launch_factor(h, h->d_v, thresh, s)) != GLU_OK) return rc;
-    if (split) {
+    if (h->sn) {
+        // the supernodal engine's panels become final one by one: their
+        // values travel to the host while the kernel still runs
+        if ((rc = glu::sn_copy_out(h->sn, h->d_v, lu_out, s)) != GLU_OK) return rc;
+    } else if (split) {
         // the columns below the dense tail are final when the main kernel
         // ends: copy them out while the cluster tail kernel runs
         const i64 head = h->col_ptr_h_t0;

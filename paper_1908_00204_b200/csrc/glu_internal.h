@@ -88,6 +88,7 @@ enum SnTaskKind : int32_t {
     kSnRect = 1,  // push rows below the source panel into every column of the target panel
     kSnUw = 2,    // write the solved U(P, K) of a push whose RECT chunks all read it
     kSnRg = 3,    // a run of one-chunk pushes from one-column panels into one target panel
+    kSnWb = 4,    // write a panel's factored diagonal block back in place
 };
 enum SnTaskFlags : int32_t {
     kSnTriF = 1,    // RECT: forward substitution of U(P, K) inside the source block first
@@ -98,7 +99,8 @@ struct SnPlan {
     int64_t n = 0, nnz = 0;
     std::vector<I4> sn;      // {s0, s1, |R_S|, first pair}
     std::vector<I4> pan;     // {p0, p1, supernode, rows below the panel}
-    std::vector<I4> panm;    // per panel {pushes' RECT chunks into it, TRSM chunks, scratch offset | -1, 0}
+    std::vector<I4> panm;    // per panel {pushes' RECT chunks into it, TRSM chunks, scratch offset | -1,
+                             //  WB + UW tasks after which its values are final}
     std::vector<I4> pairs;   // per (supernode S, target column k): {k, a, base, map}
     std::vector<int32_t> relmap;  // positions of R_S's rows in column k (absolute slots)
     std::vector<I4> push;    // {source panel, first pair, end pair, target panel}, target-major
@@ -109,6 +111,7 @@ struct SnPlan {
     //   {first slot, slots, first push, pushes}, {K, need, 0, 0}
     std::vector<I4> tasks;
     std::vector<float> task_cost;    // per task: the latency model's cost (us), for the warp assignment
+    std::vector<int64_t> col_ptr_h;  // the pattern's column pointers (host copy-out of final panels)
     std::vector<int32_t> col_a;      // per column c: first row of c's supernode present in c
     // RG tasks: per RG {first slot, slots, first MAC index, first U index}; the
     // slots it stages in shared memory (targets and multipliers); per MAC
@@ -159,6 +162,9 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes);
 void sn_free(SnDev *d);
 int sn_grid(int sm_count);
 int64_t sn_set_trace(SnDev *d, int mode);
+// Copies the values of v to the host while the factorization launched on s
+// runs (the column ranges whose panels are final), the rest once s is done.
+int64_t sn_copy_out(SnDev *d, const double *v, double *out, void *stream);
 int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks);
 // one factorization of v (A_s values after the scatter); pivot failures
 // are min-reduced into *fail as (fail_level << 32 | column) or column

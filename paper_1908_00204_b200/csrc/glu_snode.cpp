@@ -84,6 +84,7 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
     const int nt = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
     P->n = n;
     P->nnz = col_ptr[n];
+    P->col_ptr_h.assign(col_ptr, col_ptr + n + 1);
     auto llen = [&](i64 c) { return col_ptr[c + 1] - diag_pos[c] - 1; };
 
     // 1. fundamental supernodes
@@ -298,7 +299,7 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
     // deal (each warp walks its tasks in order) cannot deadlock.
     const i64 npush = (i64)P->push.size();
     auto chunks = [](i64 h) { return std::max<i64>(1, (h + 31) / 32); };
-    P->panm.assign(np, I4{0, 0, -1, 0});
+    P->panm.assign(np, I4{0, 0, -1, 0});  // .w: completions (WB, UWs) that finish the panel's values
     i64 dbl = 0;
     for (i64 p = 0; p < np; p++) {
         const I4 pn = P->pan[p];
@@ -447,8 +448,11 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
             const i32 flags = (push_tri[x] ? kSnTriF : 0) | (push_tri[x] && !uw ? kSnWriteU : 0);
             for (i64 c = 0; c < nc; c++) all.push_back({st, per, (kSnRect << 2) | flags, (i32)ps.x, (i32)c, (i32)x});
             t = st + per;
-            if (uw) all.push_back({t + kHop, 1.0 + 0.05 * (double)(w * w * npair) / 16.0, kSnUw << 2,
-                                   (i32)ps.x, 0, (i32)x});
+            if (uw) {
+                all.push_back({t + kHop, 1.0 + 0.05 * (double)(w * w * npair) / 16.0, kSnUw << 2,
+                               (i32)ps.x, 0, (i32)x});
+                P->panm[K].w++;  // the UW writes into K's columns: K is final after it
+            }
             need += nc;
         }
         close_g();
@@ -458,6 +462,10 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         const double st = (need > 0 ? t + kHop : 0.0);
         const double cost = 0.5 + 1.2 * (double)w + (double)(32 * w * w / 2) / kMacsPerUs;
         for (i64 c = 0; c < nc; c++) all.push_back({st, cost, kSnTrsm << 2, (i32)K, (i32)c, -1});
+        if (w >= 2) {  // WB: the factored block back in place once every TRSM chunk has read it
+            all.push_back({st + cost + kHop, 0.5, kSnWb << 2, (i32)K, 0, -1});
+            P->panm[K].w++;
+        }
         f_start[K] = st;
         f_done[K] = st + cost;
         crit = std::max(crit, f_done[K]);

@@ -1,6 +1,5 @@
 // glu_snode.cu -- supernodal engine: one persistent dataflow kernel over the
-// warp tasks of glu_snode.cpp, a write-back of the factored diagonal blocks,
-// then a pivot-check pass.
+// warp tasks of glu_snode.cpp, then a pivot-check pass.
 //
 // Every task is one warp.  Warps walk the task list with a static stride
 // (task i -> CTA i % grid, warp (i / grid) % 8, so consecutive tasks land on
@@ -35,9 +34,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdlib>
 #include <queue>
+#include <thread>
 #include <type_traits>
 #include <string>
 #include <vector>
@@ -70,6 +71,7 @@ struct SnParams {
     const i32 *relmap;
     i32 n_tasks;
     unsigned *cnt;  // per panel P: [2P] RECT chunks into P done, [2P + 1] TRSM chunks of P done
+    unsigned *fin;  // per panel: WB / UW tasks done (its values final once panm.w are; host copy-out)
     unsigned long long *cmax;
     int *err;
     unsigned long long *trace;  // optional: per task kTraceWords words
@@ -581,7 +583,25 @@ __device__ bool task_uw(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4 t
     __syncwarp();
     if (lane < kSnW && colok)
         for (int r = mylo + 1; r < w; r++) stv(P.v + myp.z - (s1 - (p0 + r)), R.u[r][lane]);
-    __syncwarp();
+    release(P.fin + tc.x, lane);
+    return true;
+}
+
+// WB(P): every TRSM chunk of P has read its unfactored diagonal block in
+// place, so the factored block (scratch, column-major w x w) goes back into
+// the values; lane = block row.
+__device__ bool task_wb(const SnParams &P, int4 ta, int lane, unsigned long long *tr) {
+    const int Pi = ta.y, p0 = ta.z, w = ta.w - ta.z;
+    const int4 pm = __ldg(P.panm + Pi);
+    int dcl, clol;
+    panel_cols(P, p0, w, lane, dcl, clol);
+    if (!wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
+    if (tr && lane == 0) tr[1] = tr[2] = globaltimer();
+    for (int c = 0; c < w; c++) {
+        const int dc = __shfl_sync(0xffffffffu, dcl, c), clo = __shfl_sync(0xffffffffu, clol, c);
+        if (lane < w && lane >= clo) stv(P.v + dc + (lane - c), ldv(P.dblk + pm.z + c * w + lane));
+    }
+    release(P.fin + Pi, lane);
     return true;
 }
 
@@ -728,6 +748,7 @@ __device__ __forceinline__ bool run_task(const SnParams &P, WarpSmem &S, int4 ta
         return true;
     }
     if (kind == kSnUw) return task_uw(P, S.r, ta, tb, tc, lane, tr);
+    if (kind == kSnWb) return task_wb(P, ta, lane, tr);
     const bool ok = w == 1 ? task_rect1(P, ta, tb, tc, lane, tr) : task_rect(P, S.r, ta, tb, tc, lane, tr);
     if (ok) release(P.cnt + 2 * tc.x, lane);
     return ok;
@@ -773,22 +794,6 @@ __global__ void __launch_bounds__(kSnThreads, 2) sn_kernel(SnParams P) {
     }
 }
 
-// The factored diagonal blocks (scratch, column-major w x w) written back
-// into the values: one warp per wide panel, lane = block row.
-__global__ void sn_writeback_kernel(double *v, const double *dblk, const int4 *wb, i32 nwb, const i32 *diag_pos,
-                                    const i32 *col_a) {
-    const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    for (i32 k = gw; k < nwb; k += nw) {
-        const int4 e = __ldg(wb + k);  // {p0, p1, scratch offset, 0}
-        const int p0 = e.x, w = e.y - e.x;
-        if (lane >= w) continue;
-        for (int c = 0; c < w; c++) {
-            const int clo = max(__ldg(col_a + p0 + c) - p0, 0);
-            if (lane >= clo) v[__ldg(diag_pos + p0 + c) + (lane - c)] = __ldcg(dblk + e.z + c * w + lane);
-        }
-    }
-}
 
 // pivot test of every column (_kernels.py:60-65): |piv| <= thresh * cmax.
 // One warp per column adds the maximum over its final U part and diagonal
@@ -873,6 +878,8 @@ static void sn_assign(const SnPlan *p, int W, std::vector<int4> &tw, std::vector
             // chunks of one push share (need); a different need means a new push
             settle(K, c.y);
             ready = std::max(fdone[a.y], kprev[K]);
+        } else if (kind == kSnWb) {
+            ready = fdone[a.y];
         } else if (kind == kSnUw) {
             const i64 K = c.x;
             ready = kowner[K] == c.y ? std::max(kprev[K], kcur[K]) : kprev[K];
@@ -906,15 +913,22 @@ static void sn_assign(const SnPlan *p, int W, std::vector<int4> &tw, std::vector
 }
 
 struct SnDev {
-    int4 *pairs = nullptr, *tasks = nullptr, *panm = nullptr, *wb = nullptr, *push = nullptr, *pan = nullptr;
+    int4 *pairs = nullptr, *tasks = nullptr, *panm = nullptr, *push = nullptr, *pan = nullptr;
     i32 *relmap = nullptr, *col_a = nullptr, *rg_slot = nullptr;
     uint16_t *rg_idx = nullptr, *rg_uidx = nullptr;
     double *dblk = nullptr;
-    i64 n = 0, n_tasks = 0, n_pan = 0, n_wb = 0;
+    i64 n = 0, n_tasks = 0, n_pan = 0;
     unsigned *cnt = nullptr;  // 2 per panel + the ticket counter
+    unsigned *fin = nullptr;  // per panel: WB / UW tasks done
     unsigned long long *cmax = nullptr;
     unsigned long long *trace = nullptr;  // per-task timestamps (diagnostics)
     int grid = 0;
+    // host copy-out of final panels (sn_copy_out)
+    std::vector<int32_t> h_p1, h_nch, h_fin;  // per panel: end column, TRSM chunks, final completions
+    std::vector<int64_t> h_colptr;
+    unsigned *h_poll = nullptr;               // pinned: a window of counters
+    cudaStream_t s_poll = nullptr, s_copy = nullptr;
+    cudaEvent_t ev_done = nullptr;
     int *wptr = nullptr;  // per-warp task ranges (sn_assign)
 };
 
@@ -931,8 +945,12 @@ int sn_grid(int sm_count) {
 
 void sn_free(SnDev *d) {
     if (!d) return;
-    void *ptrs[] = {d->pairs, d->tasks, d->panm,  d->wb,      d->push,   d->pan,     d->relmap, d->col_a,
-                    d->dblk,  d->cnt,   d->cmax,  d->trace, d->rg_slot, d->rg_idx, d->rg_uidx, d->wptr};
+    if (d->h_poll) cudaFreeHost(d->h_poll);
+    if (d->s_poll) cudaStreamDestroy(d->s_poll);
+    if (d->s_copy) cudaStreamDestroy(d->s_copy);
+    if (d->ev_done) cudaEventDestroy(d->ev_done);
+    void *ptrs[] = {d->pairs, d->tasks, d->panm,  d->push,   d->pan,     d->relmap, d->col_a,
+                    d->dblk,  d->cnt,   d->cmax,  d->trace, d->rg_slot, d->rg_idx, d->rg_uidx, d->wptr, d->fin};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete d;
@@ -945,14 +963,10 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
         return reinterpret_cast<const std::vector<int4> &>(v);
     };
     static_assert(sizeof(I4) == sizeof(int4), "I4 layout");
-    std::vector<int4> wb;  // {p0, p1, scratch offset, 0} of the panels with w >= 2
-    for (size_t q = 0; q < p->pan.size(); q++)
-        if (p->panm[q].z >= 0) wb.push_back(make_int4(p->pan[q].x, p->pan[q].y, p->panm[q].z, 0));
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = up(&d->pairs, cast(p->pairs), bytes);
 
     if (e == cudaSuccess) e = up(&d->panm, cast(p->panm), bytes);
-    if (e == cudaSuccess) e = up(&d->wb, wb, bytes);
     if (e == cudaSuccess) e = up(&d->push, cast(p->push), bytes);
     if (e == cudaSuccess) e = up(&d->pan, cast(p->pan), bytes);
     if (e == cudaSuccess) e = up(&d->rg_slot, p->rg_slot, bytes);
@@ -962,13 +976,22 @@ int64_t sn_upload(const SnPlan *p, SnDev **out, int64_t *bytes) {
     if (e == cudaSuccess) e = up(&d->col_a, p->col_a, bytes);
     d->n = p->n;
     d->n_tasks = (i64)p->tasks.size() / 3;
+    d->h_colptr = p->col_ptr_h;
+    d->h_p1.resize(p->pan.size());
+    d->h_nch.resize(p->pan.size());
+    d->h_fin.resize(p->pan.size());
+    for (size_t q = 0; q < p->pan.size(); q++) {
+        d->h_p1[q] = p->pan[q].y;
+        d->h_nch[q] = p->panm[q].y;
+        d->h_fin[q] = p->panm[q].w;
+    }
     d->n_pan = (i64)p->pan.size();
-    d->n_wb = (i64)wb.size();
     if (e == cudaSuccess && p->n_dblk > 0) {
         e = cudaMalloc((void **)&d->dblk, sizeof(double) * p->n_dblk);
         *bytes += (i64)sizeof(double) * p->n_dblk;
     }
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->cnt, sizeof(unsigned) * (2 * d->n_pan + 32));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&d->fin, sizeof(unsigned) * std::max<i64>(d->n_pan, 1));
     if (e == cudaSuccess) e = cudaMalloc((void **)&d->cmax, sizeof(unsigned long long) * std::max<i64>(d->n, 1));
     if (e != cudaSuccess) {
         set_error(std::string("supernodal plan upload: ") + cudaGetErrorString(e));
@@ -1024,11 +1047,67 @@ int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks) {
     return m;
 }
 
+int64_t sn_copy_out(SnDev *d, const double *v, double *out, void *stream) {
+    constexpr i64 kWin = 1 << 16;            // panels polled per round trip
+    constexpr i64 kMinBytes = 8ll << 20;     // smallest early copy
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (!d->h_poll) {
+        e = cudaHostAlloc((void **)&d->h_poll, sizeof(unsigned) * 3 * kWin, cudaHostAllocDefault);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d->s_poll, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d->s_copy, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_done, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            set_error(std::string("sn_copy_out: ") + cudaGetErrorString(e));
+            return GLU_ECUDA;
+        }
+    }
+    const i64 np = d->n_pan, nnz = d->h_colptr.back();
+    if ((e = cudaEventRecord(d->ev_done, s)) != cudaSuccess) {
+        set_error(std::string("sn_copy_out: ") + cudaGetErrorString(e));
+        return GLU_ECUDA;
+    }
+    // panels [0, wm) are final: the values of their columns are copied while
+    // the kernel runs (a panel is final once every TRSM chunk, and the WB / UW
+    // tasks writing its columns, have counted themselves)
+    i64 wm = 0, sent = 0;
+    unsigned *hc = d->h_poll, *hf = d->h_poll + 2 * kWin;
+    while (wm < np && cudaEventQuery(d->ev_done) == cudaErrorNotReady) {
+        const i64 len = std::min<i64>(kWin, np - wm);
+        e = cudaMemcpyAsync(hc, d->cnt + 2 * wm, sizeof(unsigned) * 2 * len, cudaMemcpyDeviceToHost, d->s_poll);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hf, d->fin + wm, sizeof(unsigned) * len, cudaMemcpyDeviceToHost, d->s_poll);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(d->s_poll);
+        if (e != cudaSuccess) break;
+        i64 q = 0;
+        while (q < len && hc[2 * q + 1] >= (unsigned)d->h_nch[wm + q] && hf[q] >= (unsigned)d->h_fin[wm + q]) q++;
+        wm += q;
+        const i64 upto = wm > 0 ? d->h_colptr[d->h_p1[wm - 1]] : 0;
+        if (upto - sent >= kMinBytes / (i64)sizeof(double)) {
+            e = cudaMemcpyAsync(out + sent, v + sent, sizeof(double) * (upto - sent), cudaMemcpyDeviceToHost, d->s_copy);
+            if (e != cudaSuccess) break;
+            sent = upto;
+        } else {
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
+        }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && sent < nnz)
+        e = cudaMemcpyAsync(out + sent, v + sent, sizeof(double) * (nnz - sent), cudaMemcpyDeviceToHost, d->s_copy);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->s_copy);
+    if (e != cudaSuccess) {
+        set_error(std::string("sn_copy_out: ") + cudaGetErrorString(e));
+        return GLU_ECUDA;
+    }
+    return GLU_OK;
+}
+
 int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *diag_pos,
                   const int32_t *fail_level, int32_t n, double thresh, bool by_column,
                   unsigned long long *fail, int *err, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(d->cnt, 0, sizeof(unsigned) * (2 * d->n_pan + 32), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d->fin, 0, sizeof(unsigned) * std::max<i64>(d->n_pan, 1), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d->cmax, 0, sizeof(unsigned long long) * std::max<i64>(d->n, 1), s);
     if (d->trace && e == cudaSuccess)
         e = cudaMemsetAsync(d->trace, 0, sizeof(unsigned long long) * kTraceWords * std::max<i64>(d->n_tasks, 1), s);
@@ -1053,6 +1132,7 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         P.relmap = d->relmap;
         P.n_tasks = (i32)d->n_tasks;
         P.cnt = d->cnt;
+        P.fin = d->fin;
         P.cmax = d->cmax;
         P.err = err;
         P.trace = d->trace;
@@ -1061,15 +1141,6 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         e = cudaLaunchCooperativeKernel((const void *)sn_kernel, dim3(d->grid), dim3(kSnThreads), args, kSnSmem, s);
         if (e != cudaSuccess) {
             set_error(std::string("sn_kernel: ") + cudaGetErrorString(e));
-            return GLU_ECUDA;
-        }
-    }
-    if (d->n_wb > 0) {
-        sn_writeback_kernel<<<(unsigned)std::min<i64>((d->n_wb + 7) / 8, 4736), 256, 0, s>>>(
-            v, d->dblk, d->wb, (i32)d->n_wb, diag_pos, d->col_a);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) {
-            set_error(std::string("sn_writeback_kernel: ") + cudaGetErrorString(e));
             return GLU_ECUDA;
         }
     }

@@ -25,7 +25,7 @@ import numpy as np
 
 from paper_1908_00204_b200 import _lib
 
-TRSM, RECT, UW, RG = 0, 1, 2, 3
+TRSM, RECT, UW, RG, WB = 0, 1, 2, 3, 4
 TRI_F, WRITE_U = 1, 2
 
 
@@ -124,6 +124,8 @@ def _waits(d, plan, i):
     k, P = int(d["kind"][i]), int(d["P"][i])
     if k == TRSM:
         return [(0, P, int(panm[P, 0]))]
+    if k == WB:
+        return [(1, P, int(panm[P, 1]))]
     K, need = int(d["K"][i]), int(d["need"][i])
     if k == RECT:
         return [(1, P, int(panm[P, 1])), (0, K, need)]
@@ -245,6 +247,14 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None, schedule="all", seed=0):
         if kind == RG:
             run_rg(E, i)
             return
+        if kind == WB:  # the factored block back in place
+            P_, p0_, p1_ = int(d["P"][i]), int(d["p0"][i]), int(d["p1"][i])
+            w_ = p1_ - p0_
+            clo = clo_of(p0_, w_)
+            for c in range(w_):
+                for r in range(clo[c], w_):
+                    E.wr(int(dp[p0_ + c]) + r - c, E.rdd(P_, c * w_ + r))
+            return
         P, p0, p1, s1, h = (int(d[k][i]) for k in ("P", "p0", "p1", "s1", "h"))
         w = p1 - p0
         rows = range(chunk * 32, min(h, chunk * 32 + 32))
@@ -325,14 +335,7 @@ def emulate(plan, fp, v, thresh=1e-14, fail_level=None, schedule="all", seed=0):
             if s is not None:
                 cnt[s[0], s[1]] += s[2]
         left -= len(ready)
-    # write-back of the factored diagonal blocks, then the pivot check
-    for p in np.flatnonzero(panm[:, 2] >= 0):
-        p0, p1 = int(plan["pan"][p, 0]), int(plan["pan"][p, 1])
-        w = p1 - p0
-        clo = clo_of(p0, w)
-        for c in range(w):
-            for r in range(clo[c], w):
-                v[int(dp[p0 + c]) + r - c] = dblk[(int(p), c * w + r)]
+    # the pivot check
     fail = -1
     best = None
     for c in range(n):

@@ -78,6 +78,8 @@ def main():
         k = int(kind[i])
         if k == 0:
             return [(0, int(P[i]), int(panm[P[i], 0]))]
+        if k == 4:  # WB
+            return [(1, int(P[i]), int(panm[P[i], 1]))]
         if k == 1:
             return [(1, int(P[i]), int(panm[P[i], 1])), (0, int(K[i]), int(need[i]))]
         if k == 3:  # RG: the target, then each push's source panel
@@ -89,7 +91,7 @@ def main():
     i = int(np.argmax(done))
     path = []
     ex = hop = busy = 0.0
-    kinds = np.zeros(4)
+    kinds = np.zeros(5)
     links = {}
     while i >= 0:
         best, bt, bc = -1, -1.0, -1
@@ -129,10 +131,10 @@ def main():
     print(f"  execution per task on the path: median {np.median(exs):.2f} us, p90 {np.percentile(exs, 90):.2f}")
     nb = sum(1 for x in path if x[1] == "warp")
     print(f"  warp-busy links: {nb}")
-    names = {0: "TRSM", 1: "RECT", 2: "UW", 3: "RG"}
+    names = {0: "TRSM", 1: "RECT", 2: "UW", 3: "RG", 4: "WB"}
     print("  dependency links (waited on, task <- predecessor):",
           ", ".join(f"{a} {names[b]}<-{names[c]}: {v}" for (a, b, c), v in sorted(links.items(), key=lambda z: -z[1])))
-    for kk, nm in ((0, "TRSM"), (1, "RECT"), (2, "UW"), (3, "RG")):
+    for kk, nm in ((0, "TRSM"), (1, "RECT"), (2, "UW"), (3, "RG"), (4, "WB")):
         m = [x for x in path if kind[x[0]] == kk]
         if m:
             ww = np.array([max(int(w[x[0]]), 1) for x in m])

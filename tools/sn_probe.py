@@ -57,7 +57,7 @@ def task_profile(fz, fp, a_d, v, st):
     wait_src = tr[:, 1] - tr[:, 0]
     wait_tgt = tr[:, 2] - tr[:, 1]
     by = {}
-    for k, name in ((0, "trsm"), (1, "rect"), (2, "uw")):
+    for k, name in ((0, "trsm"), (1, "rect"), (2, "uw"), (3, "rg"), (4, "wb")):
         for wc in (1, 2, 4, 8, 16):
             m = (kind == k) & (wcls == wc)
             if m.any():
