@@ -842,8 +842,9 @@ cudaError_t up(T **dst, const std::vector<T> &src, i64 *bytes) {
 // GLU_SN_ASSIGN=sim: a list-scheduling simulation of the kernel under the
 // plan's latency model -- tasks in list order, each on the warp that frees
 // first, starting when its counters would be met -- measured slightly
-// slower (cfg4 57.0 vs 55.0 ms, g400 9.14 vs 8.91 ms): the model's task
-// costs are too coarse to beat the blind deal.  Returns the warp-major
+// slower (cfg4 52.1 vs 50.5 ms, g400 8.03 vs 7.65 ms; assigning each task to
+// the least-loaded warp: 52.8 / 8.33 ms): round-robin also spreads
+// consecutive, mostly independent tasks over different SMs.  Returns the warp-major
 // records (tc.w = list index) and per-warp ranges.
 static void sn_assign(const SnPlan *p, int W, std::vector<int4> &tw, std::vector<int> &wptr) {
     constexpr double kHop = 2.5;
