@@ -474,43 +474,6 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
         set_error("supernodal plan: RG index arrays >= 2^31 entries");
         return GLU_EINVAL;
     }
-    // Order key: alpha * ASAP start + (1 - alpha) * ALAP start, where ALAP =
-    // critical path - b-level (the longest chain from the task to the end).
-    // Both are strictly increasing along every dependency (an RG task takes
-    // its last push's b-level), so any blend is a topological order.
-    double alpha = 1.0;
-    if (const char *e = std::getenv("GLU_SN_ORDER_ALPHA")) alpha = std::min(1.0, std::max(0.0, std::atof(e)));
-    if (alpha < 1.0) {
-        std::vector<double> pcost(npush, 0.0), tcost(np, 0.0), bpush(npush, 0.0), btrsm(np, 0.0), bfrom(np, 0.0);
-        for (const T &t : all) {
-            const i32 kind = t.kind >> 2;
-            if (kind == kSnTrsm) tcost[t.pi] = t.cost;
-            else if (kind == kSnRect) pcost[t.x] = t.cost;
-            else if (kind == kSnRg)
-                for (i64 y = t.x; y < t.x + t.chunk; y++) pcost[y] = kGatherSrcUs + (y == t.x ? kGatherUs : 0.0);
-        }
-        std::vector<i64> first(np + 1, npush);
-        for (i64 y = npush - 1; y >= 0; y--) first[P->push[y].w] = y;
-        for (i64 K = np - 1; K >= 0; K--) if (first[K] == npush || P->push[first[K]].w != (i32)K) first[K] = first[K + 1];
-        for (i64 K = np - 1; K >= 0; K--) {
-            btrsm[K] = tcost[K] + kHop + bfrom[K];
-            double nxt = btrsm[K];
-            for (i64 y = first[K + 1] - 1; y >= first[K]; y--) {
-                bpush[y] = pcost[y] + kHop + nxt;
-                nxt = bpush[y];
-                bfrom[P->push[y].x] = std::max(bfrom[P->push[y].x], bpush[y]);
-            }
-        }
-        double tot = 0.0;
-        for (i64 K = 0; K < np; K++) tot = std::max(tot, btrsm[K]);
-        for (T &t : all) {
-            const i32 kind = t.kind >> 2;
-            const double b = kind == kSnTrsm ? btrsm[t.pi]
-                             : kind == kSnRect ? bpush[t.x]
-                             : kind == kSnRg ? bpush[t.x + t.chunk - 1] : t.cost;
-            t.start = alpha * t.start + (1.0 - alpha) * (tot - b);
-        }
-    }
     std::stable_sort(all.begin(), all.end(), [](const T &a, const T &b) {
         return a.start != b.start ? a.start < b.start : a.cost > b.cost;
     });
