@@ -1049,8 +1049,8 @@ int64_t sn_read_trace(SnDev *d, int64_t *out, int64_t max_tasks) {
 }
 
 int64_t sn_copy_out(SnDev *d, const double *v, double *out, void *stream) {
-    constexpr i64 kWin = 1 << 16;            // panels polled per round trip
-    constexpr i64 kMinBytes = 8ll << 20;     // smallest early copy
+    constexpr i64 kWin = 1 << 18;            // panels polled per round trip
+    constexpr i64 kMinRun = 1ll << 17;       // smallest early copy (doubles: 1 MB)
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
     if (!d->h_poll) {
@@ -1063,38 +1063,68 @@ int64_t sn_copy_out(SnDev *d, const double *v, double *out, void *stream) {
             return GLU_ECUDA;
         }
     }
-    const i64 np = d->n_pan, nnz = d->h_colptr.back();
+    const i64 np = d->n_pan;
     if ((e = cudaEventRecord(d->ev_done, s)) != cudaSuccess) {
         set_error(std::string("sn_copy_out: ") + cudaGetErrorString(e));
         return GLU_ECUDA;
     }
-    // panels [0, wm) are final: the values of their columns are copied while
-    // the kernel runs (a panel is final once every TRSM chunk, and the WB / UW
-    // tasks writing its columns, have counted themselves)
-    i64 wm = 0, sent = 0;
+    // A panel is final once every TRSM chunk, and the WB / UW tasks writing
+    // its columns, have counted themselves.  While the kernel runs, windows
+    // of the counters are polled (a cursor sweeping the panels not yet
+    // copied) and every run of final, not yet copied panels worth >= 1 MB is
+    // copied out; in nested-dissection order whole subtrees finish while
+    // their ancestors' separators are still being factored.
+    std::vector<char> copied((size_t)np, 0);
+    auto slots = [&](i64 p) { return d->h_colptr[p > 0 ? d->h_p1[p - 1] : 0]; };  // first slot of panel p
+    auto copy_run = [&](i64 a, i64 b) {  // panels [a, b)
+        const i64 s0 = slots(a), s1 = d->h_colptr[d->h_p1[b - 1]];
+        std::fill(copied.begin() + a, copied.begin() + b, (char)1);
+        return cudaMemcpyAsync(out + s0, v + s0, sizeof(double) * (s1 - s0), cudaMemcpyDeviceToHost, d->s_copy);
+    };
+    i64 lo = 0, cur = 0;
     unsigned *hc = d->h_poll, *hf = d->h_poll + 2 * kWin;
-    while (wm < np && cudaEventQuery(d->ev_done) == cudaErrorNotReady) {
-        const i64 len = std::min<i64>(kWin, np - wm);
-        e = cudaMemcpyAsync(hc, d->cnt + 2 * wm, sizeof(unsigned) * 2 * len, cudaMemcpyDeviceToHost, d->s_poll);
+    while (lo < np && cudaEventQuery(d->ev_done) == cudaErrorNotReady) {
+        if (cur >= np) cur = lo;
+        const i64 len = std::min<i64>(kWin, np - cur);
+        e = cudaMemcpyAsync(hc, d->cnt + 2 * cur, sizeof(unsigned) * 2 * len, cudaMemcpyDeviceToHost, d->s_poll);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(hf, d->fin + wm, sizeof(unsigned) * len, cudaMemcpyDeviceToHost, d->s_poll);
+            e = cudaMemcpyAsync(hf, d->fin + cur, sizeof(unsigned) * len, cudaMemcpyDeviceToHost, d->s_poll);
         if (e == cudaSuccess) e = cudaStreamSynchronize(d->s_poll);
         if (e != cudaSuccess) break;
-        i64 q = 0;
-        while (q < len && hc[2 * q + 1] >= (unsigned)d->h_nch[wm + q] && hf[q] >= (unsigned)d->h_fin[wm + q]) q++;
-        wm += q;
-        const i64 upto = wm > 0 ? d->h_colptr[d->h_p1[wm - 1]] : 0;
-        if (upto - sent >= kMinBytes / (i64)sizeof(double)) {
-            e = cudaMemcpyAsync(out + sent, v + sent, sizeof(double) * (upto - sent), cudaMemcpyDeviceToHost, d->s_copy);
-            if (e != cudaSuccess) break;
-            sent = upto;
-        } else {
-            std::this_thread::sleep_for(std::chrono::microseconds(200));
+        bool issued = false;
+        for (i64 q = 0; q < len && e == cudaSuccess;) {
+            const i64 p = cur + q;
+            auto fin = [&](i64 r) {
+                return hc[2 * r + 1] >= (unsigned)d->h_nch[cur + r] && hf[r] >= (unsigned)d->h_fin[cur + r];
+            };
+            if (copied[p] || !fin(q)) {
+                q++;
+                continue;
+            }
+            i64 r = q;
+            while (r < len && !copied[cur + r] && fin(r)) r++;
+            // a run reaching the copied prefix or worth >= 1 MB goes now
+            if (p == lo || slots(cur + r) - slots(p) >= kMinRun) {
+                e = copy_run(p, cur + r);
+                issued = true;
+            }
+            q = r;
         }
+        while (lo < np && copied[lo]) lo++;
+        cur += len;
+        if (!issued) std::this_thread::sleep_for(std::chrono::microseconds(100));
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e == cudaSuccess && sent < nnz)
-        e = cudaMemcpyAsync(out + sent, v + sent, sizeof(double) * (nnz - sent), cudaMemcpyDeviceToHost, d->s_copy);
+    for (i64 p = lo; p < np && e == cudaSuccess;) {  // the rest, in maximal runs
+        if (copied[p]) {
+            p++;
+            continue;
+        }
+        i64 r = p;
+        while (r < np && !copied[r]) r++;
+        e = copy_run(p, r);
+        p = r;
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(d->s_copy);
     if (e != cudaSuccess) {
         set_error(std::string("sn_copy_out: ") + cudaGetErrorString(e));
