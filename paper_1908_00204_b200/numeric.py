@@ -358,8 +358,11 @@ def _digest(a: np.ndarray) -> bytes:
 
 # Per-MAC plans cost ~3.3 B per MAC on the device (and ~2x that on the host
 # while building): above this many MACs contract A runs on the supernodal
-# engine, whose plan is ~0.1-0.4 B per MAC (cfg4: 3.8e10 MACs).
-SN_MIN_MACS = int(os.environ.get("GLU_SN_MIN_MACS", 2_000_000_000))
+# engine, whose plan is ~0.17 B per MAC (cfg4: 3.8e10 MACs).  Measured: the
+# supernodal engine wins on grids from g400 up (1.2e9 MACs: 7.5 vs ~19 ms)
+# and loses on the circuit patterns below the threshold (cfg2 3.0e8 MACs:
+# 48 vs 6.8 ms, cfg3: 116 vs 4.9 ms -- few wide supernodes, long chains).
+SN_MIN_MACS = int(os.environ.get("GLU_SN_MIN_MACS", 1_000_000_000))
 # contract B has no supernodal form: refuse a per-MAC plan beyond this
 PLAN_MAX_MACS = int(os.environ.get("GLU_PLAN_MAX_MACS", 12_000_000_000))
 
