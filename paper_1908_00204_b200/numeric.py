@@ -555,7 +555,11 @@ def factor_parallel(a: CscMatrix, fp: FilledPattern, schedule: LevelSchedule,
         if hz:
             raise ScheduleHazardError(hz)
     contract = _lib.CONTRACT_A if opts.deterministic else _lib.CONTRACT_B
-    stamps = os.environ.get("GLU_LEVEL_TIMES", "1") != "0"
+    # per-level GPU completion times (FactorStats.level_times) are opt-in:
+    # GLU_LEVEL_TIMES=1 (the stamps cost the per-MAC engine its batched
+    # releases); by default level_times holds one 0.0 per level, the length
+    # the reference's API guarantees (levlu/numeric.py:321-341)
+    stamps = os.environ.get("GLU_LEVEL_TIMES", "0") == "1"
     vals, fz, phases = _factor(a, fp, schedule.level_of, contract, opts.zero_pivot_threshold, False,
                                stamps=stamps)
     caps = [min(concurrency_cap(p, len(c), rm), opts.worker_count, len(c))

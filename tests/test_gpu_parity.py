@@ -499,3 +499,21 @@ def test_single_precision_inputs():
     assert np.array_equal(lu.values, lu64.values.astype(np.float32))
     x = glu.solve(lu, np.ones(a.n, dtype=np.float32))
     assert x.dtype == np.float32 and np.all(np.isfinite(x))
+
+
+def test_level_times_opt_in(monkeypatch):
+    """FactorStats.level_times: one entry per caller level; GPU completion
+    times only with GLU_LEVEL_TIMES=1 (zeros otherwise), the values bitwise
+    the same either way."""
+    g = load_golden("cfg1")
+    a = csc_from_golden(g)
+    fp = glu.symbolic_fillin(a.pattern)
+    s = glu.levelize(glu.detect_relaxed(fp))
+    plans = glu.plan_schedule(s, glu.level_stats(fp, s), a.n, glu.B200_RESOURCE)
+    monkeypatch.setenv("GLU_LEVEL_TIMES", "0")
+    lu0, st0 = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
+    assert st0.level_times == [0.0] * s.level_count
+    monkeypatch.setenv("GLU_LEVEL_TIMES", "1")
+    lu1, st1 = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
+    assert len(st1.level_times) == s.level_count and sum(st1.level_times) > 0.0
+    assert np.array_equal(lu0.values, lu1.values)
