@@ -28,14 +28,18 @@
 //   * inside a push, every target receives the panel's columns in ascending
 //     order (the kernel's chains).
 //
-// The kernel is a dataflow walk over three task kinds (no phases, no grid
+// The kernel is a dataflow walk over five task kinds (no phases, no grid
 // barrier; step 6 below has the counters):
 //   TRSM(P,c)   32 rows below panel P: factor the w x w diagonal block
 //               locally, divide, in-panel updates (chunk 0 also stores the
-//               factored block in a scratch area, written back at the end)
+//               factored block in a scratch area)
+//   WB(P)       the factored block written back in place once every TRSM
+//               chunk of P has read the unfactored one
 //   RECT(x,c)   push x = (P, K), 32 rows below P into every column of K,
 //               after the forward substitution U(P, K) inside P's block
 //   UW(x)       writes the solved U(P, K) when several RECT chunks read it
+//   RG          a run of pushes from one-column panels into one target
+//               panel, applied by one warp on a shared-memory image
 #include <algorithm>
 #include <atomic>
 #include <cstdint>

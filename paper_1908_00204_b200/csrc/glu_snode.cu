@@ -1,20 +1,22 @@
 // glu_snode.cu -- supernodal engine: one persistent dataflow kernel over the
 // warp tasks of glu_snode.cpp, then a pivot-check pass.
 //
-// Every task is one warp.  Warps walk the task list with a static stride
-// (task i -> CTA i % grid, warp (i / grid) % 8, so consecutive tasks land on
-// different SMs) and run their tasks in list order.  There is no phase and
-// no grid barrier: a task waits only for the counters of what it reads
-// (glu_snode.cpp step 6) --
+// Every task is one warp.  Each warp walks its own list of tasks (built at
+// upload, sn_assign: round-robin over the list, consecutive tasks on
+// different SMs) in list order.  There is no phase and no grid barrier: a
+// task waits only for the counters of what it reads (glu_snode.cpp step 6)
+// --
 //   TRSM(P)   in[P] == every RECT chunk of every push into P
 //   RECT(x)   f[P] == every TRSM chunk of its source panel, then
 //             in[K] == every RECT chunk of the earlier pushes into K
+//   RG        in[K] once, then each push's f[P] as it reaches the push
 //   UW(x)     in[K] == the RECT chunks of x as well
+//   WB(P)     f[P] == every TRSM chunk of P (they read the unfactored block)
 // -- and counts itself with one fence + one atomic when done.  Every
-// dependency has a smaller task index, each warp runs its tasks in index
+// dependency has a smaller list index, each warp runs its tasks in list
 // order and all CTAs are co-resident (cooperative launch), so the walk
 // cannot deadlock: the smallest unfinished task can always run.
-//
+
 // A RECT task loads everything that is final once its source panel is
 // factored (its L rows, the factored diagonal block, the target positions)
 // BEFORE it waits for its target panel, so the chain of pushes into one
