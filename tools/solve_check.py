@@ -57,6 +57,11 @@ def main():
     xr, bad = orc.upper_solve(pat, lu, orc.lower_solve(pat, lu, b))
     out["cpu_oracle_ms_k1"] = (time.perf_counter() - t0) * 1e3
     out["bitwise_k1"] = bool(bad == -1 and np.array_equal(xg, xr))
+    # solution residual ||A x - b|| / ||b|| (north_star: <= 1e-10)
+    import scipy.sparse as sp
+
+    A = sp.csc_matrix((a.values, a.row_idx, a.col_ptr), shape=(a.n, a.n))
+    out["residual_k1"] = float(np.linalg.norm(A @ xg - b) / np.linalg.norm(b))
     print(json.dumps(out), flush=True)
 
 
