@@ -63,8 +63,9 @@ def task_profile(fz, fp, a_d, v, st):
             if m.any():
                 by[f"{name}{wc}"] = [int(m.sum()), round(float(np.median(execd[m])), 2),
                                      round(float(np.percentile(execd[m], 90)), 2),
-                                     round(float(np.median(wait_src[m])), 2), round(float(np.median(wait_tgt[m])), 2)]
-    out["by_kind_width[n,exec_med,exec_p90,wait_src_med,wait_tgt_med]"] = by
+                                     round(float(np.median(wait_src[m])), 2), round(float(np.median(wait_tgt[m])), 2),
+                                     round(float(execd[m].sum() * 1e-3), 1)]
+    out["by_kind_width[n,exec_med,exec_p90,wait_src_med,wait_tgt_med,exec_sum_ms]"] = by
     m = (kind == 0) & (w >= 9)
     if m.any():  # TRSM phase cycles (loads, block, rows)
         c = clk[m]
