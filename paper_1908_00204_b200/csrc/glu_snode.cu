@@ -137,6 +137,24 @@ __device__ __forceinline__ bool wait_ge(const SnParams &P, const unsigned *c, un
     return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 
+// Tasks with two waits (source, then target) poll both counters in one
+// round -- lane 0 the first, lane 1 the second, acquire loads in parallel --
+// and skip the wait of each count already reached: a task whose inputs are
+// complete when its warp reaches it (most tasks behind a busy warp) saves
+// the second L2 round trip.  Bit k: counter k reached.  The warp barrier
+// orders every lane's later loads after the acquires.
+__device__ __forceinline__ unsigned poll2(const unsigned *c0, unsigned n0, const unsigned *c1, unsigned n1,
+                                          int lane) {
+    bool ok = true;
+    if (lane < 2) {
+        const unsigned *c = lane ? c1 : c0;
+        const unsigned n = lane ? n1 : n0;
+        ok = n == 0 || ld_acquire(c) >= n;
+    }
+    __syncwarp();
+    return __ballot_sync(0xffffffffu, ok) & 3u;
+}
+
 // x / piv correctly rounded (__ddiv_rn) for the lanes that need it (use):
 // the others divide piv / piv, and a zero x gives the signed zero directly
 // -- a zero numerator or an idle lane's garbage sends __ddiv_rn down its
@@ -377,10 +395,11 @@ __device__ bool task_rect1(const SnParams &P, int4 ta, int4 tb, int4 tc, int lan
         const bool ok = __shfl_sync(0xffffffffu, (int)colok, q) != 0;
         pos[q] = (ok && act) ? target_pos(P, t, in_sn, base, map) : -1;
     }
-    if (!wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
+    const unsigned rdy = poll2(P.cnt + 2 * Pi + 1, (unsigned)pm.y, P.cnt + 2 * tc.x, (unsigned)tc.y, lane);
+    if (!(rdy & 1) && !wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
     if (tr && lane == 0) tr[1] = globaltimer();
     const double L = act ? ldv(P.v + dc + 1 + t) : 0.0;
-    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
+    if (!(rdy & 2) && !wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
     if (tr && lane == 0) tr[2] = globaltimer();
     const double u = colok ? ldv(P.v + myp.z - (s1 - p0)) : 0.0;  // U(p0, k_lane)
     double x[kSnW];
@@ -407,41 +426,38 @@ __device__ __forceinline__ void load_u_tile(const SnParams &P, RectSmem &R, int4
 }
 // The forward substitution U(r, k) -= L(r, j) * U(j, k), j ascending.
 __device__ __forceinline__ void solve_u_tile(RectSmem &R, bool colok, int mylo, int w, int lane) {
-    // lane q < 16 holds column q in registers (a shared-memory chain would
-    // serialize every step behind the previous store: ~10k cycles for w = 16);
-    // the steps are unrolled over the class width, selects keep absent
-    // U(j, k) (j < lo) out and rows >= w are never stored
-    const int q = lane & (kSnW - 1);  // lanes 16-31 shadow lanes 0-15 and store nothing
-    const bool act = lane < kSnW && colok;
-    double u[kSnW];
+    // Column q = lane % 16 lives in two lanes: half h = lane / 16 holds its
+    // rows 2s + h (s < 8) in registers (a shared-memory chain would
+    // serialize every step behind the previous store: ~10k cycles for w = 16;
+    // one lane per column issues twice the FP64 instructions).  Step j takes
+    // U(j, k) from the half that owns row j (a shuffle) and updates the rows
+    // below it, so every element keeps its chain over j ascending.  Selects
+    // keep absent U(j, k) (j < lo) out; rows >= w hold garbage that only
+    // feeds rows below them, which are never read back for the product.
+    const int q = lane & (kSnW - 1), h = lane >> 4;
+    const bool act = __shfl_sync(0xffffffffu, (int)colok, q) != 0;
+    const int qlo = __shfl_sync(0xffffffffu, mylo, q);
+    const int lo = act ? qlo : 0;  // absent columns: never stored
+    double u[kSnW / 2];
 #pragma unroll
-    for (int r = 0; r < kSnW; r++) u[r] = R.u[r][q];
-    // Rows r >= w hold garbage: they only ever feed rows above them, which are
-    // never stored, so the steps need no width test.  Columns whose U suffix
-    // starts inside the panel (lo > 0) need a select per step.
-    if (__all_sync(0xffffffffu, !act || mylo == 0)) {
+    for (int s = 0; s < kSnW / 2; s++) u[s] = R.u[2 * s + h][q];
 #pragma unroll
-        for (int j = 0; j < kSnW - 1; j++) {
-            const double uj = u[j];
-#pragma unroll
-            for (int r = j + 1; r < kSnW; r++) u[r] = msub(u[r], R.lb[j][r], uj);
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < kSnW - 1; j++) {
-            const double uj = u[j];
-            const bool on = j >= mylo;
-#pragma unroll
-            for (int r = j + 1; r < kSnW; r++) {
-                const double y = msub(u[r], R.lb[j][r], uj);
-                u[r] = on ? y : u[r];
+    for (int j = 0; j < kSnW - 1; j++) {
+        const int sj = j >> 1;
+        const double uj = __shfl_sync(0xffffffffu, u[sj], q | (j & 1) << 4);
+        if (j >= lo) {
+            if ((j & 1) == 0) {  // row j = 2 sj sits in half 0: half 1's slot sj is row j + 1
+                const double y = msub(u[sj], R.lb[j][2 * sj + h], uj);
+                u[sj] = h ? y : u[sj];
             }
+#pragma unroll
+            for (int s = sj + 1; s < kSnW / 2; s++) u[s] = msub(u[s], R.lb[j][2 * s + h], uj);
         }
     }
     __syncwarp();
     if (act) {
 #pragma unroll
-        for (int r = 0; r < kSnW; r++) R.u[r][q] = u[r];
+        for (int s = 0; s < kSnW / 2; s++) R.u[2 * s + h][q] = u[s];
     }
 }
 __device__ __forceinline__ void load_lb(const SnParams &P, RectSmem &R, int off, int w, int lane) {
@@ -487,7 +503,8 @@ __device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4
             pos[i][k] = (cok && tt < h) ? target_pos(P, tt, in_sn, base, map) : -1;
         }
     }
-    if (!wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
+    const unsigned rdy = poll2(P.cnt + 2 * Pi + 1, (unsigned)pm.y, P.cnt + 2 * tc.x, (unsigned)tc.y, lane);
+    if (!(rdy & 1) && !wait_ge(P, P.cnt + 2 * Pi + 1, (unsigned)pm.y, lane)) return false;
     if (tr && lane == 0) tr[1] = globaltimer();
 #pragma unroll 1
     for (int j = 0; j < w; j++) {
@@ -496,7 +513,7 @@ __device__ bool task_rect(const SnParams &P, RectSmem &R, int4 ta, int4 tb, int4
     }
     const bool tri = (code & kSnTriF) != 0;
     if (tri) load_lb(P, R, pm.z, w, lane);
-    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
+    if (!(rdy & 2) && !wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
     if (tr && lane == 0) tr[2] = globaltimer();
     const long long c0 = clock64();
     load_u_tile(P, R, myp, colok, mylo, p0, w, s1, lane);
@@ -696,8 +713,13 @@ __device__ bool task_rg(const SnParams &P, RgSmem &G, int4 ta, int4 tb, int4 tc,
             __nanosleep(64);
         }
     };
+    // lane 31 (no push) polls the target alongside the first staging round
+    unsigned tv = 0;
+    if (lane == 31) tv = ld_acquire(P.cnt + 2 * tc.x);
     stage(false);  // sources are usually factored long before the target is ready
-    if (!wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
+    __syncwarp();
+    const bool tgt_ok = __shfl_sync(0xffffffffu, (int)(tv >= (unsigned)tc.y), 31) != 0;
+    if (!tgt_ok && !wait_ge(P, P.cnt + 2 * tc.x, (unsigned)tc.y, lane)) return false;
     if (tr && lane == 0) tr[1] = tr[2] = globaltimer();
 #pragma unroll
     for (int j = 0; j < kRgSlots / 32; j++)
