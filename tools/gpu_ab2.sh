@@ -1,0 +1,13 @@
+# library-swap A/B (HEAD's library in tools/instr_lib/old vs the working tree's), then the window values on the new one
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+TAG=${TAG:-ab2}
+timeout -s ABRT 900 python -X faulthandler -m pytest tests/test_gpu_sn.py -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_sn_${TAG}.log 2>&1
+echo "pytest rc=$?"; tail -2 gpurun_out/pytest_sn_${TAG}.log
+cp paper_1908_00204_b200/libglu_b200.so /tmp/new.so
+for v in old new old new; do
+  if [ $v = old ]; then cp tools/instr_lib/old/libglu_b200.so paper_1908_00204_b200/libglu_b200.so; else cp /tmp/new.so paper_1908_00204_b200/libglu_b200.so; fi
+  echo "lib=$v"; timeout 600 python tools/sn_ab.py ${CFGS:-cfg4} --vals ${VALS:-0} --reps ${REPS:-5} 2>> gpurun_out/ab_${TAG}.err
+done
+cp /tmp/new.so paper_1908_00204_b200/libglu_b200.so
+echo "window values (new)"; timeout 900 python tools/sn_ab.py ${CFGS:-cfg4} g400 --vals ${WVALS:-0,1,3} --reps ${REPS:-5} 2>> gpurun_out/ab_${TAG}.err
