@@ -124,6 +124,13 @@ int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx
 /* Largest dense tail (columns) the current device's cluster kernel holds in
    distributed shared memory; 0 without a CUDA device. */
 int64_t glu_tail_capacity(void);
+/* Page-locked host buffer of nbytes (cudaHostAlloc, portable), for LU
+   values returned through glu_factor_host: the device writes them by DMA
+   while the kernel runs instead of through the driver's pageable staging.
+   Returns the address, or NULL (message: glu_last_error).  No counterpart
+   in the reference (its factors live in host memory throughout). */
+void *glu_host_alloc(int64_t nbytes);
+void glu_host_free(void *p);
 /* info[0..15] = n_levels, n_items, n_chunks, MACs, max_item_macs,
    max_chunks_per_item, deferred_macs (contract A), plan bytes, deep items,
    deep MACs, epochs, push MACs (= u8 map entries), target-list entries,

@@ -48,6 +48,8 @@ SIGNATURES = {
     "glu_find_hazards": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _i64, _p]),
     "glu_plan_build": (_i64, [_i64, _p, _p, _p, _p, _i32, _i64, _i64, _i64, _i32, _pp]),
     "glu_tail_capacity": (_i64, []),
+    "glu_host_alloc": (_p, [_i64]),
+    "glu_host_free": (None, [_p]),
     "glu_plan_build_sn": (_i64, [_i64, _p, _p, _p, _p, _p, _p, _p, _i32, _pp]),
     "glu_sn_plan_info": (None, [_p, _p]),
     "glu_sn_plan_export": (None, [_p] * 14),

@@ -2118,6 +2118,21 @@ extern "C" int64_t glu_tail_capacity(void) {
     return cap;
 }
 
+extern "C" void *glu_host_alloc(int64_t nbytes) {
+    void *p = nullptr;
+    const cudaError_t e = cudaHostAlloc(&p, (size_t)std::max<int64_t>(nbytes, 8), cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        glu::set_error(std::string("glu_host_alloc: ") + cudaGetErrorString(e));
+        return nullptr;
+    }
+    return p;
+}
+
+extern "C" void glu_host_free(void *p) {
+    if (p) cudaFreeHost(p);
+}
+
 extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
                               const int64_t *diag_pos, const int64_t *row_ptr,
                               const int64_t *col_idx, const int64_t *csc_pos,

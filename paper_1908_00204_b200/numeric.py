@@ -229,7 +229,9 @@ class Factorizer:
     def factor_host(self, a_values: np.ndarray, thresh: float) -> tuple[np.ndarray, int]:
         """H2D A values -> device scatter -> factor -> D2H LU values."""
         a = _lib.f64(a_values)
-        out = np.empty(self.nnz, dtype=np.float64)
+        out = _PINNED.empty(self.nnz) if 8 * self.nnz >= _PINNED_MIN else None
+        if out is None:
+            out = np.empty(self.nnz, dtype=np.float64)
         rc = _lib.check(_lib.lib.glu_factor_host(self._h, _lib.ptr(a), _lib.ptr(out), float(thresh)),
                         "glu_factor_host")
         return out, rc
@@ -487,6 +489,48 @@ def _refine(fp: FilledPattern, lv: np.ndarray, contract: int) -> np.ndarray:
         i, j = int(bad[0]), int(bad[1])
         raise ScheduleHazardError([Hazard(writer=i, reader=j, element=(i, j), level=int(lv[j]))])
     return _relaxed_levels(fp) if contract == _lib.CONTRACT_A else out
+
+
+_PINNED_MIN = 32 << 20  # result arrays from this size come from page-locked memory
+
+
+class _PinnedPool:
+    """Page-locked LU result buffers (glu_host_alloc).  glu_factor_host then
+    copies final panels into the result by DMA while the kernel runs; into
+    fresh pageable memory the copy goes through the driver's staging buffers
+    and first-touch page faults (cfg4: ~300 ms for 1.47 GB).  A returned
+    array owns its buffer until it and every view of it are gone; the buffer
+    then returns to the pool (``keep`` per size) for the next
+    refactorization instead of being freed."""
+
+    def __init__(self, keep: int = 2):
+        self._free: dict[int, list[int]] = {}
+        self._lock = threading.Lock()
+        self._keep = keep
+
+    def empty(self, n: int) -> np.ndarray | None:
+        nbytes = 8 * n
+        with self._lock:
+            lst = self._free.get(nbytes)
+            addr = lst.pop() if lst else None
+        if addr is None:
+            addr = _lib.lib.glu_host_alloc(nbytes)
+            if not addr:  # no device / pinned memory exhausted: pageable instead
+                return None
+        buf = (ctypes.c_double * n).from_address(addr)
+        weakref.finalize(buf, self._put, addr, nbytes).atexit = False
+        return np.frombuffer(buf, dtype=np.float64)
+
+    def _put(self, addr: int, nbytes: int) -> None:
+        with self._lock:
+            lst = self._free.setdefault(nbytes, [])
+            if len(lst) < self._keep:
+                lst.append(addr)
+                return
+        _lib.lib.glu_host_free(addr)
+
+
+_PINNED = _PinnedPool()
 
 
 def _factor(a: CscMatrix, fp: FilledPattern, level_of: np.ndarray | None, contract: int,

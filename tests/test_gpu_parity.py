@@ -517,3 +517,38 @@ def test_level_times_opt_in(monkeypatch):
     lu1, st1 = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
     assert len(st1.level_times) == s.level_count and sum(st1.level_times) > 0.0
     assert np.array_equal(lu0.values, lu1.values)
+
+
+def test_pinned_results_own_their_buffers(monkeypatch):
+    """Results in page-locked pool buffers (numeric._PinnedPool): a kept
+    result is never overwritten by a later factorization, a dropped one's
+    buffer is reused, and every result is bitwise the oracle's."""
+    import gc
+
+    from paper_1908_00204_b200 import numeric, synthetic
+
+    monkeypatch.setattr(numeric, "_PINNED_MIN", 0)
+    a = synthetic.make("cfg1")
+    fp, s, plans = _analyze(a)
+    pat = orc.Pattern.from_fp(fp)
+    opts = glu.FactorOptions(deterministic=True)
+
+    def oracle(vals):
+        v, bad = orc.scatter(pat, a.col_ptr, a.row_idx, vals)
+        assert bad == -1 and orc.factor_left_looking(pat, v, opts.zero_pivot_threshold) == -1
+        return v
+
+    lu1, _ = glu.factor_parallel(a, fp, s, plans, opts)
+    keep = lu1.values.copy()
+    assert np.array_equal(keep, oracle(a.values))
+    a2 = glu.CscMatrix(a.n, a.col_ptr, a.row_idx, synthetic.perturb_values(a, seed=3))
+    lu2, _ = glu.factor_parallel(a2, fp, s, plans, opts)
+    assert np.array_equal(lu1.values, keep)  # not aliased by the second result
+    assert np.array_equal(lu2.values, oracle(a2.values))
+    addr2 = lu2.values.ctypes.data
+    del lu2
+    gc.collect()
+    lu3, _ = glu.factor_parallel(a, fp, s, plans, opts)
+    assert lu3.values.ctypes.data == addr2  # the dropped buffer came back from the pool
+    assert np.array_equal(lu3.values, keep)
+    assert lu3.values.flags.writeable and lu3.values.flags.c_contiguous
