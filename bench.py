@@ -476,7 +476,8 @@ def run_ours(args):
         opts = glu.FactorOptions(deterministic=contract == _lib.CONTRACT_A)
         mats = [glu.CscMatrix(a.n, a.col_ptr, a.row_idx, x) for x in sets]
         os.environ["GLU_LEVEL_TIMES"] = "0"
-        glu.factor_parallel(mats[0], fp, s, plans, opts)
+        for i in range(2):  # warm-up in the timed loop's shape: the previous result stays alive
+            lu, _ = glu.factor_parallel(mats[i % nsets], fp, s, plans, opts)
         reps = max(2, min(args.steps, 5))
         t1 = time.perf_counter()
         for i in range(reps):
@@ -484,7 +485,8 @@ def run_ours(args):
         api_ms = max_over_ranks((time.perf_counter() - t1) * 1e3 / reps, dev, world)
         e2e_api = {"value": world * 1e3 / api_ms, "unit": "refactorizations/s", "ms_per_matrix": api_ms,
                    "steps": reps, "api": "factor_parallel(a, fp, schedule, plans, opts) -> LuFactors "
-                                         "(levlu/numeric.py:241; pageable numpy in and out)"}
+                                         "(levlu/numeric.py:241; numpy in, numpy out: LU values in "
+                                         "recycled page-locked buffers, numeric._PinnedPool)"}
         del lu, mats
 
     batch = None
