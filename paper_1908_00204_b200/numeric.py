@@ -217,8 +217,7 @@ class Factorizer:
         """Install the A -> A_s slot map (device scatter); cached per A pattern."""
         cp, ri = _lib.i64(a_col_ptr), _lib.i64(a_row_idx)
         last = self._input_key
-        if (last is not None and last[0].shape == cp.shape and last[1].shape == ri.shape
-                and np.array_equal(last[0], cp) and np.array_equal(last[1], ri)):
+        if last is not None and _same(last[0], cp) and _same(last[1], ri):
             return  # same A pattern as the installed map (compared, not hashed: cfg4 23 vs 215 ms)
         rc = _lib.check(_lib.lib.glu_set_input_pattern(self._h, len(ri), _lib.ptr(cp), _lib.ptr(ri)),
                         "glu_set_input_pattern")
@@ -341,6 +340,19 @@ _CACHE_LOCK = threading.RLock()
 
 
 _DIGESTS: dict = {}
+_LIBC = ctypes.CDLL(None)
+_LIBC.memcmp.restype = ctypes.c_int
+_LIBC.memcmp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+
+
+def _same(a: np.ndarray, b: np.ndarray) -> bool:
+    """Byte equality of two contiguous arrays of one dtype (memcmp: no
+    temporary boolean array; cfg4's A pattern 6 vs 20 ms)."""
+    if a.shape != b.shape or a.dtype != b.dtype:
+        return False
+    if not (a.flags.c_contiguous and b.flags.c_contiguous):
+        return bool(np.array_equal(a, b))
+    return a.nbytes == 0 or _LIBC.memcmp(a.ctypes.data, b.ctypes.data, a.nbytes) == 0
 
 
 def _digest(a: np.ndarray) -> bytes:
@@ -349,7 +361,7 @@ def _digest(a: np.ndarray) -> bytes:
     (cfg4: 3 vs 23 ms per level schedule)."""
     a64 = np.ascontiguousarray(a, dtype=np.int64)
     hit = _DIGESTS.get(id(a))
-    if hit is not None and hit[0].shape == a64.shape and np.array_equal(hit[0], a64):
+    if hit is not None and _same(hit[0], a64):
         return hit[1]
     d = hashlib.sha1(a64.tobytes()).digest()
     if len(_DIGESTS) > 16:
