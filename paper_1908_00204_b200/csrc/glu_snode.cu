@@ -78,7 +78,6 @@ struct SnParams {
     int *err;
     unsigned long long *trace;  // optional: per task kTraceWords words
     const int *wptr;            // per warp: its tasks [wptr[g], wptr[g + 1]) of the warp-major task array
-    int facq;                   // waits: relaxed polls + an acquire fence (GLU_SN_FACQ=1) instead of a confirming acquire load
 };
 
 __device__ __forceinline__ double ldv(const double *p) { return __ldcg(p); }
@@ -123,9 +122,7 @@ __device__ __forceinline__ bool wait_ge(const SnParams &P, const unsigned *c, un
     if (lane == 0 && need > 0 && ld_acquire(c) < need) {
         const unsigned long long t0 = globaltimer();
         unsigned ns = 16;
-        // facq: the count observed by a relaxed load, then an acquire fence
-        // (one L2 round trip less than a confirming acquire load)
-        while (ld_relaxed(c) < need || (!P.facq && ld_acquire(c) < need)) {
+        while (ld_relaxed(c) < need || ld_acquire(c) < need) {
             if (*(volatile int *)P.err) { ok = 0; break; }
             if (globaltimer() - t0 > kSnWatchdogNs) {
                 atomicExch(P.err, 1);
@@ -135,7 +132,6 @@ __device__ __forceinline__ bool wait_ge(const SnParams &P, const unsigned *c, un
             __nanosleep(ns);
             ns = ns < 128 ? 2 * ns : ns;
         }
-        if (P.facq) asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncwarp();
     return __shfl_sync(0xffffffffu, ok, 0) != 0;
@@ -1196,10 +1192,6 @@ int64_t sn_launch(SnDev *d, double *v, const int32_t *col_ptr, const int32_t *di
         P.err = err;
         P.trace = d->trace;
         P.wptr = d->wptr;
-        {
-            const char *fv = std::getenv("GLU_SN_FACQ");
-            P.facq = fv ? std::atoi(fv) : 0;
-        }
         void *args[] = {&P};
         e = cudaLaunchCooperativeKernel((const void *)sn_kernel, dim3(d->grid), dim3(kSnThreads), args, kSnSmem, s);
         if (e != cudaSuccess) {
