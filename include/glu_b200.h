@@ -134,7 +134,7 @@ void glu_host_free(void *p);
 /* info[0..15] = n_levels, n_items, n_chunks, MACs, max_item_macs,
    max_chunks_per_item, deferred_macs (contract A), plan bytes, deep items,
    deep MACs, epochs, push MACs (= u8 map entries), target-list entries,
-   tail start column t0 (n: no tail), tail MACs, express-queue items.  MACs (info[3]) counts
+   tail start column t0 (n: no tail), tail MACs, 0 (reserved).  MACs (info[3]) counts
    push + deep + tail MACs. */
 void glu_plan_info(const glu_plan *p, int64_t *info);
 /* level_item_ptr[n_levels+1];

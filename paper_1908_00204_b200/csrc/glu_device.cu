@@ -52,24 +52,6 @@ constexpr int kLineWords = 32;   // u32 stride between hot words (one 128 B line
 constexpr int kColRep = 4;       // replicas of each column's completion counter (spread the pollers)
 constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s: a dependency wait this long is a bug
 
-// ---------------------------------------------------------------------------
-// grid barrier (solve kernel): monotonically increasing arrival counter,
-// release on arrive, acquire on the spin.  Co-residency is guaranteed by the
-// cooperative launch.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void grid_barrier(unsigned int *count, unsigned int target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
-        unsigned int v;
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
-            if (v >= target) break;
-        }
-    }
-    __syncthreads();
-}
-
 // L2 residency: the plan streams (items, chunks, maps, deep refs: ~1 GB for
 // cfg2, read once per factorization) are loaded with an evict_first policy so
 // they do not push the 34 MB value array out of the 126 MB L2; the values
@@ -122,8 +104,6 @@ struct FactorParams {
     const i32 *level_need;  // items per phase
     i32 n;
     i32 n_items;
-    i32 n_express;          // items [0, n_express) are dealt to CTAs [0, express_R)
-    i32 express_R;
     i32 n_levels;
     i32 n_div;              // columns the final pass divides (the dense tail divides its own)
     i32 nb;                 // value sets factored by this launch (batch-major, set_stride apart)
@@ -138,7 +118,6 @@ struct FactorParams {
     unsigned long long *level_ns;  // optional per-phase completion timestamps
     unsigned long long *trace;     // optional per-item timestamps (diagnostics)
     i32 trace_i0, trace_i1;        // traced item range
-    i32 prefetch;                  // L2-prefetch the next item's static plan data when its phase < prefetch
     i32 poll_ns;                   // sleep between dependency polls
     i32 fail_by_column;            // 1: key = column only (sequential API semantics)
 };
@@ -416,28 +395,6 @@ __device__ __forceinline__ bool wait_cols(const FactorParams &P, int lane, bool 
 // the MACs applied there epoch by epoch (entries of one epoch hit distinct
 // targets; only epochs are ordered), and every target written back once.
 
-// L2 prefetch of an item's static plan data (descriptor already loaded):
-// its chunk descriptors, u8 map and target list, or the first deep refs.
-__device__ __forceinline__ void prefetch_item(const FactorParams &P, int4 a, int4 b, int4 c, int lane) {
-    if (c.y < 0 || (c.y >> 2) >= P.prefetch) return;
-    const char *p = nullptr;
-    if (c.y & 1) {
-        const i64 off = (i64)(unsigned)a.x | ((i64)a.y << 32);
-        if (lane < 8 && lane * 8 < c.x) p = reinterpret_cast<const char *>(P.deep + off) + lane * 128;
-    } else {
-        const i64 moff = (i64)(unsigned)a.x | ((i64)a.y << 32);
-        const i64 toff = (i64)(unsigned)a.z | ((i64)a.w << 32);
-        if (lane < 5) {
-            if (lane * 128 < b.z * 16) p = reinterpret_cast<const char *>(P.chunks + b.y) + lane * 128;
-        } else if (lane < 7) {
-            if ((lane - 5) * 128 < c.x) p = reinterpret_cast<const char *>(P.map8 + moff) + (lane - 5) * 128;
-        } else if (lane < 10) {
-            if ((lane - 7) * 128 < 2 * b.w) p = reinterpret_cast<const char *>(P.tgt16 + toff) + (lane - 7) * 128;
-        }
-    }
-    if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 __device__ __forceinline__ int round_chunk(int rbase, int lane, int nch, int est) {
     const unsigned start_bits = __reduce_or_sync(
         0xffffffffu, (lane < nch && est > rbase && est < rbase + 32) ? (1u << (est - rbase)) : 0u);
@@ -513,7 +470,6 @@ __device__ __forceinline__ bool run_push(const FactorParams &P, int4 a, int4 b, 
         !wait_cols(P, lane, lane < nch, ch.y, jneed, lane < ncol, kcol, kneed, lvl, cs, rep))
         return false;
     stamp(rec, 4, lane);
-    prefetch_item(P, na, nb, nc, lane);
     // value phase: NS value sets per round of loads (batch launches share
     // the static part, the dependency wait and the release across all sets)
     int ep[KR];
@@ -627,7 +583,6 @@ __device__ __forceinline__ bool run_deep(const FactorParams &P, int4 a, int4 b, 
         return false;
     }
     stamp(rec, 3, lane);
-    prefetch_item(P, na, nb, nc, lane);
     // once per value set of the launch (the refs stream again for each)
     for (int bs = 0; bs < P.nb; ++bs) {
     if (bs > 0) issue_ring();
@@ -750,21 +705,8 @@ __global__ void __launch_bounds__(kThreads, 1) factor_kernel(FactorParams P) {
     }
     __syncthreads();
     if (P.level_ns && blockIdx.x == 0 && threadIdx.x == 0) P.level_ns[0] = globaltimer();
-    // queue of this warp: the express items on the first express_R CTAs, the
-    // rest on the others; consecutive items on consecutive SMs in each
-    int q_lo = 0, q_hi = P.n_items, g0 = gw, qstride = nw;
-    if (P.express_R > 0) {
-        const int R = P.express_R, wslot = threadIdx.x >> 5;
-        if ((int)blockIdx.x < R) {
-            q_hi = P.n_express;
-            g0 = wslot * R + blockIdx.x;
-            qstride = R * kWarps;
-        } else {
-            q_lo = P.n_express;
-            g0 = q_lo + wslot * ((int)gridDim.x - R) + ((int)blockIdx.x - R);
-            qstride = ((int)gridDim.x - R) * kWarps;
-        }
-    }
+    // this warp's items: consecutive items on consecutive SMs
+    const int q_hi = P.n_items, g0 = gw, qstride = nw;
     int cur = -1, coarse = 0, nq = 0;
     unsigned ran = 0;
     __shared__ WarpQ wqs[kWarps];
@@ -1346,22 +1288,6 @@ __global__ void scatter_kernel(const double *a, const i32 *slot, i64 nz, double 
 // subtraction chain in order from shuffles, so the bits match the
 // sequential column sweep.
 // ---------------------------------------------------------------------------
-struct SolveParams {
-    const double *v;
-    double *x;
-    const i32 *lvl_ptr;   // per solve level, range into rows
-    const i32 *rows;
-    const i32 *ent_ptr;   // per row, range into ent_col/ent_slot
-    const i32 *ent_col;
-    const i32 *ent_slot;
-    const i32 *diag_pos;  // upper only
-    i32 n_levels;
-    unsigned int *bar;
-    i32 upper;
-    i32 nrhs;      // right-hand sides, x + r * ldx
-    long long ldx;
-};
-
 constexpr int kSolveRing = 4;  // entry-index chunks in flight per warp (cp.async)
 
 __device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pred) {
@@ -1370,93 +1296,6 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pre
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveParams S) {
-    __shared__ __align__(16) double pbuf[kWarps][32];
-    __shared__ int icol[kWarps][kSolveRing][32], islot[kWarps][kSolveRing][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int gw = blockIdx.x * kWarps + w;
-    const int nw = gridDim.x * kWarps;
-    unsigned int target = 0;
-    for (int l = 0; l < S.n_levels; ++l) {
-        const int r0 = __ldg(S.lvl_ptr + l), r1 = __ldg(S.lvl_ptr + l + 1);
-        const int cnt_l = r1 - r0;
-        // (row, right-hand side) pairs of the level over the warps
-        for (int idx = gw; idx < cnt_l * S.nrhs; idx += nw) {
-            const int ri = r0 + idx % cnt_l;
-            double *X = S.x + (size_t)(idx / cnt_l) * S.ldx;
-            const int i = __ldg(S.rows + ri);
-            const int e0 = __ldg(S.ent_ptr + i), e1 = __ldg(S.ent_ptr + i + 1);
-            double acc = ldv(X + i);
-            const int ne = e1 - e0, ng = (ne + 31) >> 5;
-            // Pipeline per row: entry indices stream into a shared ring
-            // kSolveRing chunks ahead (cp.async), the x / L-or-U value loads of
-            // chunk g+1 are in flight while lanes form the products of chunk g
-            // (independent roundings) and lane 0 runs the ordered chain --
-            // ascending column for L (skipping zero x, _kernels.py:176-183),
-            // descending for U (_kernels.py:186-197) -- from shared memory.
-            auto ent = [&](int k) { return S.upper ? (e1 - 1 - k) : (e0 + k); };
-            auto issue_idx = [&](int g) {
-                const int k = 32 * g + lane;
-                const int e = ent(min(k, ne - 1));
-                cp_async4(&icol[w][g % kSolveRing][lane], S.ent_col + e, k < ne);
-                cp_async4(&islot[w][g % kSolveRing][lane], S.ent_slot + e, k < ne);
-                cp_async_commit();
-            };
-#pragma unroll
-            for (int g = 0; g < kSolveRing; ++g) issue_idx(g);
-            double xa = 0.0, va = 0.0;  // operands of the chunk being consumed next
-            cp_async_wait<kSolveRing - 1>();
-            __syncwarp();
-            if (lane < ne) {
-                xa = ldv(X + icol[w][0][lane]);
-                va = ldv(S.v + islot[w][0][lane]);
-            }
-            for (int g = 0; g < ng; ++g) {
-                // operands of chunk g+1 (its indices landed: at most kSolveRing-2
-                // newer groups pending)
-                double xb = 0.0, vb = 0.0;
-                cp_async_wait<kSolveRing - 2>();
-                __syncwarp();
-                if (32 * (g + 1) + lane < ne) {
-                    xb = ldv(X + icol[w][(g + 1) % kSolveRing][lane]);
-                    vb = ldv(S.v + islot[w][(g + 1) % kSolveRing][lane]);
-                }
-                __syncwarp();
-                issue_idx(g + kSolveRing);  // refill the slot of chunk g
-                const bool live = 32 * g + lane < ne;
-                const bool use = live && (S.upper ? true : (xa != 0.0));
-                // a skipped entry contributes +0.0: subtracting +0.0 is an exact
-                // no-op in IEEE round-to-nearest (also for -0, inf and NaN), so
-                // the chain is pure subtractions with no select in its path
-                pbuf[w][lane] = use ? __dmul_rn(va, xa) : 0.0;
-                __syncwarp();
-                if (lane == 0) {
-                    const double2 *pb = reinterpret_cast<const double2 *>(pbuf[w]);
-                    const int cnt = min(32, ne - 32 * g);
-                    if (cnt == 32) {
-#pragma unroll
-                        for (int s2 = 0; s2 < 16; ++s2) {
-                            const double2 x = pb[s2];
-                            acc = __dsub_rn(acc, x.x);
-                            acc = __dsub_rn(acc, x.y);
-                        }
-                    } else {
-                        for (int s1 = 0; s1 < cnt; ++s1) acc = __dsub_rn(acc, pbuf[w][s1]);
-                    }
-                }
-                __syncwarp();
-                xa = xb;
-                va = vb;
-            }
-            cp_async_wait<0>();
-            __syncwarp();
-            if (S.upper && lane == 0) acc = __ddiv_rn(acc, ldv(S.v + __ldg(S.diag_pos + i)));
-            if (lane == 0) stv(X + i, acc);
-        }
-        target += gridDim.x;
-        grid_barrier(S.bar, target);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Dataflow triangular solves (default): no grid barrier.  Every unknown of
@@ -1955,7 +1794,6 @@ struct glu_handle {
     i32 *col_total = nullptr;   // per column: items into it
     glu::ColDep *cdeps = nullptr;
     i64 tail_t0 = 0;            // dense cluster tail: columns [tail_t0, n)
-    i64 n_express = 0, express_R = 0;
     i64 max_push_macs = 0;  // largest push item of the plan (kernel variant)
     TailShape tail;
     double *tail_g = nullptr;
@@ -1983,14 +1821,12 @@ struct glu_handle {
     i32 *a_slot = nullptr;
     // scratch
     unsigned long long *fail = nullptr;
-    unsigned int *bar = nullptr;
     int *ifail = nullptr;
     int *err_acc = nullptr;  // sticky watchdog word across the launches of one batched call
     // dataflow solves: sentinel-managed y buffer, [ticket, err] words
     double *solve_y = nullptr;
     i64 solve_y_cap = 0;
     unsigned *sctl = nullptr;
-    int solve_mode = 0;  // 0 dataflow, 1 level-synchronous (grid barrier per level)
     int solve_tblock = 1;  // dataflow solve: tickets per grab (0 = static round-robin)
     bool solve_multi = true;  // k > 1: lanes over right-hand sides (solve_dfm_kernel)
     double *solve_yi = nullptr, *solve_zi = nullptr;  // interleaved y / x, sentinel between calls
@@ -2013,7 +1849,6 @@ struct glu_handle {
     i64 trace_l0 = 0, trace_nl = 0, trace_cap = 0;
     bool time_levels = false;
     bool fail_by_column = false;
-    int prefetch = 0;  // phases whose items get their plan data L2-prefetched (option 5)
     int poll_ns = 32;
     std::vector<double> last_level_ms;
     // host-API staging
@@ -2180,9 +2015,7 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
         if ((rc = upload_raw(h, &h->cdeps, pv.cdeps, pv.n_cdeps)) != GLU_OK) return fail(rc);
         h->tail_t0 = pv.tail_t0;
         h->col_ptr_h_t0 = col_ptr[pv.tail_t0];
-        h->n_express = pv.n_express;
         h->max_push_macs = pv.max_push_macs;
-        h->express_R = pv.express_R;
         const i64 m = n - pv.tail_t0;
         if (m > 0) {
             h->tail = pick_tail((int)m, nullptr);
@@ -2272,7 +2105,6 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     h->l_ptr_h = std::move(lp); h->u_ptr_h = std::move(up_);
 #undef UP
     if (cudaMalloc((void **)&h->fail, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc((void **)&h->bar, sizeof(unsigned int)) != cudaSuccess ||
         cudaMalloc((void **)&h->ifail, sizeof(int)) != cudaSuccess ||
         cudaMalloc((void **)&h->err_acc, sizeof(int)) != cudaSuccess ||
         cudaMalloc((void **)&h->sctl, 2 * sizeof(unsigned)) != cudaSuccess) {
@@ -2284,7 +2116,6 @@ extern "C" int64_t glu_create(int64_t n, const int64_t *col_ptr, const int64_t *
     h->grid = std::min({coop_grid((const void *)factor_kernel<4, 1>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)factor_kernel<2, 2>, h->sm_count, kFactorDynSmem),
                         coop_grid((const void *)factor_kernel<2, 1>, h->sm_count, kFactorDynSmem),
-                        coop_grid((const void *)solve_kernel, h->sm_count),
                         coop_grid((const void *)solve_df_kernel, h->sm_count),
                         coop_grid((const void *)solve_dfm_kernel, h->sm_count)});
     if (h->grid <= 0) { glu::set_error("persistent kernel cannot be co-resident"); return fail(GLU_ECUDA); }
@@ -2297,7 +2128,7 @@ extern "C" void glu_destroy(glu_handle *h) {
     void *ptrs[] = {h->col_ptr, h->row_idx, h->diag_pos, h->level_of, h->level_need, h->col_total, h->cdeps, h->sync, h->tail_g, h->fail_batch, h->items,
                     h->chunks, h->map8, h->tgt16, h->deep, h->l_lvl_ptr, h->l_rows, h->l_ptr, h->l_col, h->l_slot,
                     h->u_lvl_ptr, h->u_rows, h->u_ptr, h->u_col, h->u_slot, h->a_slot, h->fail,
-                    h->bar, h->ifail, h->err_acc, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->l_split, h->solve_part, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
+                    h->ifail, h->err_acc, h->tail_trace, h->tail_mk, h->tail_blk, h->tail_umax, h->solve_y, h->solve_yi, h->solve_zi, h->tasks_l, h->tasks_u, h->l_rows_nt, h->u_rows_nt, h->l_split, h->solve_part, h->sctl, h->level_ns, h->trace, h->d_a, h->d_v, h->d_x, h->d_ab, h->d_vb};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     glu::sn_free(h->sn);
@@ -2336,9 +2167,6 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             }
             return GLU_OK;
         }
-        case 5:  // tuning: L2-prefetch the next item's plan data for items of phases < value (0 = off)
-            h->prefetch = (int)std::max<int64_t>(0, std::min<int64_t>(value, INT32_MAX));
-            return GLU_OK;
         case 6:  // tuning: nanoseconds between dependency polls
             h->poll_ns = (int)std::max<int64_t>(0, std::min<int64_t>(value, 100000));
             return GLU_OK;
@@ -2351,8 +2179,11 @@ extern "C" int64_t glu_set_option(glu_handle *h, int64_t key, int64_t value) {
             for (auto &e : h->kev) GLU_CUDA(cudaEventCreate(&e));
             return GLU_OK;
         }
-        case 9:  // solves: 0 dataflow (default), 1 level-synchronous
-            h->solve_mode = value != 0 ? 1 : 0;
+        case 9:  // solves: 0 dataflow (the only solve kernel; the level-synchronous one was removed)
+            if (value != 0) {
+                glu::set_error("option 9: the level-synchronous solve kernel was removed (dataflow only)");
+                return GLU_EINVAL;
+            }
             return GLU_OK;
         case 11:  // tuning: k > 1 right-hand sides, 1 lanes over right-hand sides, 0 one warp each
             h->solve_multi = value != 0;
@@ -2522,8 +2353,6 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.level_need = h->level_need;
     P.n = (i32)h->n;
     P.n_items = (i32)h->n_items;
-    P.n_express = (i32)h->n_express;
-    P.express_R = (i32)std::min<i64>(h->express_R, h->grid - 1);
     P.n_levels = (i32)h->n_levels;
     P.n_div = (i32)h->tail_t0;
     P.nb = nb;
@@ -2540,7 +2369,6 @@ static int64_t launch_factor(glu_handle *h, double *v, double thresh, cudaStream
     P.fail_by_column = h->fail_by_column ? 1 : 0;
     P.trace = nullptr;
     P.trace_i0 = P.trace_i1 = 0;
-    P.prefetch = h->prefetch;
     P.poll_ns = h->poll_ns;
     if (h->trace_nl > 0 && h->trace) {
         P.trace = h->trace;
@@ -2750,29 +2578,6 @@ extern "C" int64_t glu_factor_batch_host(glu_handle *h, int64_t batch, const dou
     return batch_status(h, batch, fail_cols, s);
 }
 
-static int64_t launch_solve_level(glu_handle *h, const double *lu, double *x, bool upper,
-                                  cudaStream_t s, int nrhs, i64 ldx) {
-    SolveParams S;
-    S.v = lu;
-    S.x = x;
-    S.upper = upper ? 1 : 0;
-    S.lvl_ptr = upper ? h->u_lvl_ptr : h->l_lvl_ptr;
-    S.rows = upper ? h->u_rows : h->l_rows;
-    S.ent_ptr = upper ? h->u_ptr : h->l_ptr;
-    S.ent_col = upper ? h->u_col : h->l_col;
-    S.ent_slot = upper ? h->u_slot : h->l_slot;
-    S.diag_pos = h->diag_pos;
-    S.n_levels = (i32)(upper ? h->u_levels : h->l_levels);
-    S.bar = h->bar;
-    S.nrhs = nrhs;
-    S.ldx = ldx;
-    GLU_CUDA(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int), s));
-    void *args[] = {&S};
-    GLU_CUDA(cudaLaunchCooperativeKernel((const void *)solve_kernel, dim3(h->grid), dim3(kThreads),
-                                         args, 0, s));
-    return GLU_OK;
-}
-
 // y scratch of the dataflow solves, all-sentinel between calls
 static int64_t ensure_solve_y(glu_handle *h, int nrhs, cudaStream_t s) {
     const i64 need = std::max<i64>(h->n, 1) * nrhs;
@@ -2919,15 +2724,7 @@ static int64_t run_solves(glu_handle *h, const double *lu, double *x, int part, 
                           int nrhs = 1, i64 ldx = 0, i64 v_stride = 0) {
     if (ldx <= 0) ldx = h->n;
     i64 rc;
-    if (v_stride != 0 && h->solve_mode == 1) {
-        glu::set_error("batch solves need the dataflow solve kernel (option 9 = 0)");
-        return GLU_EINVAL;
-    }
-    if (h->solve_mode == 1 || h->n == 0) {
-        if (part != 2 && (rc = launch_solve_level(h, lu, x, false, s, nrhs, ldx)) != GLU_OK) return rc;
-        if (part != 1 && (rc = launch_solve_level(h, lu, x, true, s, nrhs, ldx)) != GLU_OK) return rc;
-        return GLU_OK;
-    }
+    if (h->n == 0) return GLU_OK;
     const int mg = h->sm_count * 4;
     GLU_CUDA(cudaMemsetAsync(h->sctl + 1, 0, sizeof(unsigned), s));
     if (nrhs > 1 && h->solve_multi && v_stride == 0) {

@@ -691,7 +691,6 @@ struct glu_plan {
     std::vector<i32> col_total;
     std::vector<glu::ColDep> cdeps;  // per item: destination columns and their earlier-phase counts
     i64 tail_t0 = 0, tail_macs = 0;
-    i64 n_express = 0, express_R = 0;  // express queue: items [0, n_express) on the first express_R SMs
     i64 max_item_macs = 0;
     i64 max_push_macs = 0;
     i64 max_chunks = 0;
@@ -1023,38 +1022,10 @@ extern "C" int64_t glu_plan_build(int64_t n, const int64_t *col_ptr, const int64
             pend_k[k]++;
         }
     }
-    // Express queue: in thin phases, the items into columns that are sources
-    // within the next K phases (the critical chain and the items one or two
-    // hops behind it) go to a separate list that the kernel deals to a few
-    // reserved SMs.  A release fence waits behind every memory request its SM
-    // has in flight, so the critical chain fences on quiet SMs while the bulk
-    // of each phase runs on the others.
-    i64 express_R = 0, express_K = 3, express_max = 3000;  // off unless GLU_EXPRESS_R is set
-    if (const char *e = std::getenv("GLU_EXPRESS_R")) express_R = std::atoll(e);
-    if (const char *e = std::getenv("GLU_EXPRESS_K")) express_K = std::atoll(e);
-    if (const char *e = std::getenv("GLU_EXPRESS_MAX")) express_max = std::atoll(e);
-    i64 n_express = 0;
-    if (express_R > 0) {
-        std::vector<i64> per_phase(n_levels, 0);
-        for (auto &r : refs) per_phase[r.lvl]++;
-        auto is_express = [&](const Ref &r) {
-            const LocalItem &x = outs[r.tid].items[r.idx];
-            return x.kind == glu::kPush && per_phase[x.lvl] <= express_max &&
-                   level_of[x.k] - x.lvl <= express_K;
-        };
-        std::stable_partition(refs.begin(), refs.end(), is_express);
-        for (auto &r : refs) {
-            if (!is_express(r)) break;
-            n_express++;
-        }
-        if (n_express == 0) express_R = 0;
-    }
     auto *plan = new glu_plan();
     plan->n_levels = n_levels;
     plan->tail_t0 = t0;
     plan->tail_macs = tail_macs;
-    plan->n_express = n_express;
-    plan->express_R = express_R;
     plan->level_item_ptr.assign(n_levels + 1, 0);
     plan->items.reserve(refs.size());
     plan->chunks.reserve(total_chunks);
@@ -1124,15 +1095,15 @@ extern "C" void glu_plan_info(const glu_plan *p, int64_t *info) {
     info[12] = (i64)p->tgt16.size();
     info[13] = p->tail_t0;
     info[14] = p->tail_macs;
-    info[15] = p->n_express;
+    info[15] = 0;  // reserved (was the express-queue item count)
 }
 
 extern "C" void glu_plan_export(const glu_plan *p, int64_t *level_item_ptr, int64_t *items,
                                 int64_t *chunks, int64_t *deep, uint8_t *map8, int64_t *tgt) {
     if (level_item_ptr)
         std::memcpy(level_item_ptr, p->level_item_ptr.data(), p->level_item_ptr.size() * sizeof(i64));
-    // items in phase order (the express queue sits in front of the device
-    // array); level_item_ptr indexes this order
+    // items in phase order (the device array's order); level_item_ptr
+    // indexes this order
     std::vector<i64> order(p->items.size());
     for (size_t i = 0; i < order.size(); i++) order[i] = (i64)i;
     std::stable_sort(order.begin(), order.end(), [&](i64 x, i64 y) {
@@ -1252,11 +1223,9 @@ const glu_plan_view plan_view(const glu_plan *p) {
     v.n_tgt = (i64)p->tgt16.size();
     v.col_total = p->col_total.data();
     v.tail_t0 = p->tail_t0;
-    v.n_express = p->n_express;
     v.cdeps = p->cdeps.data();
     v.max_push_macs = p->max_push_macs;
     v.n_cdeps = (i64)p->cdeps.size();
-    v.express_R = p->express_R;
     v.sn = p->sn.get();
     return v;
 }

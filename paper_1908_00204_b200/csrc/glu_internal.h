@@ -141,11 +141,9 @@ struct glu_plan_view {
     int64_t n_tgt;
     const int32_t *col_total;  // per column: items into it (all phases)
     int64_t tail_t0;           // columns >= tail_t0: dense cluster tail (n: none)
-    int64_t n_express;         // items [0, n_express): express queue
     const ColDep *cdeps;
     int64_t n_cdeps;
     int64_t max_push_macs;     // largest push item (selects the kernel variant)
-    int64_t express_R;         // SMs reserved for the express queue
     const SnPlan *sn;          // supernodal engine (no items above), or null
 };
 

@@ -161,7 +161,7 @@ class Factorizer:
             self.plan_info = dict(zip(("levels", "items", "chunks", "macs", "max_item_macs",
                                        "max_chunks", "deferred_macs", "plan_bytes", "deep_items",
                                        "deep_macs", "epochs", "push_macs", "targets", "tail_t0",
-                                       "tail_macs", "express_items"),
+                                       "tail_macs", "reserved"),
                                       info.tolist()))
             if engine == "sn":
                 sinfo = np.zeros(16, dtype=np.int64)
@@ -186,8 +186,6 @@ class Factorizer:
         self._lock = threading.Lock()
         if "GLU_POLL_NS" in os.environ:  # tuning: ns between dependency polls (option 6)
             self.set_option(6, int(os.environ["GLU_POLL_NS"]))
-        if "GLU_PREFETCH_PHASES" in os.environ:  # tuning: L2-prefetch plan data of the first phases (option 5)
-            self.set_option(5, int(os.environ["GLU_PREFETCH_PHASES"]))
         info = np.zeros(12, dtype=np.int64)
         _lib.lib.glu_handle_info(h, _lib.ptr(info))
         self.handle_info = dict(zip(("n", "nnz", "levels", "items", "chunks", "macs",

@@ -249,36 +249,35 @@ def _solve_factorizer(lu):
     return glu.get_factorizer(lu.pattern, glu.numeric._relaxed_levels(lu.pattern), 0)
 
 
-@pytest.mark.parametrize("mode", [0, 1])  # 0 dataflow (default), 1 level-synchronous
-def test_solve_modes_interleaved_bitwise(mode):
-    """Both solve kernels, every entry point, interleaved in an order that
-    exercises the dataflow solve's sentinel buffer hand-over (L-only leaves
-    it via a move, U-only enters it via one)."""
+def test_solve_entry_points_interleaved_bitwise():
+    """Every solve entry point, interleaved in an order that exercises the
+    dataflow solve's sentinel buffer hand-over (L-only leaves it via a move,
+    U-only enters it via one); the removed level-synchronous kernel's option
+    is refused."""
     from paper_1908_00204_b200 import synthetic
 
     a = synthetic.make("cfg1")
     fp, s, plans = _analyze(a)
     lu, _ = glu.factor_parallel(a, fp, s, plans, glu.FactorOptions())
     fz = _solve_factorizer(lu)
-    fz.set_option(9, mode)
-    try:
-        pat = orc.Pattern.from_fp(fp)
-        rng = np.random.default_rng(11)
-        for step in range(3):
-            b = rng.standard_normal(a.n)
-            b[rng.integers(0, a.n, 50)] = 0.0
-            yr = orc.lower_solve(pat, lu.values, b)
-            xr, bad = orc.upper_solve(pat, lu.values, yr)
-            assert bad == -1
-            assert np.array_equal(glu.lower_solve(lu, b), yr), step
-            assert np.array_equal(glu.solve(lu, b), xr), step
-            assert np.array_equal(glu.upper_solve(lu, yr), xr), step
-            B = np.stack([b, -b, np.zeros(a.n)], axis=1)
-            X = glu.solve_many(lu, B)
-            assert np.array_equal(X[:, 0], xr) and np.array_equal(X[:, 1], glu.solve(lu, -b))
-            assert not X[:, 2].any()
-    finally:
-        fz.set_option(9, 0)
+    with pytest.raises(glu.numeric._lib.GluError):
+        fz.set_option(9, 1)
+    fz.set_option(9, 0)
+    pat = orc.Pattern.from_fp(fp)
+    rng = np.random.default_rng(11)
+    for step in range(3):
+        b = rng.standard_normal(a.n)
+        b[rng.integers(0, a.n, 50)] = 0.0
+        yr = orc.lower_solve(pat, lu.values, b)
+        xr, bad = orc.upper_solve(pat, lu.values, yr)
+        assert bad == -1
+        assert np.array_equal(glu.lower_solve(lu, b), yr), step
+        assert np.array_equal(glu.solve(lu, b), xr), step
+        assert np.array_equal(glu.upper_solve(lu, yr), xr), step
+        B = np.stack([b, -b, np.zeros(a.n)], axis=1)
+        X = glu.solve_many(lu, B)
+        assert np.array_equal(X[:, 0], xr) and np.array_equal(X[:, 1], glu.solve(lu, -b))
+        assert not X[:, 2].any()
 
 
 def test_solve_rhs_carrying_the_sentinel_pattern():
@@ -407,8 +406,7 @@ def test_pivot_breakdown_inside_cfg1_matches_oracle(det):
         assert e.value.column == want_seq
 
 
-@pytest.mark.parametrize("check_refusal", [False, True])
-def test_solve_batch_per_set_bitwise(check_refusal):
+def test_solve_batch_per_set_bitwise():
     """refactorize_batch -> solve_batch (the Newton-loop pair): every set's
     solution is bitwise the oracle's solve with that set's factors; a set
     with an exactly zero diagonal reports the column upper_solve raises."""
@@ -426,14 +424,6 @@ def test_solve_batch_per_set_bitwise(check_refusal):
     L[4, fp.diag_pos[bad_col]] = 0.0  # set 4: a zero diagonal
     B = np.random.default_rng(9).standard_normal((nb, a.n))
     B[2] = 0.0
-    if check_refusal:  # the level-synchronous kernel has no per-set factors: refused
-        fz = glu.get_factorizer(lu.pattern, glu.numeric._relaxed_levels(lu.pattern), 0)
-        fz.set_option(9, 1)
-        try:
-            with pytest.raises(Exception):
-                glu.solve_batch(lu, L, B)
-        finally:
-            fz.set_option(9, 0)
     X, status = glu.solve_batch(lu, L, B)
     pat = orc.Pattern.from_fp(fp)
     for k in range(nb):

@@ -22,8 +22,6 @@ st = torch.cuda.current_stream()
 fz.set_option(1, 0)
 if "GLU_POLL" in os.environ:
     fz.set_option(6, int(os.environ["GLU_POLL"]))
-if "GLU_PREFETCH" in os.environ:
-    fz.set_option(5, int(os.environ["GLU_PREFETCH"]))
 for _ in range(3):
     fz.scatter_device(ad, v, st); fz.factor_device(v, 1e-14, st)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

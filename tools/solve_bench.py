@@ -14,8 +14,6 @@ fp = glu.symbolic_fillin(a.pattern)
 s = glu.levelize(glu.detect_relaxed(fp))
 fz = glu.get_factorizer(fp, s.level_of, 0)
 fz.set_input(a.col_ptr, a.row_idx)
-mode = int(os.environ.get("GLU_SOLVE_MODE", "0"))  # 0 dataflow, 1 level-synchronous
-fz.set_option(9, mode)
 tblock = int(os.environ.get("GLU_SOLVE_TBLOCK", "-1"))
 if tblock >= 0:
     fz.set_option(10, tblock)
@@ -31,7 +29,7 @@ assert rc == -1
 dev = torch.device("cuda", 0)
 lu_d = torch.from_numpy(lu).to(dev)
 st = torch.cuda.current_stream()
-out = {"config": cfg, "solve_mode": ["dataflow", "level-synchronous"][mode], "tblock": tblock, "multi": multi, "tail_cta": stail, "long_row": long_row, "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
+out = {"config": cfg, "tblock": tblock, "multi": multi, "tail_cta": stail, "long_row": long_row, "n": a.n, "lsolve_levels": fz.handle_info["lsolve_levels"],
        "usolve_levels": fz.handle_info["usolve_levels"]}
 for k in (1, 8, 32):
     x = torch.randn((k, a.n), dtype=torch.float64, device=dev)
