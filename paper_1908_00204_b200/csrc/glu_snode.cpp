@@ -320,7 +320,8 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
     }
     P->n_dblk = dbl;
     // latency model (us), calibrated on the B200 traces (tools/sn_critpath.py)
-    constexpr double kHop = 2.5;                 // release -> observe
+    // (GLU_SN_HOP: tuning override of the hand-off latency, order only)
+    const double kHop = std::getenv("GLU_SN_HOP") ? std::max(0.1, std::atof(std::getenv("GLU_SN_HOP"))) : 2.5;  // release -> observe
     constexpr double kMacsPerUs = 4000.0;        // one warp's FP64 chain rate
     constexpr double kGatherSrcUs = 0.15;        // one push inside an RG (shared-memory chains)
     constexpr double kGatherUs = 3.0;            // an RG's staging loads
