@@ -326,7 +326,9 @@ int64_t sn_build(int64_t n, const int64_t *col_ptr, const int64_t *row_idx, cons
     constexpr double kGatherSrcUs = 0.15;        // one push inside an RG (shared-memory chains)
     constexpr double kGatherUs = 3.0;            // an RG's staging loads
     constexpr i64 kMaxGather = kRgPushes;        // pushes per RG task (one per lane)
-    constexpr i64 kMinGather = 3;                // shorter runs stay RECT tasks (their slots load before the waits)
+    // runs shorter than this stay RECT tasks; 1 (every eligible run an RG task) measured best:
+    // cfg4 48.5 vs 48.8 ms (3), g400 7.54 vs 7.74, g800 19.8 vs 20.3 (GLU_SN_MINGATHER: tuning override)
+    const i64 kMinGather = std::getenv("GLU_SN_MINGATHER") ? std::max<i64>(1, std::atoll(std::getenv("GLU_SN_MINGATHER"))) : 1;
     std::vector<double> f_done(np, 0.0), f_start(np, 0.0);
     struct T {
         double start, cost;
